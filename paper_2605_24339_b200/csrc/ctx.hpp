@@ -1,0 +1,108 @@
+// Device context behind gmcp_ctx (include/gmcp_b200.h).
+#pragma once
+
+#include "common.cuh"
+
+namespace gmcp_b200 {
+
+struct DevSurface {
+  int32_t n_tris = 0, n_edges = 0, n_verts = 0;
+  DBuf<int32_t> tris, edges, tri_edges, verts;
+  std::vector<int32_t> h_tris, h_edges, h_tri_edges, h_verts;  // host mirror (setup only)
+};
+
+// Contact-Hessian assembly plan, rebuilt whenever the sample set changes.
+// Level 1 (K7, one warp per slave run) reduces each run of samples sharing a
+// slave triangle into a compact partial; level 2 (K8, one warp per vertex
+// row) gathers the partials of the runs touching that vertex into its BCSR
+// row and gradient. Both levels sum in a fixed order: bitwise deterministic.
+struct AssemblyPlan {
+  int64_t n_runs = 0;
+  DBuf<int64_t> run_off;     // [R+1] sample range of each run
+  DBuf<int32_t> run_slave;   // [R][3]
+  DBuf<int32_t> lm_off;      // [R+1] local master vertex table offsets
+  DBuf<int32_t> lm_ids;      // global ids, ascending within a run
+  DBuf<int32_t> lp_off;      // [R+1] local master pair table offsets
+  DBuf<int32_t> lp;          // packed (a << 16 | b), local indices, a <= b
+  DBuf<int64_t> pbase;       // [R] partial base offset (doubles)
+  int64_t partial_len = 0;
+  DBuf<double> partial;
+  // BCSR pattern over all N vertex rows
+  int32_t n_rows = 0;
+  int64_t nnzb = 0;
+  DBuf<int32_t> rowptr;      // [N+1]
+  DBuf<int32_t> cols;        // [nnzb]
+  DBuf<double> vals;         // [nnzb][9]
+  DBuf<int32_t> row_ent_off; // [N+1]
+  DBuf<int64_t> row_ent;     // (run << 20) | role ; role < 3 slave i, else 3 + local master
+  bool valid = false;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int64_t n_dof = 0;
+  gmcp_barrier_params params{};
+  bool have_params = false;
+
+  DevSurface slave, master;
+  DBuf<double> x, dx, grad, eps_ref;
+
+  // candidate pairs (CSR per slave tri)
+  DBuf<int64_t> pair_off[3];
+  DBuf<int32_t> pair_ids[3];
+  bool have_pairs = false;
+
+  // samples
+  int64_t ns = 0;
+  DBuf<int8_t> s_type;
+  DBuf<int32_t> s_slave, s_master;
+  DBuf<double> s_beta_s, s_beta_m, s_wm, s_eta, s_weight, s_gamma, s_eps, s_gref, s_coef;
+  DBuf<int64_t> face_idx;  // indices of face samples (pressure field order)
+
+  AssemblyPlan plan;
+
+  // reduction scratch
+  DBuf<double> red_d;
+  DBuf<unsigned long long> red_u;
+
+  DevSamples samples() const {
+    DevSamples d;
+    d.n = ns;
+    d.type = s_type.p;
+    d.slave = s_slave.p;
+    d.master = s_master.p;
+    d.beta_s = s_beta_s.p;
+    d.wm = s_wm.p;
+    d.coef = s_coef.p;
+    d.eps = s_eps.p;
+    d.gamma = s_gamma.p;
+    return d;
+  }
+  int64_t n_vertices() const { return n_dof / 3; }
+  void sync() { GMCP_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+// --- entry points implemented in the .cu files (all enqueue on ctx.stream) ---
+// contact_eval.cu
+void derive_sample_fields(Ctx& c);  // coef, wm, face_idx from the raw fields
+struct EnergyOut {
+  double energy, min_gap, min_gap_prefix;
+  int64_t first_bad, first_degenerate;
+};
+EnergyOut run_energy(Ctx& c, bool need_prefix_min);
+void build_assembly_plan(Ctx& c);  // host-side plan from the device samples
+// mode 0: gradient only, 1: gradient + Hessian. Returns energy; throws on infeasible.
+double run_assembly(Ctx& c, int mode, int64_t* bad);
+void run_pressure(Ctx& c, gmcp_pressure_record* out_host);
+void run_force_summary(Ctx& c, double* out12);
+void run_kinematics(Ctx& c, double* g, int32_t* nv, int32_t* ids, double* dg);
+void time_assembly(Ctx& c, int reps, int flush_l2, double* ms_pass, double* ms_kernel);
+// exact.cu (-fmad=false)
+double run_step_filter(Ctx& c);
+double run_displacement_cap(Ctx& c);
+void run_broadphase(Ctx& c, double r, int64_t* counts);
+int64_t run_sampler(Ctx& c, const double* eps_ref_dev);
+
+}  // namespace gmcp_b200

@@ -1,0 +1,1034 @@
+// Broadphase (K1-K3) and mortar sampler (K4-K5), bit-exact with the reference.
+// Compiled with -fmad=false: every floating-point operation below is a plain
+// IEEE op in the reference's order, so candidate sets and samples are
+// bitwise equal to build_candidate_pairs / build_contact_state.
+//
+//  K1 lbvh_build   Morton codes of master-triangle AABB centroids, CUB radix
+//                  sort, Karras (2012) hierarchy, bottom-up AABB refit.
+//  K2 lbvh_query   one thread per slave triangle, stack traversal with the
+//                  inflated query box; count pass -> scan -> emit pass, then a
+//                  per-triangle sort (the reference sorts, so traversal order
+//                  is irrelevant).                  contact_sampling.hpp:296-326
+//  K3 features     per slave triangle sorted-unique candidate edges / vertex
+//                  features.                        contact_sampling.hpp:328-337
+//  K4 point_owner  master vertex -> owning slave triangles (interior: all,
+//                  else the first boundary one).     contact_sampling.hpp:403-436
+//  K5 sample       one thread per (slave tri, feature) task in reference
+//                  order: clip / quadrature / freeze; count -> scan -> emit.
+//                                                    contact_sampling.hpp:97-215,438-485
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "ctx.hpp"
+#include "kin.cuh"
+
+namespace gmcp_b200 {
+
+namespace {
+
+constexpr double kDblMax = 1.7976931348623157e308;
+
+// ---------------------------------------------------------------------------
+// scan / sort helpers (CUB, temp storage owned here)
+
+struct Scratch {
+  DBuf<unsigned char> tmp;
+  void* get(size_t bytes) {
+    tmp.resize(std::max<size_t>(bytes, 1));
+    return tmp.p;
+  }
+};
+Scratch g_scratch;
+
+template <class T>
+void exclusive_scan(const T* in, T* out, int64_t n, cudaStream_t s) {
+  size_t bytes = 0;
+  GMCP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+  void* t = g_scratch.get(bytes);
+  GMCP_CUDA(cub::DeviceScan::ExclusiveSum(t, bytes, in, out, n, s));
+}
+
+template <class K, class V>
+void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, int64_t n, cudaStream_t s, int end_bit) {
+  size_t bytes = 0;
+  GMCP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, n, 0, end_bit, s));
+  void* t = g_scratch.get(bytes);
+  GMCP_CUDA(cub::DeviceRadixSort::SortPairs(t, bytes, kin, kout, vin, vout, n, 0, end_bit, s));
+}
+
+template <class K>
+void sort_keys(const K* kin, K* kout, int64_t n, cudaStream_t s, int end_bit) {
+  size_t bytes = 0;
+  GMCP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kin, kout, n, 0, end_bit, s));
+  void* t = g_scratch.get(bytes);
+  GMCP_CUDA(cub::DeviceRadixSort::SortKeys(t, bytes, kin, kout, n, 0, end_bit, s));
+}
+
+int grid_for(int64_t n, int threads) {
+  const int64_t b = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 64));
+}
+
+#define GRID_LOOP(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------------------
+// K1: LBVH over master triangle boxes
+
+struct Box {
+  double lo[3], hi[3];
+};
+
+__device__ __forceinline__ Box tri_box(const double* __restrict__ x, const int32_t* t) {
+  Box b;
+  for (int k = 0; k < 3; ++k) {
+    b.lo[k] = kDblMax;
+    b.hi[k] = -kDblMax;
+  }
+  for (int i = 0; i < 3; ++i) {
+    const d3 p = ld3(x, t[i]);
+    const double v[3] = {p.x, p.y, p.z};
+    for (int k = 0; k < 3; ++k) {
+      b.lo[k] = dmin(b.lo[k], v[k]);
+      b.hi[k] = dmax(b.hi[k], v[k]);
+    }
+  }
+  return b;
+}
+
+__device__ __forceinline__ bool overlaps(const Box& a, const Box& b) {  // core.hpp:71-73
+  for (int k = 0; k < 3; ++k)
+    if (!(a.lo[k] <= b.hi[k]) || !(b.lo[k] <= a.hi[k])) return false;
+  return true;
+}
+
+__global__ void k_master_boxes(int32_t n, const int32_t* __restrict__ tris, const double* __restrict__ x,
+                               Box* __restrict__ boxes, unsigned long long* bounds) {
+  unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+  GRID_LOOP(t, n) {
+    const Box b = tri_box(x, tris + 3 * t);
+    boxes[t] = b;
+    for (int k = 0; k < 3; ++k) {
+      const double c = 0.5 * (b.lo[k] + b.hi[k]);
+      const unsigned long long o = ord_bits(c);
+      lo[k] = o < lo[k] ? o : lo[k];
+      hi[k] = o > hi[k] ? o : hi[k];
+    }
+  }
+  for (int k = 0; k < 3; ++k) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[k] = min(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = max(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&bounds[k], lo[k]);
+      atomicMax(&bounds[3 + k], hi[k]);
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned int expand_bits(unsigned int v) {
+  v = (v * 0x00010001u) & 0xFF0000FFu;
+  v = (v * 0x00000101u) & 0x0F00F00Fu;
+  v = (v * 0x00000011u) & 0xC30C30C3u;
+  v = (v * 0x00000005u) & 0x49249249u;
+  return v;
+}
+
+__global__ void k_morton(int32_t n, const Box* __restrict__ boxes, const unsigned long long* __restrict__ bounds,
+                         unsigned long long* __restrict__ keys, int32_t* __restrict__ idx) {
+  double lo[3], ext[3];
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = from_ord_bits(bounds[k]);
+    const double h = from_ord_bits(bounds[3 + k]);
+    ext[k] = h - lo[k] > 0 ? h - lo[k] : 1.0;
+  }
+  GRID_LOOP(t, n) {
+    unsigned int q[3];
+    for (int k = 0; k < 3; ++k) {
+      const double c = 0.5 * (boxes[t].lo[k] + boxes[t].hi[k]);
+      double u = (c - lo[k]) / ext[k];
+      u = u < 0 ? 0 : (u > 1 ? 1 : u);
+      q[k] = (unsigned int)(u * 1023.0);
+    }
+    const unsigned long long m = (expand_bits(q[0]) << 2) | (expand_bits(q[1]) << 1) | expand_bits(q[2]);
+    keys[t] = (m << 32) | (unsigned int)t;  // unique keys: index breaks ties
+    idx[t] = (int32_t)t;
+  }
+}
+
+__device__ __forceinline__ int delta(const unsigned long long* k, int n, int i, int j) {
+  if (j < 0 || j >= n) return -1;
+  return __clzll(k[i] ^ k[j]);
+}
+
+// Karras 2012: internal nodes 0..n-2, leaves n-1..2n-2.
+__global__ void k_karras(int n, const unsigned long long* __restrict__ k, int32_t* __restrict__ left,
+                         int32_t* __restrict__ right, int32_t* __restrict__ parent) {
+  GRID_LOOP(ii, n - 1) {
+    const int i = (int)ii;
+    const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
+    const int dmin_ = delta(k, n, i, i - d);
+    int lmax = 2;
+    while (delta(k, n, i, i + lmax * d) > dmin_) lmax *= 2;
+    int l = 0;
+    for (int t = lmax / 2; t >= 1; t /= 2)
+      if (delta(k, n, i, i + (l + t) * d) > dmin_) l += t;
+    const int j = i + l * d;
+    const int dnode = delta(k, n, i, j);
+    int s = 0;
+    for (int div = 2;; div *= 2) {
+      const int t = (l + div - 1) / div;
+      if (delta(k, n, i, i + (s + t) * d) > dnode) s += t;
+      if (t == 1) break;
+    }
+    const int gamma = i + s * d + min(d, 0);
+    const int lo = min(i, j), hi = max(i, j);
+    const int L = (lo == gamma) ? (n - 1 + gamma) : gamma;
+    const int R = (hi == gamma + 1) ? (n - 1 + gamma + 1) : gamma + 1;
+    left[i] = L;
+    right[i] = R;
+    parent[L] = i;
+    parent[R] = i;
+  }
+}
+
+__device__ __forceinline__ Box ldcg_box(const Box* b) {  // L2 view: written by other SMs
+  Box r;
+  const double* p = reinterpret_cast<const double*>(b);
+  for (int k = 0; k < 3; ++k) {
+    r.lo[k] = __ldcg(p + k);
+    r.hi[k] = __ldcg(p + 3 + k);
+  }
+  return r;
+}
+
+__global__ void k_refit(int n, const int32_t* __restrict__ sorted_idx, const Box* __restrict__ tri_boxes,
+                        const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+                        const int32_t* __restrict__ parent, Box* nodes, int32_t* flags) {
+  GRID_LOOP(t, n) {
+    int node = n - 1 + (int)t;
+    nodes[node] = tri_boxes[sorted_idx[t]];
+    if (n == 1) continue;
+    __threadfence();
+    int p = parent[node];
+    while (p >= 0) {
+      if (atomicAdd(&flags[p], 1) == 0) break;  // first arrival: sibling not ready
+      __threadfence();
+      const Box a = ldcg_box(nodes + __ldcg(left + p)), b = ldcg_box(nodes + __ldcg(right + p));
+      Box u;
+      for (int k2 = 0; k2 < 3; ++k2) {
+        u.lo[k2] = dmin(a.lo[k2], b.lo[k2]);
+        u.hi[k2] = dmax(a.hi[k2], b.hi[k2]);
+      }
+      nodes[p] = u;
+      __threadfence();
+      p = p == 0 ? -1 : parent[p];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: queries. mode 0 counts, mode 1 emits + sorts per slave tri.
+
+__device__ __forceinline__ void isort(int32_t* a, int n) {
+  for (int i = 1; i < n; ++i) {
+    const int32_t v = a[i];
+    int j = i - 1;
+    while (j >= 0 && a[j] > v) {
+      a[j + 1] = a[j];
+      --j;
+    }
+    a[j + 1] = v;
+  }
+}
+__device__ __forceinline__ int sort_unique(int32_t* a, int n) {
+  isort(a, n);
+  if (n == 0) return 0;
+  int k = 1;
+  for (int i = 1; i < n; ++i)
+    if (a[i] != a[k - 1]) a[k++] = a[i];
+  return k;
+}
+
+template <int Mode>
+__global__ void k_query(int32_t nst, const int32_t* __restrict__ stris, const double* __restrict__ x, double r,
+                        int n_leaf, const Box* __restrict__ nodes, const int32_t* __restrict__ left,
+                        const int32_t* __restrict__ right, const int32_t* __restrict__ sorted_idx,
+                        int64_t* __restrict__ cnt, const int64_t* __restrict__ off, int32_t* __restrict__ out,
+                        int* overflow) {
+  GRID_LOOP(st, nst) {
+    Box q = tri_box(x, stris + 3 * st);
+    for (int k = 0; k < 3; ++k) {  // Aabb::inflated, core.hpp:77-82
+      q.lo[k] = q.lo[k] - r;
+      q.hi[k] = q.hi[k] + r;
+    }
+    int stack[64];
+    int top = 0;
+    stack[top++] = n_leaf == 1 ? 0 : 0;
+    int64_t c = 0;
+    const int64_t base = Mode ? off[st] : 0;
+    while (top > 0) {
+      const int node = stack[--top];
+      if (!overlaps(nodes[node], q)) continue;
+      if (node >= n_leaf - 1) {
+        if (Mode) out[base + c] = sorted_idx[node - (n_leaf - 1)];
+        ++c;
+      } else {
+        if (top + 2 > 64) {
+          atomicExch(overflow, 1);
+          break;
+        }
+        stack[top++] = right[node];
+        stack[top++] = left[node];
+      }
+    }
+    if (Mode) isort(out + base, (int)c);
+    else cnt[st] = c;
+  }
+}
+
+// K3: candidate edges / vertex features per slave tri (sorted unique).
+// Writes into tmp at 3*tri_off[st] and the unique counts.
+__global__ void k_features(int32_t nst, const int64_t* __restrict__ tri_off, const int32_t* __restrict__ tri_ids,
+                           const int32_t* __restrict__ mtris, const int32_t* __restrict__ mtri_edges,
+                           const int32_t* __restrict__ mverts, int32_t n_mverts, int32_t* __restrict__ tmp_e,
+                           int32_t* __restrict__ tmp_v, int64_t* __restrict__ ecnt, int64_t* __restrict__ vcnt) {
+  GRID_LOOP(st, nst) {
+    const int64_t a = tri_off[st], b = tri_off[st + 1];
+    int32_t* E = tmp_e + 3 * a;
+    int32_t* V = tmp_v + 3 * a;
+    int k = 0;
+    for (int64_t i = a; i < b; ++i) {
+      const int mt = tri_ids[i];
+      for (int e = 0; e < 3; ++e) {
+        E[k] = mtri_edges[3 * mt + e];
+        const int gv = mtris[3 * mt + e];
+        int lo = 0, hi = n_mverts;  // lower_bound into master.verts
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (mverts[mid] < gv) lo = mid + 1; else hi = mid;
+        }
+        V[k] = lo;
+        ++k;
+      }
+    }
+    ecnt[st] = sort_unique(E, k);
+    vcnt[st] = sort_unique(V, k);
+  }
+}
+
+__global__ void k_compact(int32_t nst, const int64_t* __restrict__ tri_off, const int32_t* __restrict__ tmp,
+                          const int64_t* __restrict__ off, int32_t* __restrict__ out) {
+  GRID_LOOP(st, nst) {
+    const int32_t* src = tmp + 3 * tri_off[st];
+    for (int64_t i = off[st]; i < off[st + 1]; ++i) out[i] = src[i - off[st]];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// geometry (reference op order; this TU has no FMA contraction)
+
+struct Frame {
+  d3 origin, t1, t2, n;
+};
+
+// geometry.hpp:14-21
+__device__ __forceinline__ bool triangle_normal(d3 a, d3 b, d3 c, d3& n) {
+  const d3 cr = cross(b - a, c - a);
+  const d3 lo = mk3(dmin(dmin(dmin(kDblMax, a.x), b.x), c.x), dmin(dmin(dmin(kDblMax, a.y), b.y), c.y),
+                    dmin(dmin(dmin(kDblMax, a.z), b.z), c.z));
+  const d3 hi = mk3(dmax(dmax(dmax(-kDblMax, a.x), b.x), c.x), dmax(dmax(dmax(-kDblMax, a.y), b.y), c.y),
+                    dmax(dmax(dmax(-kDblMax, a.z), b.z), c.z));
+  const double diag2 = norm(hi - lo);
+  const double area_eps = 1e-12 * diag2 * diag2;
+  if (0.5 * norm(cr) <= area_eps) return false;
+  n = unit(cr);
+  return true;
+}
+// geometry.hpp:127-134
+__device__ __forceinline__ bool tangent_frame(d3 a, d3 b, d3 c, Frame& f) {
+  if (!triangle_normal(a, b, c, f.n)) return false;
+  f.origin = a;
+  f.t1 = unit(b - a);
+  f.t2 = cross(f.n, f.t1);
+  return true;
+}
+__device__ __forceinline__ d2 to_plane(const Frame& f, d3 p) {
+  const d3 d = p - f.origin;
+  return d2{dot(d, f.t1), dot(d, f.t2)};
+}
+// geometry.hpp:101-103
+__device__ __forceinline__ double signed_area_2d(d2 a, d2 b, d2 c) {
+  return 0.5 * ((b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x));
+}
+// geometry.hpp:106-114
+__device__ __forceinline__ bool barycentric_2d(d2 p, d2 a, d2 b, d2 c, d3& out) {
+  const double area = signed_area_2d(a, b, c);
+  const double diag = dmax(dmax(norm2(b - a), norm2(c - a)), norm2(c - b));
+  if (fabs(area) <= 1e-14 * diag * diag) return false;
+  const double u = signed_area_2d(p, b, c) / area;
+  const double v = signed_area_2d(a, p, c) / area;
+  out = mk3(u, v, 1.0 - u - v);
+  return true;
+}
+__device__ __forceinline__ double hermite_step(double x, double delta) {  // barrier.hpp:69-74
+  if (x <= 0) return 0;
+  if (x >= delta) return 1;
+  const double t = x / delta;
+  return t * t * (3.0 - 2.0 * t);
+}
+__device__ __forceinline__ double adaptive_eps(double g, double eps_max) { return dmin(0.9 * g, eps_max); }
+__device__ __forceinline__ double min3(d3 a) { return dmin(dmin(a.x, a.y), a.z); }
+__device__ __forceinline__ d3 clamp_bary(d3 b) {  // contact_sampling.hpp:80-83
+  b = mk3(dmax(b.x, 0.0), dmax(b.y, 0.0), dmax(b.z, 0.0));
+  const double s = b.x + b.y + b.z;
+  return b / s;
+}
+__device__ __forceinline__ double local_scale(const d3* s) {  // contact_sampling.hpp:88-90
+  return (norm(s[1] - s[0]) + norm(s[2] - s[0]) + norm(s[2] - s[1])) / 3.0;
+}
+
+// quadrature.hpp:20-81
+__device__ __forceinline__ int tri_quad(int order, double q[6][4]) {
+  switch (order) {
+    case 1:
+      q[0][0] = q[0][1] = q[0][2] = 1.0 / 3.0;
+      q[0][3] = 1.0;
+      return 1;
+    case 2: {
+      const double a = 2.0 / 3.0, b = 1.0 / 6.0, w = 1.0 / 3.0;
+      const double t[3][4] = {{a, b, b, w}, {b, a, b, w}, {b, b, a, w}};
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 4; ++j) q[i][j] = t[i][j];
+      return 3;
+    }
+    case 3: {
+      const double a = 0.659027622374092, b = 0.231933368553031, c = 0.109039009072877, w = 1.0 / 6.0;
+      const double t[6][4] = {{a, b, c, w}, {a, c, b, w}, {b, a, c, w}, {b, c, a, w}, {c, a, b, w}, {c, b, a, w}};
+      for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 4; ++j) q[i][j] = t[i][j];
+      return 6;
+    }
+    default: {
+      const double a1 = 0.108103018168070, b1 = 0.445948490915965, w1 = 0.223381589678011;
+      const double a2 = 0.816847572980459, b2 = 0.091576213509771, w2 = 0.109951743655322;
+      const double t[6][4] = {{a1, b1, b1, w1}, {b1, a1, b1, w1}, {b1, b1, a1, w1},
+                              {a2, b2, b2, w2}, {b2, a2, b2, w2}, {b2, b2, a2, w2}};
+      for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 4; ++j) q[i][j] = t[i][j];
+      return 6;
+    }
+  }
+}
+__device__ __forceinline__ int seg_quad(int points, double q[5][2]) {
+  const double x2[2] = {-0.5773502691896257, 0.5773502691896257}, w2[2] = {1.0, 1.0};
+  const double x3[3] = {-0.7745966692414834, 0.0, 0.7745966692414834}, w3[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
+  const double x4[4] = {-0.8611363115940526, -0.3399810435848563, 0.3399810435848563, 0.8611363115940526};
+  const double w4[4] = {0.3478548451374538, 0.6521451548625461, 0.6521451548625461, 0.3478548451374538};
+  const double x5[5] = {-0.9061798459386640, -0.5384693101056831, 0.0, 0.5384693101056831, 0.9061798459386640};
+  const double w5[5] = {0.2369268850561891, 0.4786286704993665, 0.5688888888888889, 0.4786286704993665,
+                        0.2369268850561891};
+  const double *xs, *ws;
+  switch (points) {
+    case 1:
+      q[0][0] = 0.5;
+      q[0][1] = 1.0;
+      return 1;
+    case 2: xs = x2; ws = w2; break;
+    case 3: xs = x3; ws = w3; break;
+    case 4: xs = x4; ws = w4; break;
+    default: xs = x5; ws = w5; points = 5; break;
+  }
+  for (int i = 0; i < points; ++i) {
+    q[i][0] = 0.5 * (1.0 + xs[i]);
+    q[i][1] = 0.5 * ws[i];
+  }
+  return points;
+}
+
+// ---------------------------------------------------------------------------
+// K4: point ownership
+
+struct SamplerArgs {
+  const double* x;
+  const double* eps_ref;
+  int32_t nst;
+  const int32_t* stris;
+  const int32_t* mtris;
+  const int32_t* medges;
+  const int32_t* mverts;
+  gmcp_barrier_params P;
+};
+
+// One thread per master vertex feature mv: walks the ascending slave tris
+// listing mv (CSR by mv) and emits the owning tris (count or write).
+template <int Mode>
+__global__ void k_point_owner(SamplerArgs A, int32_t nmv, const int64_t* __restrict__ by_off,
+                              const int32_t* __restrict__ by_st, int64_t* __restrict__ cnt,
+                              const int64_t* __restrict__ off, unsigned long long* __restrict__ keys,
+                              unsigned long long* err) {
+  GRID_LOOP(mv, nmv) {
+    const d3 v = ld3(A.x, A.mverts[mv]);
+    int first_boundary = -1;
+    bool any_interior = false;
+    int64_t c = 0;
+    const int64_t b0 = by_off[mv], b1 = by_off[mv + 1];
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1 && !any_interior) break;
+      for (int64_t k = b0; k < b1; ++k) {
+        const int st = by_st[k];
+        const d3 s[3] = {ld3(A.x, A.stris[3 * st]), ld3(A.x, A.stris[3 * st + 1]), ld3(A.x, A.stris[3 * st + 2])};
+        Frame f;
+        d3 bary;
+        if (!tangent_frame(s[0], s[1], s[2], f) ||
+            !barycentric_2d(to_plane(f, v), to_plane(f, s[0]), to_plane(f, s[1]), to_plane(f, s[2]), bary)) {
+          atomicMin(err, 0ull);  // ownership errors precede every emission error
+          break;
+        }
+        const double mn = min3(bary);
+        if (mn < -1e-12) continue;
+        if (pass == 0) {
+          if (mn > 1e-9) any_interior = true;
+          else if (first_boundary < 0) first_boundary = st;
+        } else if (mn > 1e-9) {
+          if (Mode) keys[off[mv] + c] = ((unsigned long long)st << 32) | (unsigned int)mv;
+          ++c;
+        }
+      }
+    }
+    if (!any_interior && first_boundary >= 0) {
+      if (Mode) keys[off[mv] + c] = ((unsigned long long)first_boundary << 32) | (unsigned int)mv;
+      ++c;
+    }
+    if (!Mode) cnt[mv] = c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: sampling tasks. task = (slave tri, kind, feature), reference order.
+
+struct Out {
+  int8_t* type;
+  int32_t *slave, *master;
+  double *beta_s, *beta_m, *eta, *weight, *gamma, *eps, *g_ref;
+};
+
+struct SampleRec {
+  int8_t type;
+  int32_t master[3];
+  d3 bs, bm;
+  double eta, weight, gamma, g;
+};
+
+// freeze (contact_sampling.hpp:471-485): returns false if the sample is dropped;
+// sets g_ref/eps. err_code: 0 ok, 1 degenerate at eps_reference.
+__device__ __forceinline__ bool freeze(const SamplerArgs& A, const int32_t* sid, const SampleRec& r, double& g_ref,
+                                       double& eps, bool& err) {
+  err = false;
+  if (!(r.g > 0)) return false;  // g_now == r.g bitwise (same normal, xs, xm)
+  g_ref = r.g;
+  if (A.eps_ref) {
+    const double* X = A.eps_ref;
+    const d3 a0 = ld3(X, sid[0]), a1 = ld3(X, sid[1]), a2 = ld3(X, sid[2]);
+    d3 n;
+    if (!triangle_normal(a0, a1, a2, n)) {
+      err = true;
+      return false;
+    }
+    const d3 xs = (r.bs.x * a0 + r.bs.y * a1) + r.bs.z * a2;
+    d3 xm;
+    if (r.type == GMCP_FACE)
+      xm = (r.bm.x * ld3(X, r.master[0]) + r.bm.y * ld3(X, r.master[1])) + r.bm.z * ld3(X, r.master[2]);
+    else if (r.type == GMCP_EDGE)
+      xm = (1.0 - r.eta) * ld3(X, r.master[0]) + r.eta * ld3(X, r.master[1]);
+    else
+      xm = ld3(X, r.master[0]);
+    const double gs = dot(n, xm - xs);
+    if (gs > 0) g_ref = gs;
+  }
+  eps = adaptive_eps(g_ref, A.P.eps_max);
+  return true;
+}
+
+template <int Mode>
+__device__ __forceinline__ void put(const SamplerArgs& A, const int32_t* sid, const SampleRec& r, int64_t& c,
+                                    int64_t base, const Out& O, bool& err) {
+  double g_ref, eps;
+  if (!freeze(A, sid, r, g_ref, eps, err)) return;
+  if (Mode) {
+    const int64_t i = base + c;
+    O.type[i] = r.type;
+    for (int k = 0; k < 3; ++k) {
+      O.slave[3 * i + k] = sid[k];
+      O.master[3 * i + k] = r.master[k];
+    }
+    O.beta_s[3 * i] = r.bs.x;
+    O.beta_s[3 * i + 1] = r.bs.y;
+    O.beta_s[3 * i + 2] = r.bs.z;
+    O.beta_m[3 * i] = r.bm.x;
+    O.beta_m[3 * i + 1] = r.bm.y;
+    O.beta_m[3 * i + 2] = r.bm.z;
+    O.eta[i] = r.eta;
+    O.weight[i] = r.weight;
+    O.gamma[i] = r.gamma;
+    O.eps[i] = eps;
+    O.g_ref[i] = g_ref;
+  }
+  ++c;
+}
+
+// Sutherland-Hodgman, contact_sampling.hpp:39-58
+__device__ __forceinline__ int clip_polygon(d2* poly, int n, const d2* tri) {
+  d2 out[12];
+  for (int e = 0; e < 3; ++e) {
+    if (n < 3) break;
+    const d2 a = tri[e];
+    const d2 dir = tri[(e + 1) % 3] - a;
+    int m = 0;
+    for (int i = 0; i < n; ++i) {
+      const d2 p = poly[i], q = poly[(i + 1) % n];
+      const double dp = cross2(dir, p - a);
+      const double dq = cross2(dir, q - a);
+      if (dp >= 0) out[m++] = p;
+      if ((dp >= 0) != (dq >= 0)) out[m++] = p + (dp / (dp - dq)) * (q - p);
+    }
+    for (int i = 0; i < m; ++i) poly[i] = out[i];
+    n = m;
+  }
+  return n;
+}
+__device__ __forceinline__ int merge_close(d2* poly, int n, double tol) {  // :60-66
+  d2 out[12];
+  int m = 0;
+  for (int i = 0; i < n; ++i)
+    if (m == 0 || norm2(poly[i] - out[m - 1]) > tol) out[m++] = poly[i];
+  while (m >= 2 && norm2(out[0] - out[m - 1]) <= tol) --m;
+  for (int i = 0; i < m; ++i) poly[i] = out[i];
+  return m;
+}
+__device__ __forceinline__ double polygon_area(const d2* poly, int n) {  // :68-76
+  double twice = 0;
+  for (int i = 0; i < n; ++i) twice += cross2(poly[i], poly[(i + 1) % n]);
+  return 0.5 * twice;
+}
+
+// task kinds
+constexpr int kFace = 0, kEdge = 1, kPoint = 2;
+
+template <int Mode>
+__global__ void __launch_bounds__(128) k_sample(SamplerArgs A, int64_t ntask, const int32_t* __restrict__ task_st,
+                                                const int32_t* __restrict__ task_feat,
+                                                const int8_t* __restrict__ task_kind, int64_t* __restrict__ cnt,
+                                                const int64_t* __restrict__ off, Out O, unsigned long long* err) {
+  GRID_LOOP(t, ntask) {
+    const int st = task_st[t];
+    const int kind = task_kind[t];
+    const int feat = task_feat[t];
+    const int32_t* sid = A.stris + 3 * st;
+    const d3 s[3] = {ld3(A.x, sid[0]), ld3(A.x, sid[1]), ld3(A.x, sid[2])};
+    int64_t c = 0;
+    const int64_t base = Mode ? off[t] : 0;
+    bool bad = false, ferr = false;
+    Frame f;
+    if (!tangent_frame(s[0], s[1], s[2], f)) {
+      bad = true;
+    } else if (kind == kFace) {  // sample_face, contact_sampling.hpp:97-141
+      const int32_t* mid = A.mtris + 3 * feat;
+      const d3 m[3] = {ld3(A.x, mid[0]), ld3(A.x, mid[1]), ld3(A.x, mid[2])};
+      const d2 s2[3] = {to_plane(f, s[0]), to_plane(f, s[1]), to_plane(f, s[2])};
+      const d2 m2[3] = {to_plane(f, m[0]), to_plane(f, m[1]), to_plane(f, m[2])};
+      const double scale = local_scale(s);
+      const double merge_tol = 1e-12 * scale;
+      const double area_tol = 1e-14 * scale * scale;
+      const double m_area = signed_area_2d(m2[0], m2[1], m2[2]);
+      if (fabs(m_area) > area_tol) {
+        d2 poly[12] = {m2[0], m2[1], m2[2]};
+        if (m_area < 0) {
+          const d2 tmp = poly[1];
+          poly[1] = poly[2];
+          poly[2] = tmp;
+        }
+        int n = clip_polygon(poly, 3, s2);
+        n = merge_close(poly, n, merge_tol);
+        if (n >= 3 && polygon_area(poly, n) > area_tol) {
+          double q[6][4];
+          const int nq = tri_quad(A.P.quad_order_face, q);
+          for (int i = 1; i + 1 < n && !bad; ++i) {
+            const d2 p0 = poly[0], p1 = poly[i], p2 = poly[i + 1];
+            const double sub_area = signed_area_2d(p0, p1, p2);
+            if (sub_area <= area_tol) continue;
+            for (int k = 0; k < nq; ++k) {
+              const d2 pt = (q[k][0] * p0 + q[k][1] * p1) + q[k][2] * p2;
+              SampleRec r;
+              r.type = GMCP_FACE;
+              d3 bs;
+              if (!barycentric_2d(pt, s2[0], s2[1], s2[2], bs) || !barycentric_2d(pt, m2[0], m2[1], m2[2], r.bm)) {
+                bad = true;
+                break;
+              }
+              r.bs = clamp_bary(bs);
+              r.weight = q[k][3] * sub_area;
+              r.gamma = hermite_step(min3(r.bm), A.P.delta_face);
+              r.eta = 0;
+              const d3 xs = (r.bs.x * s[0] + r.bs.y * s[1]) + r.bs.z * s[2];
+              const d3 xm = (r.bm.x * m[0] + r.bm.y * m[1]) + r.bm.z * m[2];
+              r.g = dot(f.n, xm - xs);
+              r.master[0] = mid[0];
+              r.master[1] = mid[1];
+              r.master[2] = mid[2];
+              put<Mode>(A, sid, r, c, base, O, ferr);
+              if (ferr) {
+                bad = true;
+                break;
+              }
+            }
+          }
+        }
+      }
+    } else if (kind == kEdge) {  // sample_edge, contact_sampling.hpp:146-192
+      const int32_t* eid = A.medges + 2 * feat;
+      const d3 e0 = ld3(A.x, eid[0]), e1 = ld3(A.x, eid[1]);
+      const d2 s2[3] = {to_plane(f, s[0]), to_plane(f, s[1]), to_plane(f, s[2])};
+      const double scale = local_scale(s);
+      const d2 q0 = to_plane(f, e0);
+      const d2 dq = to_plane(f, e1) - q0;
+      bool keep = !(norm2(dq) <= 1e-12 * scale);
+      double t0 = 0, t1 = 1;
+      for (int k = 0; k < 3 && keep; ++k) {
+        const d2 a = s2[k];
+        const d2 dir = s2[(k + 1) % 3] - a;
+        const double ca = cross2(dir, q0 - a);
+        const double dc = cross2(dir, dq);
+        if (fabs(dc) <= 1e-14 * scale * scale) {
+          if (ca < 0) keep = false;
+        } else if (dc > 0) {
+          t0 = dmax(t0, -ca / dc);
+        } else {
+          t1 = dmin(t1, -ca / dc);
+        }
+      }
+      if (keep && (t1 - t0 > 1e-12)) {
+        const double len3 = norm(e1 - e0) * (t1 - t0);
+        double q[5][2];
+        const int nq = seg_quad(A.P.quad_order_edge, q);
+        for (int k = 0; k < nq; ++k) {
+          SampleRec r;
+          r.type = GMCP_EDGE;
+          const double eta = t0 + (t1 - t0) * q[k][0];
+          r.eta = eta;
+          d3 bs;
+          if (!barycentric_2d(q0 + eta * dq, s2[0], s2[1], s2[2], bs)) {
+            bad = true;
+            break;
+          }
+          r.bs = clamp_bary(bs);
+          r.bm = mk3(0, 0, 0);
+          r.weight = q[k][1] * len3;
+          r.gamma = hermite_step(eta, A.P.delta_edge) * hermite_step(1.0 - eta, A.P.delta_edge);
+          const d3 xs = (r.bs.x * s[0] + r.bs.y * s[1]) + r.bs.z * s[2];
+          const d3 xm = (1.0 - eta) * e0 + eta * e1;
+          r.g = dot(f.n, xm - xs);
+          r.master[0] = eid[0];
+          r.master[1] = eid[1];
+          r.master[2] = -1;
+          put<Mode>(A, sid, r, c, base, O, ferr);
+          if (ferr) {
+            bad = true;
+            break;
+          }
+        }
+      }
+    } else {  // sample_point, contact_sampling.hpp:196-215
+      const int vid = A.mverts[feat];
+      const d3 v = ld3(A.x, vid);
+      d3 bary;
+      if (!barycentric_2d(to_plane(f, v), to_plane(f, s[0]), to_plane(f, s[1]), to_plane(f, s[2]), bary)) {
+        bad = true;
+      } else if (!(min3(bary) < -1e-12)) {
+        SampleRec r;
+        r.type = GMCP_POINT;
+        r.bs = clamp_bary(bary);
+        r.bm = mk3(0, 0, 0);
+        r.eta = 0;
+        r.weight = 1;
+        r.gamma = 1;
+        const d3 xs = (r.bs.x * s[0] + r.bs.y * s[1]) + r.bs.z * s[2];
+        r.g = dot(f.n, v - xs);
+        r.master[0] = vid;
+        r.master[1] = r.master[2] = -1;
+        put<Mode>(A, sid, r, c, base, O, ferr);
+        if (ferr) bad = true;
+      }
+    }
+    if (bad) atomicMin(err, (unsigned long long)t + 1);  // +1: 0 is reserved for ownership errors
+    if (!Mode) cnt[t] = c;
+  }
+}
+
+// tasks per slave tri in reference order: faces (cand tris), edges (cand
+// edges), points (owned vertices ascending)
+__global__ void k_tasks(int32_t nst, const int64_t* __restrict__ toff, const int32_t* __restrict__ tids,
+                        const int64_t* __restrict__ eoff, const int32_t* __restrict__ eids,
+                        const int64_t* __restrict__ poff, const int32_t* __restrict__ pids,
+                        int32_t* __restrict__ task_st, int32_t* __restrict__ task_feat, int8_t* __restrict__ task_kind) {
+  GRID_LOOP(st, nst) {
+    int64_t o = toff[st] + eoff[st] + poff[st];
+    for (int64_t i = toff[st]; i < toff[st + 1]; ++i, ++o) {
+      task_st[o] = (int32_t)st;
+      task_feat[o] = tids[i];
+      task_kind[o] = kFace;
+    }
+    for (int64_t i = eoff[st]; i < eoff[st + 1]; ++i, ++o) {
+      task_st[o] = (int32_t)st;
+      task_feat[o] = eids[i];
+      task_kind[o] = kEdge;
+    }
+    for (int64_t i = poff[st]; i < poff[st + 1]; ++i, ++o) {
+      task_st[o] = (int32_t)st;
+      task_feat[o] = pids[i];
+      task_kind[o] = kPoint;
+    }
+  }
+}
+
+// CSR offsets from sorted keys whose high 32 bits are the segment id.
+__global__ void k_seg_offsets(int64_t n, const unsigned long long* __restrict__ keys, int32_t nseg,
+                              int64_t* __restrict__ off) {
+  GRID_LOOP(s, (int64_t)nseg + 1) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)(keys[mid] >> 32) < s) lo = mid + 1; else hi = mid;
+    }
+    off[s] = lo;
+  }
+}
+__global__ void k_low32(int64_t n, const unsigned long long* __restrict__ keys, int32_t* __restrict__ out) {
+  GRID_LOOP(i, n) out[i] = (int32_t)(keys[i] & 0xffffffffull);
+}
+__global__ void k_pair_keys(int32_t nst, const int64_t* __restrict__ off, const int32_t* __restrict__ ids,
+                            unsigned long long* __restrict__ keys) {
+  GRID_LOOP(st, nst) {
+    for (int64_t i = off[st]; i < off[st + 1]; ++i) keys[i] = ((unsigned long long)ids[i] << 32) | (unsigned int)st;
+  }
+}
+
+int64_t last_of(const DBuf<int64_t>& a, int64_t idx, cudaStream_t s) {
+  int64_t v = 0;
+  GMCP_CUDA(cudaMemcpyAsync(&v, a.p + idx, sizeof v, cudaMemcpyDeviceToHost, s));
+  GMCP_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+}  // namespace
+
+// ===========================================================================
+
+void run_broadphase(Ctx& c, double r, int64_t* counts) {
+  cudaStream_t s = c.stream;
+  // self-contact check (contact_sampling.hpp:286-294), host mirrors are sorted
+  {
+    const auto& a = c.slave.h_verts;
+    const auto& b = c.master.h_verts;
+    size_t i = 0, j = 0;
+    while (i < a.size() && j < b.size()) {
+      if (a[i] == b[j])
+        throw StatusError(GMCP_ERR_CONFIG,
+                          "build_candidate_pairs: slave and master share vertices (self-contact is not supported)");
+      if (a[i] < b[j]) ++i; else ++j;
+    }
+  }
+  const int32_t nst = c.slave.n_tris, nmt = c.master.n_tris;
+  for (int k = 0; k < 3; ++k) {
+    c.pair_off[k].resize(nst + 1);
+    c.pair_off[k].zero(s);
+  }
+  if (nst == 0 || nmt == 0) {
+    for (int k = 0; k < 3; ++k) c.pair_ids[k].resize(0);
+    c.have_pairs = true;
+    counts[0] = counts[1] = counts[2] = 0;
+    c.sync();
+    return;
+  }
+  // K1: boxes, Morton keys, sort, hierarchy, refit
+  DBuf<Box> tboxes, nodes;
+  DBuf<unsigned long long> bounds, keys, keys_sorted;
+  DBuf<int32_t> idx, idx_sorted, left, right, parent, flags;
+  tboxes.resize(nmt);
+  bounds.resize(6);
+  const unsigned long long binit[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+  GMCP_CUDA(cudaMemcpyAsync(bounds.p, binit, sizeof binit, cudaMemcpyHostToDevice, s));
+  k_master_boxes<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, c.master.tris.p, c.x.p, tboxes.p, bounds.p);
+  keys.resize(nmt);
+  keys_sorted.resize(nmt);
+  idx.resize(nmt);
+  idx_sorted.resize(nmt);
+  k_morton<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, tboxes.p, bounds.p, keys.p, idx.p);
+  sort_pairs(keys.p, keys_sorted.p, idx.p, idx_sorted.p, nmt, s, 64);
+  const int nnodes = 2 * nmt - 1;
+  nodes.resize(nnodes);
+  left.resize(std::max(nmt - 1, 1));
+  right.resize(std::max(nmt - 1, 1));
+  parent.resize(nnodes);
+  flags.resize(std::max(nmt - 1, 1));
+  flags.zero(s);
+  GMCP_CUDA(cudaMemsetAsync(parent.p, 0xff, nnodes * sizeof(int32_t), s));
+  if (nmt > 1) k_karras<<<grid_for(nmt - 1, 256), 256, 0, s>>>(nmt, keys_sorted.p, left.p, right.p, parent.p);
+  k_refit<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, idx_sorted.p, tboxes.p, left.p, right.p, parent.p, nodes.p, flags.p);
+  c.launches += 3 + (nmt > 1 ? 1 : 0) + 2;
+  // K2: count, scan, emit+sort
+  DBuf<int64_t> cnt;
+  DBuf<int> ovf;
+  cnt.resize(nst + 1);
+  cnt.zero(s);
+  ovf.resize(1);
+  ovf.zero(s);
+  k_query<0><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.x.p, r, nmt, nodes.p, left.p, right.p,
+                                                 idx_sorted.p, cnt.p, nullptr, nullptr, ovf.p);
+  exclusive_scan(cnt.p, c.pair_off[0].p, nst + 1, s);
+  const int64_t ntri = last_of(c.pair_off[0], nst, s);
+  c.pair_ids[0].resize(std::max<int64_t>(ntri, 1));
+  k_query<1><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.x.p, r, nmt, nodes.p, left.p, right.p,
+                                                 idx_sorted.p, nullptr, c.pair_off[0].p, c.pair_ids[0].p, ovf.p);
+  c.pair_ids[0].n = ntri;
+  // K3: candidate edges / verts
+  DBuf<int32_t> tmp_e, tmp_v;
+  DBuf<int64_t> ecnt, vcnt;
+  tmp_e.resize(std::max<int64_t>(3 * ntri, 1));
+  tmp_v.resize(std::max<int64_t>(3 * ntri, 1));
+  ecnt.resize(nst + 1);
+  vcnt.resize(nst + 1);
+  ecnt.zero(s);
+  vcnt.zero(s);
+  k_features<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.master.tris.p,
+                                                 c.master.tri_edges.p, c.master.verts.p, c.master.n_verts, tmp_e.p,
+                                                 tmp_v.p, ecnt.p, vcnt.p);
+  exclusive_scan(ecnt.p, c.pair_off[1].p, nst + 1, s);
+  exclusive_scan(vcnt.p, c.pair_off[2].p, nst + 1, s);
+  const int64_t ne = last_of(c.pair_off[1], nst, s), nv = last_of(c.pair_off[2], nst, s);
+  c.pair_ids[1].resize(std::max<int64_t>(ne, 1));
+  c.pair_ids[2].resize(std::max<int64_t>(nv, 1));
+  k_compact<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, tmp_e.p, c.pair_off[1].p, c.pair_ids[1].p);
+  k_compact<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, tmp_v.p, c.pair_off[2].p, c.pair_ids[2].p);
+  c.pair_ids[1].n = ne;
+  c.pair_ids[2].n = nv;
+  c.launches += 5;
+  GMCP_CUDA(cudaGetLastError());
+  int of = 0;
+  GMCP_CUDA(cudaMemcpyAsync(&of, ovf.p, sizeof of, cudaMemcpyDeviceToHost, s));
+  c.sync();
+  if (of) throw StatusError(GMCP_ERR_CONFIG, "broadphase: LBVH traversal stack overflow");
+  counts[0] = ntri;
+  counts[1] = ne;
+  counts[2] = nv;
+  c.have_pairs = true;
+}
+
+int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
+  cudaStream_t s = c.stream;
+  const int32_t nst = c.slave.n_tris, nmv = c.master.n_verts;
+  SamplerArgs A;
+  A.x = c.x.p;
+  A.eps_ref = eps_ref_dev;
+  A.nst = nst;
+  A.stris = c.slave.tris.p;
+  A.mtris = c.master.tris.p;
+  A.medges = c.master.edges.p;
+  A.mverts = c.master.verts.p;
+  A.P = c.params;
+  DBuf<unsigned long long> err;
+  err.resize(1);
+  GMCP_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
+
+  // K4: inverse lists mv -> slave tris (ascending st), ownership, regroup by st
+  const int64_t nvc = (int64_t)c.pair_ids[2].n;
+  DBuf<unsigned long long> k1, k2;
+  DBuf<int64_t> by_off, pcnt, poff, pt_off;
+  DBuf<int32_t> by_st, pt_ids;
+  by_off.resize(nmv + 1);
+  by_st.resize(std::max<int64_t>(nvc, 1));
+  if (nvc) {
+    k1.resize(nvc);
+    k2.resize(nvc);
+    k_pair_keys<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[2].p, c.pair_ids[2].p, k1.p);
+    sort_keys(k1.p, k2.p, nvc, s, 64);
+    k_seg_offsets<<<grid_for(nmv + 1, 256), 256, 0, s>>>(nvc, k2.p, nmv, by_off.p);
+    k_low32<<<grid_for(nvc, 256), 256, 0, s>>>(nvc, k2.p, by_st.p);
+    c.launches += 3;
+  } else {
+    by_off.zero(s);
+  }
+  pcnt.resize(nmv + 1);
+  pcnt.zero(s);
+  poff.resize(nmv + 1);
+  if (nmv) {
+    k_point_owner<0><<<grid_for(nmv, 128), 128, 0, s>>>(A, nmv, by_off.p, by_st.p, pcnt.p, nullptr, nullptr, err.p);
+    ++c.launches;
+  }
+  exclusive_scan(pcnt.p, poff.p, nmv + 1, s);
+  const int64_t npts = last_of(poff, nmv, s);
+  pt_off.resize(nst + 1);
+  pt_ids.resize(std::max<int64_t>(npts, 1));
+  if (npts) {
+    k1.resize(npts);
+    k2.resize(npts);
+    k_point_owner<1><<<grid_for(nmv, 128), 128, 0, s>>>(A, nmv, by_off.p, by_st.p, nullptr, poff.p, k1.p, err.p);
+    sort_keys(k1.p, k2.p, npts, s, 64);
+    k_seg_offsets<<<grid_for(nst + 1, 256), 256, 0, s>>>(npts, k2.p, nst, pt_off.p);
+    k_low32<<<grid_for(npts, 256), 256, 0, s>>>(npts, k2.p, pt_ids.p);
+    c.launches += 3;
+  } else {
+    pt_off.zero(s);
+  }
+  // K5: tasks in reference order, count -> scan -> emit
+  const int64_t ntask = (int64_t)c.pair_ids[0].n + (int64_t)c.pair_ids[1].n + npts;
+  DBuf<int32_t> task_st, task_feat;
+  DBuf<int8_t> task_kind;
+  DBuf<int64_t> tcnt, toff;
+  task_st.resize(std::max<int64_t>(ntask, 1));
+  task_feat.resize(std::max<int64_t>(ntask, 1));
+  task_kind.resize(std::max<int64_t>(ntask, 1));
+  tcnt.resize(ntask + 1);
+  tcnt.zero(s);
+  toff.resize(ntask + 1);
+  Out O{};
+  if (ntask) {
+    k_tasks<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.pair_off[1].p,
+                                                c.pair_ids[1].p, pt_off.p, pt_ids.p, task_st.p, task_feat.p,
+                                                task_kind.p);
+    k_sample<0><<<grid_for(ntask, 128), 128, 0, s>>>(A, ntask, task_st.p, task_feat.p, task_kind.p, tcnt.p, nullptr,
+                                                      O, err.p);
+    c.launches += 2;
+  }
+  exclusive_scan(tcnt.p, toff.p, ntask + 1, s);
+  const int64_t n = last_of(toff, ntask, s);
+  unsigned long long e = 0;
+  GMCP_CUDA(cudaMemcpyAsync(&e, err.p, sizeof e, cudaMemcpyDeviceToHost, s));
+  c.sync();
+  if (e != ~0ull) throw StatusError(GMCP_ERR_DEGENERATE, "build_contact_state: degenerate triangle (MeshError)");
+  c.ns = n;
+  c.s_type.resize(n);
+  c.s_slave.resize(3 * n);
+  c.s_master.resize(3 * n);
+  c.s_beta_s.resize(3 * n);
+  c.s_beta_m.resize(3 * n);
+  c.s_eta.resize(n);
+  c.s_weight.resize(n);
+  c.s_gamma.resize(n);
+  c.s_eps.resize(n);
+  c.s_gref.resize(n);
+  O = Out{c.s_type.p, c.s_slave.p, c.s_master.p, c.s_beta_s.p, c.s_beta_m.p, c.s_eta.p,
+          c.s_weight.p, c.s_gamma.p, c.s_eps.p, c.s_gref.p};
+  if (n) {
+    k_sample<1><<<grid_for(ntask, 128), 128, 0, s>>>(A, ntask, task_st.p, task_feat.p, task_kind.p, nullptr, toff.p,
+                                                      O, err.p);
+    ++c.launches;
+  }
+  GMCP_CUDA(cudaGetLastError());
+  derive_sample_fields(c);
+  c.sync();
+  return n;
+}
+
+}  // namespace gmcp_b200
