@@ -1,0 +1,78 @@
+/* GMCP B200 quasi-static solver C-ABI: the device-resident replacement of
+ * gmcp::System (proj/include/gmcp/solver.hpp:63-376). Bodies are linear-
+ * elastic tet meshes (elasticity.hpp), Dirichlet dofs are eliminated by
+ * masking, contact pairs run the GMCP pipeline of include/gmcp_b200.h, and
+ * the Newton direction comes from a block-Jacobi preconditioned CG on the
+ * 3x3 BCSR Hessian instead of the reference's SimplicialLDLT
+ * (solver.hpp:325-375).
+ *
+ *   gmcp_system_add_body          System::add_body            solver.hpp:73-91
+ *   gmcp_system_fix_dofs          System::fix_dof / fix_vertex solver.hpp:97-105
+ *   gmcp_system_set_external_force System::f_ext              solver.hpp:69
+ *   gmcp_system_add_contact_pair  System::add_contact_pair    solver.hpp:110-121
+ *                                 (surfaces + params resolved by the caller)
+ *   gmcp_system_solve             System::solve               solver.hpp:125-228
+ */
+#ifndef GMCP_SOLVER_H
+#define GMCP_SOLVER_H
+
+#include "gmcp_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gmcp_system gmcp_system;
+
+/* SolverSettings (solver.hpp:35-42) + the Krylov controls that replace LDL^T. */
+typedef struct {
+  int32_t load_steps;        /* 10 */
+  int32_t max_newton_iters;  /* 200 */
+  double newton_tol;         /* <= 0: derived from loads (solver.hpp:256-269) */
+  int32_t max_line_search;   /* 40 */
+  double pcg_tol;            /* relative residual ||r||_2 / ||b||_2, e.g. 1e-10 */
+  int32_t pcg_max_iters;     /* e.g. 20000 */
+} gmcp_solver_settings;
+
+/* StepStats (solver.hpp:44-53) + PCG iterations. */
+typedef struct {
+  int32_t step, newton_iters, rebuilds, backtracks;
+  int64_t pcg_iters;
+  double residual, energy, min_gap;
+  int32_t energy_monotone;
+} gmcp_step_stats;
+
+/* RunStats (solver.hpp:55-61). residual is set when a solve fails. */
+typedef struct {
+  int64_t total_newton_iters, total_rebuilds, total_pcg_iters;
+  double newton_tol_used, wall_seconds, residual;
+} gmcp_run_stats;
+
+/* StepCallback (solver.hpp:123): stats and the host copy of x after each load step. */
+typedef void (*gmcp_step_callback)(const gmcp_step_stats* stats, const double* x, int64_t n_dof, void* user);
+
+const char* gmcp_system_last_error(void);
+int gmcp_system_create(int device, gmcp_system** out);
+void gmcp_system_destroy(gmcp_system* sys);
+int gmcp_system_add_body(gmcp_system* sys, const double* verts, int64_t n_verts, const int32_t* tets,
+                         int64_t n_tets, double youngs, double poisson, int32_t* vertex_offset);
+int gmcp_system_fix_dofs(gmcp_system* sys, int64_t n, const int64_t* dofs, const double* targets);
+int gmcp_system_set_external_force(gmcp_system* sys, const double* f_ext, int64_t n_dof);
+int gmcp_system_add_contact_pair(gmcp_system* sys, const gmcp_surface* slave, const gmcp_surface* master,
+                                 const gmcp_barrier_params* resolved, int32_t* pair_id);
+/* On failure returns GMCP_ERR_SOLVER / GMCP_ERR_CONFIG like the reference's
+ * SolverError / ConfigError; out->residual carries SolverError::residual. */
+int gmcp_system_solve(gmcp_system* sys, const gmcp_solver_settings* settings, gmcp_step_callback cb,
+                      void* user, gmcp_run_stats* out);
+int gmcp_system_positions(gmcp_system* sys, double* x, int64_t n_dof);
+int gmcp_system_set_positions(gmcp_system* sys, const double* x, int64_t n_dof);
+int64_t gmcp_system_num_samples(gmcp_system* sys, int32_t pair);
+int gmcp_system_pair_force_summary(gmcp_system* sys, int32_t pair, double* out12);
+int gmcp_system_pair_pressure(gmcp_system* sys, int32_t pair, int64_t* n, gmcp_pressure_record* out);
+int64_t gmcp_system_launch_count(const gmcp_system* sys);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

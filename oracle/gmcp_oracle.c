@@ -15,6 +15,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include "gmcp_oracle_api.h"
 
@@ -1159,5 +1160,29 @@ int orc_force_summary(const orc_state* S, const gmcp_barrier_params* P, const do
   const v3 total = add3(add3(face, edge), point);
   const v3 all[4] = {face, edge, point, total};
   for (int j = 0; j < 4; ++j) memcpy(out + 3 * j, all[j].v, sizeof all[j].v);
+  return GMCP_OK;
+}
+
+int orc_time_assembly(const orc_state* S, const gmcp_barrier_params* P, const double* x, int32_t reps,
+                      double* best_seconds, int64_t* n_triplets) {
+  double best = 1e300;
+  double* grad = (double*)calloc((size_t)(S->n_dof > 0 ? S->n_dof : 1), sizeof(double));
+  for (int32_t r = 0; r < reps; ++r) {
+    int64_t bad, nb;
+    double e;
+    memset(grad, 0, sizeof(double) * (size_t)S->n_dof);
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    const int rc = orc_add_contact_gradient_hessian(S, P, x, grad, &e, &bad, &nb, NULL, NULL, NULL, n_triplets);
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    if (rc) {
+      free(grad);
+      return rc;
+    }
+    const double dt = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+    if (dt < best) best = dt;
+  }
+  free(grad);
+  *best_seconds = best;
   return GMCP_OK;
 }

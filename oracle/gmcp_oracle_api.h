@@ -94,6 +94,11 @@ int orc_pressure_field(const orc_state* st, const gmcp_barrier_params* p, const 
 int orc_force_summary(const orc_state* st, const gmcp_barrier_params* p, const double* x,
                       double* out);
 
+/* CPU baseline timing: best-of-reps seconds of one assembly call
+ * (add_contact_gradient_hessian) over the state, excluding marshalling. */
+int orc_time_assembly(const orc_state* st, const gmcp_barrier_params* p, const double* x, int32_t reps,
+                      double* best_seconds, int64_t* n_triplets);
+
 #ifdef __cplusplus
 }
 #endif

@@ -288,6 +288,15 @@ class OracleState:
         self.orc._check(self.L.orc_pressure_field(self.h, C.byref(cp), self._p(x), C.byref(n), self._p(out)))
         return out
 
+    def time_assembly(self, params, x, reps=1):
+        """Best-of-reps seconds of one add_contact_gradient_hessian call."""
+        x = self._x(x)
+        cp = params_struct(params)
+        sec, nt = C.c_double(), C.c_int64()
+        self.orc._check(self.L.orc_time_assembly(self.h, C.byref(cp), self._p(x), C.c_int32(reps), C.byref(sec),
+                                                 C.byref(nt)))
+        return sec.value, nt.value
+
     def force_summary(self, params, x):
         x = self._x(x)
         cp = params_struct(params)

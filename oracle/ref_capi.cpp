@@ -414,6 +414,26 @@ int orc_force_summary(const orc_state* s, const gmcp_barrier_params* p, const do
   });
 }
 
+int orc_time_assembly(const orc_state* s, const gmcp_barrier_params* p, const double* x, int32_t reps,
+                      double* best_seconds, int64_t* n_triplets) {
+  return guarded([&] {
+    const VecX xv = to_vec(x, s->n_dof);
+    const BarrierParams bp = to_params(p);
+    double best = 1e300;
+    for (int r = 0; r < reps; ++r) {
+      VecX grad = VecX::Zero(s->n_dof);
+      std::vector<Eigen::Triplet<Real>> trips;
+      const auto t0 = std::chrono::steady_clock::now();
+      add_contact_gradient_hessian(s->state, bp, xv, grad, trips);
+      const auto t1 = std::chrono::steady_clock::now();
+      best = std::min(best, std::chrono::duration<double>(t1 - t0).count());
+      *n_triplets = static_cast<int64_t>(trips.size());
+    }
+    *best_seconds = best;
+    return GMCP_OK;
+  });
+}
+
 // ---------------------------------------------------------------------------
 // ref_* helpers: mesh generators / boundary extraction (tet_mesh.hpp:56-168,
 // contact_sampling.hpp:226-255) and whole-scene solves (solver.hpp:125-228).

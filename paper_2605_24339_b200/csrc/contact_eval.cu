@@ -510,11 +510,11 @@ void launch_assembly(Ctx& c, int mode) {
   const DevSamples S = c.samples();
   const int rb = (int)std::max<int64_t>(1, std::min<int64_t>((P.n_runs + kRunWarps - 1) / kRunWarps, 148 * 16));
   if (mode == 1)
-    k_run_partials<true><<<rb, 32 * kRunWarps, 0, c.stream>>>(S, c.x.p, P.n_runs, P.run_off.p, P.run_slave.p,
+    k_run_partials<true><<<rb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
                                                               P.lm_off.p, P.lm_ids.p, P.lp_off.p, P.lp.p,
                                                               P.pbase.p, P.partial.p, c.red_u.p);
   else
-    k_run_partials<false><<<rb, 32 * kRunWarps, 0, c.stream>>>(S, c.x.p, P.n_runs, P.run_off.p, P.run_slave.p,
+    k_run_partials<false><<<rb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
                                                                P.lm_off.p, P.lm_ids.p, P.lp_off.p, P.lp.p,
                                                                P.pbase.p, P.partial.p, c.red_u.p);
   const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P.n_rows + 7) / 8, 148 * 32));
@@ -605,7 +605,7 @@ void time_assembly(Ctx& c, int reps, int flush_l2, double* ms_pass, double* ms_k
       ++c.launches;
     }
     GMCP_CUDA(cudaEventRecord(k0, c.stream));
-    k_run_partials<true><<<rb, 32 * kRunWarps, 0, c.stream>>>(S, c.x.p, P.n_runs, P.run_off.p, P.run_slave.p,
+    k_run_partials<true><<<rb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
                                                               P.lm_off.p, P.lm_ids.p, P.lp_off.p, P.lp.p,
                                                               P.pbase.p, P.partial.p, c.red_u.p);
     ++c.launches;

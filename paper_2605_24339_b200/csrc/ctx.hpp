@@ -48,6 +48,11 @@ struct Ctx {
 
   DevSurface slave, master;
   DBuf<double> x, dx, grad, eps_ref;
+  // A System (solver.cu) points its contact pairs at its own x / dx buffers.
+  double* x_ext = nullptr;
+  double* dx_ext = nullptr;
+  double* X() const { return x_ext ? x_ext : x.p; }
+  double* DX() const { return dx_ext ? dx_ext : dx.p; }
 
   // candidate pairs (CSR per slave tri)
   DBuf<int64_t> pair_off[3];

@@ -201,7 +201,7 @@ EnergyOut run_energy(Ctx& c, bool need_prefix_min) {
   c.red_d.resize(kRedBlocks + 8);
   const DevSamples S = c.samples();
   if (S.n == 0) return o;
-  k_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(S, c.x.p, S.n, c.red_d.p, c.red_u.p);
+  k_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(S, c.X(), S.n, c.red_d.p, c.red_u.p);
   k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p, kRedBlocks, 1, c.red_d.p + kRedBlocks);
   c.launches += 2;
   GMCP_CUDA(cudaGetLastError());
@@ -219,7 +219,7 @@ EnergyOut run_energy(Ctx& c, bool need_prefix_min) {
     // try_contact_energy stops at the first offending sample: its energy and
     // min gap cover samples [0, first_bad] only (contact_energy.hpp:98-104).
     reset_red(c);
-    k_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(S, c.x.p, o.first_bad + 1, c.red_d.p, c.red_u.p);
+    k_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(S, c.X(), o.first_bad + 1, c.red_d.p, c.red_u.p);
     k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p, kRedBlocks, 1, c.red_d.p + kRedBlocks);
     c.launches += 2;
     GMCP_CUDA(cudaGetLastError());
@@ -238,7 +238,7 @@ void run_pressure(Ctx& c, gmcp_pressure_record* out_host) {
   DBuf<gmcp_pressure_record> out;
   out.resize(nf);
   reset_red(c);
-  k_pressure<<<grid_for(nf, 256), 256, 0, c.stream>>>(c.samples(), c.x.p, nf, c.face_idx.p, c.params.kappa_face,
+  k_pressure<<<grid_for(nf, 256), 256, 0, c.stream>>>(c.samples(), c.X(), nf, c.face_idx.p, c.params.kappa_face,
                                                       out.p, c.red_u.p);
   ++c.launches;
   GMCP_CUDA(cudaGetLastError());
@@ -259,7 +259,7 @@ void run_force_summary(Ctx& c, double* out12) {
     for (int q = 0; q < 12; ++q) out12[q] = 0;
     return;
   }
-  k_force<<<kRedBlocks, kRedThreads, 0, c.stream>>>(c.samples(), c.x.p, c.red_d.p, c.red_u.p);
+  k_force<<<kRedBlocks, kRedThreads, 0, c.stream>>>(c.samples(), c.X(), c.red_d.p, c.red_u.p);
   k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p, kRedBlocks, 9, c.red_d.p + 9 * kRedBlocks);
   c.launches += 2;
   GMCP_CUDA(cudaGetLastError());
@@ -283,7 +283,7 @@ void run_kinematics(Ctx& c, double* g, int32_t* nv, int32_t* ids, double* dg) {
   nvd.resize(n);
   idd.resize(6 * n);
   reset_red(c);
-  k_kinematics<<<grid_for(n, 256), 256, 0, c.stream>>>(c.samples(), c.x.p, gd.p, nvd.p, idd.p, dgd.p, c.red_u.p);
+  k_kinematics<<<grid_for(n, 256), 256, 0, c.stream>>>(c.samples(), c.X(), gd.p, nvd.p, idd.p, dgd.p, c.red_u.p);
   ++c.launches;
   GMCP_CUDA(cudaGetLastError());
   unsigned long long u[4];
@@ -302,7 +302,7 @@ double run_step_filter(Ctx& c) {
   c.red_u.resize(4);
   const unsigned long long init[4] = {ord_bits_host(1.0), ~0ull, ~0ull, 0ull};
   GMCP_CUDA(cudaMemcpyAsync(c.red_u.p, init, sizeof init, cudaMemcpyHostToDevice, c.stream));
-  k_step_filter<<<grid_for(c.ns, 256), 256, 0, c.stream>>>(c.samples(), c.x.p, c.dx.p, c.red_u.p);
+  k_step_filter<<<grid_for(c.ns, 256), 256, 0, c.stream>>>(c.samples(), c.X(), c.DX(), c.red_u.p);
   ++c.launches;
   GMCP_CUDA(cudaGetLastError());
   unsigned long long u[4];
@@ -317,12 +317,12 @@ double run_displacement_cap(Ctx& c) {
   const unsigned long long init[4] = {0ull, ~0ull, ~0ull, ord_bits_host(0.0)};
   GMCP_CUDA(cudaMemcpyAsync(c.red_u.p, init, sizeof init, cudaMemcpyHostToDevice, c.stream));
   if (c.ns) {
-    k_cap_active<<<grid_for(c.ns, 256), 256, 0, c.stream>>>(c.samples(), c.x.p, c.red_u.p);
+    k_cap_active<<<grid_for(c.ns, 256), 256, 0, c.stream>>>(c.samples(), c.X(), c.red_u.p);
     ++c.launches;
   }
   const int64_t nv = c.n_vertices();
   if (nv) {
-    k_max_move<<<grid_for(nv, 256), 256, 0, c.stream>>>(nv, c.dx.p, c.red_u.p);
+    k_max_move<<<grid_for(nv, 256), 256, 0, c.stream>>>(nv, c.DX(), c.red_u.p);
     ++c.launches;
   }
   GMCP_CUDA(cudaGetLastError());

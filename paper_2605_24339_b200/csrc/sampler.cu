@@ -859,7 +859,7 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   bounds.resize(6);
   const unsigned long long binit[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
   GMCP_CUDA(cudaMemcpyAsync(bounds.p, binit, sizeof binit, cudaMemcpyHostToDevice, s));
-  k_master_boxes<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, c.master.tris.p, c.x.p, tboxes.p, bounds.p);
+  k_master_boxes<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, c.master.tris.p, c.X(), tboxes.p, bounds.p);
   keys.resize(nmt);
   keys_sorted.resize(nmt);
   idx.resize(nmt);
@@ -884,12 +884,12 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   cnt.zero(s);
   ovf.resize(1);
   ovf.zero(s);
-  k_query<0><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.x.p, r, nmt, nodes.p, left.p, right.p,
+  k_query<0><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
                                                  idx_sorted.p, cnt.p, nullptr, nullptr, ovf.p);
   exclusive_scan(cnt.p, c.pair_off[0].p, nst + 1, s);
   const int64_t ntri = last_of(c.pair_off[0], nst, s);
   c.pair_ids[0].resize(std::max<int64_t>(ntri, 1));
-  k_query<1><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.x.p, r, nmt, nodes.p, left.p, right.p,
+  k_query<1><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
                                                  idx_sorted.p, nullptr, c.pair_off[0].p, c.pair_ids[0].p, ovf.p);
   c.pair_ids[0].n = ntri;
   // K3: candidate edges / verts
@@ -929,7 +929,7 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
   cudaStream_t s = c.stream;
   const int32_t nst = c.slave.n_tris, nmv = c.master.n_verts;
   SamplerArgs A;
-  A.x = c.x.p;
+  A.x = c.X();
   A.eps_ref = eps_ref_dev;
   A.nst = nst;
   A.stris = c.slave.tris.p;

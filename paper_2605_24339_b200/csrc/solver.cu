@@ -1,0 +1,995 @@
+// Device-resident quasi-static solver: the reference's System::solve
+// (proj/include/gmcp/solver.hpp:125-228) with the LDL^T direct solve replaced
+// by a block-Jacobi preconditioned CG over 3x3 BCSR (K9), the linear elastic
+// operator (elasticity.hpp:39-141) as a constant BCSR (K11), and the contact
+// terms from the per-pair contexts (K6-K10). Positions, step, gradient and
+// every Krylov vector stay on the device for the whole run; the host reads
+// only scalars (residual, alpha, energy decrease, convergence) per iteration.
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <map>
+#include <memory>
+
+#include "../../include/gmcp_solver.h"
+#include "ctx.hpp"
+#include "kin.cuh"
+
+namespace gmcp_b200 {
+
+namespace {
+
+constexpr int kMaxPairs = 4;
+constexpr int kThreads = 256;
+constexpr int kBlocks = 592;  // fixed grid: deterministic reductions
+
+// ---------------------------------------------------------------------------
+// deterministic single-kernel reductions: per-block partials + "last block"
+// sums them in block order.
+
+struct RedSlot {
+  double* parts;          // [kBlocks * width]
+  unsigned int* counter;  // arrival counter (reset by the last block)
+};
+
+template <int W>
+__device__ __forceinline__ bool block_reduce_last(double (&v)[W], RedSlot rs, double (&out)[W]) {
+  __shared__ double sh[W][kThreads / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    double t = warp_sum(v[q]);
+    if (lane == 0) sh[q][wid] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      double t = 0;
+      for (int i = 0; i < kThreads / 32; ++i) t += sh[q][i];
+      rs.parts[blockIdx.x * W + q] = t;
+    }
+    __threadfence();
+    last = atomicAdd(rs.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    double t = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads) t += __ldcg(rs.parts + i * W + q);
+    t = warp_sum(t);
+    if (lane == 0) sh[q][wid] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      double t = 0;
+      for (int i = 0; i < kThreads / 32; ++i) t += sh[q][i];
+      out[q] = t;
+    }
+    *rs.counter = 0;
+  }
+  return true;  // out valid in thread 0 of the last block
+}
+
+// ---------------------------------------------------------------------------
+// BCSR descriptor (3x3 blocks, rows = vertices)
+
+struct Bcsr {
+  const int32_t* rowptr = nullptr;
+  const int32_t* cols = nullptr;
+  const double* vals = nullptr;
+};
+struct MatSet {
+  Bcsr el;
+  Bcsr c[kMaxPairs];
+  int np = 0;
+};
+
+__device__ __forceinline__ d3 bmv(const double* b, d3 p) {
+  return d3{b[0] * p.x + b[1] * p.y + b[2] * p.z, b[3] * p.x + b[4] * p.y + b[5] * p.z,
+            b[6] * p.x + b[7] * p.y + b[8] * p.z};
+}
+
+// y_v = sum_j A_vj p_j for one row, lanes stride the row's blocks, then a
+// fixed butterfly -> deterministic.
+__device__ __forceinline__ d3 row_mv(const Bcsr& A, int v, const double* __restrict__ p, int lane) {
+  d3 acc = mk3(0, 0, 0);
+  const int a = A.rowptr[v], b = A.rowptr[v + 1];
+  for (int k = a + lane; k < b; k += 32) acc = acc + bmv(A.vals + 9 * (int64_t)k, ld3(p, A.cols[k]));
+  return acc;
+}
+
+// K9a: q = mask .* (H p), partial dot p.q -> alpha = rz / pq (last block).
+__global__ void __launch_bounds__(kThreads) k_spmv_pq(int nv, MatSet M, const double* __restrict__ mask,
+                                                      const double* __restrict__ p, double* __restrict__ q,
+                                                      double* scal, RedSlot rs) {
+  const int lane = threadIdx.x & 31;
+  double dots[1] = {0};
+  const int nw = gridDim.x * (kThreads / 32);
+  for (int v = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); v < nv; v += nw) {
+    d3 acc = row_mv(M.el, v, p, lane);
+    for (int k = 0; k < M.np; ++k) acc = acc + row_mv(M.c[k], v, p, lane);
+    acc.x = warp_sum(acc.x);
+    acc.y = warp_sum(acc.y);
+    acc.z = warp_sum(acc.z);
+    if (lane == 0) {
+      const d3 m = ld3(mask, v);
+      const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
+      q[3 * v] = y.x;
+      q[3 * v + 1] = y.y;
+      q[3 * v + 2] = y.z;
+      dots[0] += dot(ld3(p, v), y);
+    }
+  }
+  double out[1];
+  if (block_reduce_last<1>(dots, rs, out) && threadIdx.x == 0) {
+    scal[1] = out[0];                                    // pq
+    scal[2] = out[0] != 0 ? scal[0] / out[0] : 0.0;      // alpha = rz / pq
+  }
+}
+
+// K9b: x += a p, r -= a q, z = Minv r, partial r.z, r.r -> beta (last block).
+__global__ void __launch_bounds__(kThreads) k_update(int nv, const double* __restrict__ p, const double* __restrict__ q,
+                                                     double* __restrict__ x, double* __restrict__ r,
+                                                     double* __restrict__ z, const double* __restrict__ minv,
+                                                     double* scal, RedSlot rs) {
+  const double a = scal[2];
+  double dots[2] = {0, 0};
+  for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
+    const d3 pv = ld3nc(p, v), qv = ld3nc(q, v);
+    d3 xv = ld3nc(x, v), rv = ld3nc(r, v);
+    xv = xv + a * pv;
+    rv = rv - a * qv;
+    const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
+    x[3 * v] = xv.x;
+    x[3 * v + 1] = xv.y;
+    x[3 * v + 2] = xv.z;
+    r[3 * v] = rv.x;
+    r[3 * v + 1] = rv.y;
+    r[3 * v + 2] = rv.z;
+    z[3 * v] = zv.x;
+    z[3 * v + 1] = zv.y;
+    z[3 * v + 2] = zv.z;
+    dots[0] += dot(rv, zv);
+    dots[1] += dot(rv, rv);
+  }
+  double out[2];
+  if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
+    const double rz_old = scal[0];
+    scal[3] = rz_old != 0 ? out[0] / rz_old : 0.0;  // beta
+    scal[0] = out[0];                                // rz
+    scal[4] = out[1];                                // rr
+  }
+}
+
+// K9c: p = z + beta p
+__global__ void k_pupdate(int64_t n, const double* __restrict__ z, double* __restrict__ p, const double* scal) {
+  const double b = scal[3];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + b * p[i];
+}
+
+// PCG init: r = b = -mask.*grad, z = Minv r, p = z, x = 0; rz, rr, bb.
+__global__ void __launch_bounds__(kThreads) k_pcg_init(int nv, const double* __restrict__ grad,
+                                                       const double* __restrict__ mask, const double* __restrict__ minv,
+                                                       double* __restrict__ x, double* __restrict__ r,
+                                                       double* __restrict__ z, double* __restrict__ p, double* scal,
+                                                       RedSlot rs) {
+  double dots[2] = {0, 0};
+  for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
+    const d3 m = ld3(mask, v), g = ld3(grad, v);
+    const d3 rv = mk3(-m.x * g.x, -m.y * g.y, -m.z * g.z);
+    const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
+    for (int k = 0; k < 3; ++k) x[3 * v + k] = 0;
+    r[3 * v] = rv.x;
+    r[3 * v + 1] = rv.y;
+    r[3 * v + 2] = rv.z;
+    z[3 * v] = p[3 * v] = zv.x;
+    z[3 * v + 1] = p[3 * v + 1] = zv.y;
+    z[3 * v + 2] = p[3 * v + 2] = zv.z;
+    dots[0] += dot(rv, zv);
+    dots[1] += dot(rv, rv);
+  }
+  double out[2];
+  if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
+    scal[0] = out[0];  // rz
+    scal[4] = out[1];  // rr
+    scal[5] = out[1];  // bb
+  }
+}
+
+// Block-Jacobi: Minv_v = inverse of the masked 3x3 diagonal block.
+__device__ __forceinline__ const double* find_diag(const Bcsr& A, int v) {
+  int lo = A.rowptr[v], hi = A.rowptr[v + 1];
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A.cols[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return (lo < A.rowptr[v + 1] && A.cols[lo] == v) ? A.vals + 9 * (int64_t)lo : nullptr;
+}
+
+__global__ void k_block_jacobi(int nv, MatSet M, const double* __restrict__ mask, double* __restrict__ minv) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    double D[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const double* e = find_diag(M.el, v);
+    if (e)
+      for (int q = 0; q < 9; ++q) D[q] = e[q];
+    for (int k = 0; k < M.np; ++k) {
+      const double* c = find_diag(M.c[k], v);
+      if (c)
+        for (int q = 0; q < 9; ++q) D[q] += c[q];
+    }
+    const double m[3] = {mask[3 * v], mask[3 * v + 1], mask[3 * v + 2]};
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        if (m[a] == 0 || m[b] == 0) D[3 * a + b] = (a == b) ? 1.0 : 0.0;
+      }
+    const double c00 = D[4] * D[8] - D[5] * D[7], c01 = D[2] * D[7] - D[1] * D[8], c02 = D[1] * D[5] - D[2] * D[4];
+    const double c10 = D[5] * D[6] - D[3] * D[8], c11 = D[0] * D[8] - D[2] * D[6], c12 = D[2] * D[3] - D[0] * D[5];
+    const double c20 = D[3] * D[7] - D[4] * D[6], c21 = D[1] * D[6] - D[0] * D[7], c22 = D[0] * D[4] - D[1] * D[3];
+    const double det = D[0] * c00 + D[1] * c10 + D[2] * c20;
+    double* o = minv + 9 * (int64_t)v;
+    if (det != 0 && isfinite(det)) {
+      const double id = 1.0 / det;
+      o[0] = c00 * id; o[1] = c01 * id; o[2] = c02 * id;
+      o[3] = c10 * id; o[4] = c11 * id; o[5] = c12 * id;
+      o[6] = c20 * id; o[7] = c21 * id; o[8] = c22 * id;
+    } else {  // point Jacobi fallback
+      for (int q = 0; q < 9; ++q) o[q] = 0;
+      for (int a = 0; a < 3; ++a) o[4 * a] = D[4 * a] != 0 ? 1.0 / D[4 * a] : 1.0;
+    }
+  }
+}
+
+// Elastic gradient K_el (x - rest) -> grad = g_el + sum_pairs g_c - lambda f_ext.
+// Also residual = max |grad_d| over free dofs (order-free max).
+__global__ void k_grad_total(int nv, Bcsr K, const double* __restrict__ x, const double* __restrict__ rest,
+                             const double* __restrict__ fext, double lambda, const double* const* __restrict__ gc,
+                             int np, const double* __restrict__ mask, double* __restrict__ gel,
+                             double* __restrict__ grad, unsigned long long* red) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long best = 0;
+  const int nw = gridDim.x * (blockDim.x / 32);
+  for (int v = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); v < nv; v += nw) {
+    d3 acc = mk3(0, 0, 0);
+    for (int k = K.rowptr[v] + lane; k < K.rowptr[v + 1]; k += 32) {
+      const int j = K.cols[k];
+      acc = acc + bmv(K.vals + 9 * (int64_t)k, ld3(x, j) - ld3(rest, j));
+    }
+    acc.x = warp_sum(acc.x);
+    acc.y = warp_sum(acc.y);
+    acc.z = warp_sum(acc.z);
+    if (lane == 0) {
+      gel[3 * v] = acc.x;
+      gel[3 * v + 1] = acc.y;
+      gel[3 * v + 2] = acc.z;
+      double g[3] = {acc.x, acc.y, acc.z};
+      for (int k = 0; k < np; ++k)
+        for (int a = 0; a < 3; ++a) g[a] += gc[k][3 * v + a];
+      for (int a = 0; a < 3; ++a) {
+        g[a] -= lambda * fext[3 * v + a];
+        grad[3 * v + a] = g[a];
+        if (mask[3 * v + a] != 0) {
+          const unsigned long long b = ord_bits(fabs(g[a]));
+          best = b > best ? b : best;
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (lane == 0) atomicMax(red, best);
+}
+
+// Scalars for the line search: out = [g_el.dx, dx.K dx, f.dx] (K dx via SpMV).
+__global__ void __launch_bounds__(kThreads) k_ls_coeffs(int nv, Bcsr K, const double* __restrict__ dx,
+                                                        const double* __restrict__ gel,
+                                                        const double* __restrict__ fext, double* out, RedSlot rs) {
+  const int lane = threadIdx.x & 31;
+  double d[3] = {0, 0, 0};
+  const int nw = gridDim.x * (kThreads / 32);
+  for (int v = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); v < nv; v += nw) {
+    d3 acc = row_mv(K, v, dx, lane);
+    acc.x = warp_sum(acc.x);
+    acc.y = warp_sum(acc.y);
+    acc.z = warp_sum(acc.z);
+    if (lane == 0) {
+      const d3 dv = ld3(dx, v);
+      d[0] += dot(ld3(gel, v), dv);
+      d[1] += dot(dv, acc);
+      d[2] += dot(ld3(fext, v), dv);
+    }
+  }
+  double o[3];
+  if (block_reduce_last<3>(d, rs, o) && threadIdx.x == 0)
+    for (int q = 0; q < 3; ++q) out[q] = o[q];
+}
+
+// Elastic energy 0.5 u.(K u) and external work f.u, u = x - rest.
+__global__ void __launch_bounds__(kThreads) k_energy_el(int nv, const double* __restrict__ gel,
+                                                        const double* __restrict__ x, const double* __restrict__ rest,
+                                                        const double* __restrict__ fext, double* out, RedSlot rs) {
+  double d[2] = {0, 0};
+  for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
+    const d3 u = ld3(x, v) - ld3(rest, v);
+    d[0] += dot(ld3(gel, v), u);
+    d[1] += dot(ld3(fext, v), u);
+  }
+  double o[2];
+  if (block_reduce_last<2>(d, rs, o) && threadIdx.x == 0) {
+    out[0] = 0.5 * o[0];
+    out[1] = o[1];
+  }
+}
+
+__global__ void k_axpy_to(int64_t n, const double* __restrict__ x, double a, const double* __restrict__ dx,
+                          double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = x[i] + a * dx[i];
+}
+
+// max |x_v - ref_v| over a vertex list (pair_motion, solver.hpp:279-290)
+__global__ void k_motion(int64_t n, const int32_t* __restrict__ verts, const double* __restrict__ x,
+                         const double* __restrict__ ref, unsigned long long* red) {
+  unsigned long long best = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = verts[i];
+    const unsigned long long b = ord_bits(norm(ld3(x, v) - ld3(ref, v)));
+    best = b > best ? b : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(red, best);
+}
+
+int grid_for(int64_t n, int threads) {
+  const int64_t b = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
+}
+
+}  // namespace
+
+// ===========================================================================
+
+struct Body {
+  std::vector<double> verts;  // rest (local)
+  std::vector<int32_t> tets;
+  double E, nu, lambda, mu;
+  int32_t offset, nv;
+  std::vector<double> vol;   // per tet
+  std::vector<double> grads; // per tet [4][3]
+};
+
+struct PairRt {
+  std::unique_ptr<Ctx> c;
+  gmcp_barrier_params params;
+  DBuf<double> ref_pos;      // positions at sampling time
+  DBuf<int32_t> motion_verts;  // slave.verts ++ master.verts
+};
+
+struct SystemImpl {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n_dof = 0;
+  int64_t launches = 0;
+  std::vector<Body> bodies;
+  std::vector<double> rest, f_ext, dirichlet;
+  std::vector<uint8_t> fixed;
+  std::vector<std::unique_ptr<PairRt>> pairs;
+  // device
+  DBuf<double> x, dx, xtry, rest_d, fext_d, mask_d, grad, gel, r, z, p, q, minv, scal, parts, lsco, eel;
+  DBuf<unsigned int> counter;
+  DBuf<unsigned long long> redu;
+  DBuf<int32_t> k_rowptr, k_cols;
+  DBuf<double> k_vals;
+  DBuf<const double*> gc_ptrs;
+  bool el_built = false;
+  int64_t el_nnzb = 0;
+  std::vector<double> x_host;
+  // stats of the last solve
+  int64_t pcg_iters_total = 0;
+
+  int nv() const { return (int)(n_dof / 3); }
+  void sync() { GMCP_CUDA(cudaStreamSynchronize(stream)); }
+  RedSlot slot(int off) {
+    return RedSlot{parts.p, counter.p + off};
+  }
+};
+
+namespace {
+
+// elasticity.hpp:20-31
+void make_material(double E, double nu, double& lambda, double& mu) {
+  if (!(E > 0)) throw StatusError(GMCP_ERR_CONFIG, "material: Young's modulus must be positive");
+  if (!(nu > -1.0) || nu >= 0.5 - 1e-6)
+    throw StatusError(GMCP_ERR_CONFIG, "material: Poisson ratio must lie in (-1, 0.5 - 1e-6)");
+  lambda = E * nu / ((1 + nu) * (1 - 2 * nu));
+  mu = E / (2 * (1 + nu));
+}
+
+// elasticity.hpp:39-61 (rest shape-function gradients)
+void build_operators(Body& b) {
+  const int64_t nt = (int64_t)b.tets.size() / 4;
+  b.vol.resize(nt);
+  b.grads.resize(12 * nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    const int32_t* tt = &b.tets[4 * t];
+    double D[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int r = 0; r < 3; ++r) D[r][i] = b.verts[3 * tt[i + 1] + r] - b.verts[3 * tt[0] + r];
+    const double det = D[0][0] * (D[1][1] * D[2][2] - D[2][1] * D[1][2]) -
+                       D[1][0] * (D[0][1] * D[2][2] - D[2][1] * D[0][2]) +
+                       D[2][0] * (D[0][1] * D[1][2] - D[1][1] * D[0][2]);
+    b.vol[t] = det / 6.0;
+    if (!(b.vol[t] > 0))
+      throw StatusError(GMCP_ERR_DEGENERATE, "build_element_operators: non-positive tet volume at tet " +
+                                                 std::to_string(t));
+    double G[3][3];  // inverse of D
+    G[0][0] = (D[1][1] * D[2][2] - D[1][2] * D[2][1]) / det;
+    G[0][1] = (D[0][2] * D[2][1] - D[0][1] * D[2][2]) / det;
+    G[0][2] = (D[0][1] * D[1][2] - D[0][2] * D[1][1]) / det;
+    G[1][0] = (D[1][2] * D[2][0] - D[1][0] * D[2][2]) / det;
+    G[1][1] = (D[0][0] * D[2][2] - D[0][2] * D[2][0]) / det;
+    G[1][2] = (D[0][2] * D[1][0] - D[0][0] * D[1][2]) / det;
+    G[2][0] = (D[1][0] * D[2][1] - D[1][1] * D[2][0]) / det;
+    G[2][1] = (D[0][1] * D[2][0] - D[0][0] * D[2][1]) / det;
+    G[2][2] = (D[0][0] * D[1][1] - D[0][1] * D[1][0]) / det;
+    double* g = &b.grads[12 * t];
+    for (int k = 0; k < 3; ++k) g[k] = 0;
+    for (int i = 0; i < 3; ++i)
+      for (int k = 0; k < 3; ++k) {
+        g[3 * (i + 1) + k] = G[i][k];
+        g[k] -= G[i][k];
+      }
+  }
+}
+
+// Constant elastic BCSR (elasticity.hpp:124-141), blocks summed in tet order.
+void build_elastic(SystemImpl& S) {
+  const int nv = S.nv();
+  std::vector<std::vector<std::pair<int32_t, std::array<double, 9>>>> rows(nv);
+  for (const Body& b : S.bodies) {
+    const int64_t nt = (int64_t)b.tets.size() / 4;
+    for (int64_t t = 0; t < nt; ++t) {
+      const double* g = &b.grads[12 * t];
+      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+          const double* gi = g + 3 * i;
+          const double* gj = g + 3 * j;
+          const double gg = gi[0] * gj[0] + gi[1] * gj[1] + gi[2] * gj[2];
+          std::array<double, 9> blk;
+          for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c)
+              blk[3 * r + c] = b.vol[t] * (b.lambda * gi[r] * gj[c] + b.mu * gj[r] * gi[c] + (r == c ? b.mu * gg : 0.0));
+          const int32_t bi = b.offset + b.tets[4 * t + i], bj = b.offset + b.tets[4 * t + j];
+          auto& row = rows[bi];
+          auto it = std::find_if(row.begin(), row.end(), [&](const auto& e) { return e.first == bj; });
+          if (it == row.end()) {
+            row.push_back({bj, blk});
+          } else {
+            for (int q = 0; q < 9; ++q) it->second[q] += blk[q];
+          }
+        }
+    }
+  }
+  std::vector<int32_t> rowptr(nv + 1, 0), cols;
+  std::vector<double> vals;
+  for (int v = 0; v < nv; ++v) {
+    auto& row = rows[v];
+    std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (const auto& e : row) {
+      cols.push_back(e.first);
+      vals.insert(vals.end(), e.second.begin(), e.second.end());
+    }
+    rowptr[v + 1] = (int32_t)cols.size();
+  }
+  S.k_rowptr.upload(rowptr, S.stream);
+  S.k_cols.upload(cols, S.stream);
+  S.k_vals.upload(vals, S.stream);
+  S.el_nnzb = (int64_t)cols.size();
+  S.el_built = true;
+}
+
+MatSet mats(SystemImpl& S) {
+  MatSet M;
+  M.el = Bcsr{S.k_rowptr.p, S.k_cols.p, S.k_vals.p};
+  M.np = (int)S.pairs.size();
+  for (int k = 0; k < M.np; ++k) {
+    const AssemblyPlan& P = S.pairs[k]->c->plan;
+    M.c[k] = Bcsr{P.rowptr.p, P.cols.p, P.vals.p};
+  }
+  return M;
+}
+
+// solver.hpp:256-269
+double derived_newton_tol(const SystemImpl& S) {
+  double scale = 0;
+  for (double f : S.f_ext) scale = std::max(scale, std::abs(f));
+  double vol_sum = 0, e_max = 0;
+  long n_elem = 0;
+  for (const Body& b : S.bodies) {
+    for (double v : b.vol) vol_sum += v;
+    n_elem += (long)b.vol.size();
+    e_max = std::max(e_max, b.E);
+  }
+  const double h = std::cbrt(6.0 * vol_sum / std::max<long>(n_elem, 1));
+  scale = std::max(scale, 1e-6 * e_max * h * h);
+  return 1e-6 * std::max(scale, 1e-6);
+}
+
+void rebuild_pair(SystemImpl& S, PairRt& pr, const double* eps_ref_dev) {
+  Ctx& c = *pr.c;
+  int64_t counts[3];
+  run_broadphase(c, pr.params.detection_radius, counts);
+  run_sampler(c, eps_ref_dev);
+  c.plan.valid = false;
+  build_assembly_plan(c);
+  pr.ref_pos.resize(S.n_dof);
+  GMCP_CUDA(cudaMemcpyAsync(pr.ref_pos.p, S.x.p, S.n_dof * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
+}
+
+// Returns {feasible, contact energy sum, min gap} at positions xp.
+struct CE {
+  bool feasible;
+  double energy, min_gap;
+};
+CE contact_energy_at(SystemImpl& S, double* xp) {
+  CE o{true, 0.0, 1.7976931348623157e308};
+  for (auto& pr : S.pairs) {
+    Ctx& c = *pr->c;
+    double* saved = c.x_ext;
+    c.x_ext = xp;
+    const EnergyOut e = run_energy(c, false);
+    c.x_ext = saved;
+    if (e.first_degenerate >= 0 && (e.first_bad < 0 || e.first_degenerate < e.first_bad))
+      throw StatusError(GMCP_ERR_DEGENERATE, "contact sample on a degenerate slave triangle");
+    o.min_gap = std::min(o.min_gap, e.min_gap);
+    if (e.first_bad >= 0) {
+      o.feasible = false;
+      return o;
+    }
+    o.energy += e.energy;
+  }
+  return o;
+}
+
+// Elastic + external energy at S.x (gel must hold K (x - rest)).
+void elastic_terms(SystemImpl& S, double& e_el, double& work) {
+  k_energy_el<<<kBlocks, kThreads, 0, S.stream>>>(S.nv(), S.gel.p, S.x.p, S.rest_d.p, S.fext_d.p, S.eel.p, S.slot(0));
+  ++S.launches;
+  double h[2];
+  GMCP_CUDA(cudaMemcpyAsync(h, S.eel.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
+  S.sync();
+  e_el = h[0];
+  work = h[1];
+}
+
+// grad = K u + sum contact grads - lambda f ; returns residual (max |grad| free)
+double assemble(SystemImpl& S, double lambda) {
+  std::vector<const double*> gp;
+  for (auto& pr : S.pairs) {
+    int64_t bad = -1;
+    run_assembly(*pr->c, 1, &bad);
+    gp.push_back(pr->c->grad.p);
+  }
+  S.gc_ptrs.resize(std::max<size_t>(gp.size(), 1));
+  if (!gp.empty())
+    GMCP_CUDA(cudaMemcpyAsync(S.gc_ptrs.p, gp.data(), gp.size() * sizeof(double*), cudaMemcpyHostToDevice, S.stream));
+  GMCP_CUDA(cudaMemsetAsync(S.redu.p, 0, sizeof(unsigned long long), S.stream));
+  k_grad_total<<<grid_for((int64_t)S.nv() * 32, 256), 256, 0, S.stream>>>(
+      S.nv(), Bcsr{S.k_rowptr.p, S.k_cols.p, S.k_vals.p}, S.x.p, S.rest_d.p, S.fext_d.p, lambda, S.gc_ptrs.p,
+      (int)gp.size(), S.mask_d.p, S.gel.p, S.grad.p, S.redu.p);
+  ++S.launches;
+  unsigned long long u;
+  GMCP_CUDA(cudaMemcpyAsync(&u, S.redu.p, sizeof u, cudaMemcpyDeviceToHost, S.stream));
+  S.sync();
+  return from_ord_bits(u);
+}
+
+// Block-Jacobi PCG on the masked system. Returns iterations; dx in S.dx.
+int pcg(SystemImpl& S, double tol, int maxit, double* rel_out) {
+  const int nv = S.nv();
+  const MatSet M = mats(S);
+  k_block_jacobi<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, M, S.mask_d.p, S.minv.p);
+  k_pcg_init<<<kBlocks, kThreads, 0, S.stream>>>(nv, S.grad.p, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p, S.p.p,
+                                                 S.scal.p, S.slot(0));
+  S.launches += 2;
+  double h[6];
+  GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
+  S.sync();
+  const double bb = h[5];
+  if (bb == 0) {
+    *rel_out = 0;
+    return 0;
+  }
+  const double target = tol * tol * bb;
+  int it = 0;
+  const int chunk = 8;
+  const int gsp = grid_for((int64_t)nv * 32, kThreads);
+  while (it < maxit) {
+    for (int k = 0; k < chunk && it < maxit; ++k, ++it) {
+      k_spmv_pq<<<std::min(gsp, kBlocks), kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.p.p, S.q.p, S.scal.p,
+                                                                    S.slot(1));
+      k_update<<<kBlocks, kThreads, 0, S.stream>>>(nv, S.p.p, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
+                                                  S.slot(2));
+      k_pupdate<<<grid_for(S.n_dof, 256), 256, 0, S.stream>>>(S.n_dof, S.z.p, S.p.p, S.scal.p);
+      S.launches += 3;
+    }
+    GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
+    S.sync();
+    if (!(h[4] > target)) break;  // rr <= tol^2 bb (or NaN guard below)
+    if (!std::isfinite(h[4])) throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
+  }
+  *rel_out = std::sqrt(h[4] / bb);
+  GMCP_CUDA(cudaGetLastError());
+  return it;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// solve loop (solver.hpp:125-228)
+
+void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callback cb, void* user,
+                  gmcp_run_stats* out) {
+  if (S.bodies.empty()) throw StatusError(GMCP_ERR_CONFIG, "solve: no bodies");
+  if (st.load_steps < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: load_steps must be >= 1");
+  if (st.max_newton_iters < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: max_newton_iters must be >= 1");
+  if (st.max_line_search < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: max_line_search must be >= 1");
+  const auto t_start = std::chrono::steady_clock::now();
+  const double tol = st.newton_tol > 0 ? st.newton_tol : derived_newton_tol(S);
+  int64_t n_free = 0;
+  for (uint8_t f : S.fixed) n_free += f == 0;
+  if (n_free == 0) throw StatusError(GMCP_ERR_CONFIG, "solve: no free degrees of freedom");
+  if (!S.el_built) build_elastic(S);
+  // fixed dofs at their targets (solver.hpp:139-140)
+  for (int64_t d = 0; d < S.n_dof; ++d)
+    if (S.fixed[d]) S.x_host[d] = S.dirichlet[d];
+  const int64_t n = S.n_dof;
+  for (auto* b : {&S.x, &S.dx, &S.xtry, &S.grad, &S.gel, &S.r, &S.z, &S.p, &S.q}) b->resize(n);
+  S.minv.resize(3 * n);
+  S.scal.resize(16);
+  S.eel.resize(4);
+  S.lsco.resize(4);
+  S.parts.resize(kBlocks * 4);
+  S.counter.resize(8);
+  S.counter.zero(S.stream);
+  S.redu.resize(4);
+  S.x.upload(S.x_host, S.stream);
+  S.dx.zero(S.stream);
+  S.rest_d.upload(S.rest, S.stream);
+  S.fext_d.upload(S.f_ext, S.stream);
+  std::vector<double> mask(n);
+  for (int64_t d = 0; d < n; ++d) mask[d] = S.fixed[d] ? 0.0 : 1.0;
+  S.mask_d.upload(mask, S.stream);
+  DBuf<double> eps_ref;  // run-start positions anchor every support radius (solver.hpp:146)
+  eps_ref.resize(n);
+  GMCP_CUDA(cudaMemcpyAsync(eps_ref.p, S.x.p, n * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
+  for (auto& pr : S.pairs) {
+    pr->c->x_ext = S.x.p;
+    pr->c->dx_ext = S.dx.p;
+    pr->c->n_dof = n;
+    pr->c->stream = S.stream;
+  }
+  out->total_newton_iters = 0;
+  out->total_rebuilds = 0;
+  out->total_pcg_iters = 0;
+  out->newton_tol_used = tol;
+  for (int step = 1; step <= st.load_steps; ++step) {
+    const double lambda = (double)step / st.load_steps;
+    gmcp_step_stats ss{};
+    ss.step = step;
+    ss.min_gap = 1.7976931348623157e308;
+    ss.energy_monotone = 1;
+    for (auto& pr : S.pairs) rebuild_pair(S, *pr, eps_ref.p);
+    // total energy at x (solver.hpp:154): elastic via K u, contact, external work
+    double resid = assemble(S, lambda);
+    double e_el, work;
+    elastic_terms(S, e_el, work);
+    CE ce = contact_energy_at(S, S.x.p);
+    if (!ce.feasible) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
+    double energy = e_el + ce.energy - lambda * work;
+    ss.min_gap = std::min(ss.min_gap, ce.min_gap);
+    bool converged = false;
+    for (int it = 0; it < st.max_newton_iters; ++it) {
+      if (it > 0) resid = assemble(S, lambda);
+      if (resid <= tol) {
+        converged = true;
+        break;
+      }
+      double rel;
+      const int pit = pcg(S, st.pcg_tol, st.pcg_max_iters, &rel);
+      ss.pcg_iters += pit;
+      ss.newton_iters += 1;
+      double alpha = 1.0;
+      for (auto& pr : S.pairs) {
+        alpha = std::min(alpha, run_step_filter(*pr->c));
+        alpha = std::min(alpha, run_displacement_cap(*pr->c));
+      }
+      // line search on the exact energy decrease:
+      // dE(a) = a g_el.dx + a^2/2 dx.K dx - lambda a f.dx + Psi(x + a dx) - Psi(x)
+      k_ls_coeffs<<<kBlocks, kThreads, 0, S.stream>>>(S.nv(), Bcsr{S.k_rowptr.p, S.k_cols.p, S.k_vals.p}, S.dx.p,
+                                                      S.gel.p, S.fext_d.p, S.lsco.p, S.slot(3));
+      ++S.launches;
+      double co[3];
+      GMCP_CUDA(cudaMemcpyAsync(co, S.lsco.p, sizeof co, cudaMemcpyDeviceToHost, S.stream));
+      S.sync();
+      bool accepted = false;
+      for (int ls = 0; ls < st.max_line_search; ++ls) {
+        k_axpy_to<<<grid_for(n, 256), 256, 0, S.stream>>>(n, S.x.p, alpha, S.dx.p, S.xtry.p);
+        ++S.launches;
+        const CE t = contact_energy_at(S, S.xtry.p);
+        if (t.feasible) {
+          const double dE = alpha * co[0] + 0.5 * alpha * alpha * co[1] - lambda * alpha * co[2] + (t.energy - ce.energy);
+          if (dE < 0) {
+            GMCP_CUDA(cudaMemcpyAsync(S.x.p, S.xtry.p, n * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
+            energy += dE;
+            ce = t;
+            ss.min_gap = std::min(ss.min_gap, t.min_gap);
+            accepted = true;
+            break;
+          }
+        }
+        ss.backtracks += 1;
+        alpha *= 0.5;
+      }
+      if (!accepted) {
+        out->residual = resid;
+        throw StatusError(GMCP_ERR_SOLVER, "load step " + std::to_string(step) +
+                                               ": line search failed to find a feasible decrease");
+      }
+      // re-sample pairs whose vertices outran the frozen sampling (solver.hpp:201-209)
+      bool rebuilt = false;
+      for (auto& pr : S.pairs) {
+        const int64_t m = (int64_t)pr->motion_verts.n;
+        GMCP_CUDA(cudaMemsetAsync(S.redu.p + 1, 0, sizeof(unsigned long long), S.stream));
+        if (m) {
+          k_motion<<<grid_for(m, 256), 256, 0, S.stream>>>(m, pr->motion_verts.p, S.x.p, pr->ref_pos.p, S.redu.p + 1);
+          ++S.launches;
+        }
+        unsigned long long u;
+        GMCP_CUDA(cudaMemcpyAsync(&u, S.redu.p + 1, sizeof u, cudaMemcpyDeviceToHost, S.stream));
+        S.sync();
+        if (from_ord_bits(u) > 0.5 * pr->params.eps_max) {
+          rebuild_pair(S, *pr, eps_ref.p);
+          rebuilt = true;
+          ss.rebuilds += 1;
+        }
+      }
+      if (rebuilt) {
+        resid = assemble(S, lambda);
+        elastic_terms(S, e_el, work);
+        ce = contact_energy_at(S, S.x.p);
+        if (!ce.feasible) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
+        energy = e_el + ce.energy - lambda * work;
+      }
+    }
+    if (!converged) {
+      out->residual = resid;
+      throw StatusError(GMCP_ERR_SOLVER, "load step " + std::to_string(step) + ": Newton exceeded " +
+                                             std::to_string(st.max_newton_iters) + " iterations");
+    }
+    // report the energy recomputed at the converged state
+    elastic_terms(S, e_el, work);
+    energy = e_el + ce.energy - lambda * work;
+    ss.residual = resid;
+    ss.energy = energy;
+    out->total_newton_iters += ss.newton_iters;
+    out->total_rebuilds += ss.rebuilds;
+    out->total_pcg_iters += ss.pcg_iters;
+    S.x.download(S.x_host.data(), n, S.stream);
+    S.sync();
+    if (cb) cb(&ss, S.x_host.data(), n, user);
+  }
+  S.x.download(S.x_host.data(), n, S.stream);
+  S.sync();
+  out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+}  // namespace gmcp_b200
+
+// ===========================================================================
+// C-ABI (include/gmcp_solver.h)
+
+using namespace gmcp_b200;
+
+struct gmcp_system {
+  SystemImpl s;
+};
+
+namespace {
+thread_local std::string g_serr;
+template <class F>
+int sguard(F&& f) {
+  try {
+    return f();
+  } catch (const StatusError& e) {
+    g_serr = e.what();
+    return e.code;
+  } catch (const CudaError& e) {
+    g_serr = e.what();
+    return GMCP_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_serr = e.what();
+    return GMCP_ERR_ARG;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* gmcp_system_last_error(void) { return g_serr.c_str(); }
+
+int gmcp_system_create(int device, gmcp_system** out) {
+  return sguard([&] {
+    int nd = 0;
+    GMCP_CUDA(cudaGetDeviceCount(&nd));
+    if (device < 0 || device >= nd) throw StatusError(GMCP_ERR_CUDA, "no such CUDA device");
+    GMCP_CUDA(cudaSetDevice(device));
+    auto* s = new gmcp_system;
+    s->s.device = device;
+    GMCP_CUDA(cudaStreamCreateWithFlags(&s->s.stream, cudaStreamNonBlocking));
+    *out = s;
+    return GMCP_OK;
+  });
+}
+
+void gmcp_system_destroy(gmcp_system* s) {
+  if (!s) return;
+  cudaSetDevice(s->s.device);
+  cudaStreamSynchronize(s->s.stream);
+  cudaStream_t st = s->s.stream;
+  for (auto& pr : s->s.pairs) pr->c->stream = nullptr;
+  delete s;
+  cudaStreamDestroy(st);
+}
+
+int gmcp_system_add_body(gmcp_system* sys, const double* verts, int64_t nv, const int32_t* tets, int64_t nt, double E,
+                         double nu, int32_t* vertex_offset) {
+  return sguard([&] {
+    SystemImpl& S = sys->s;
+    Body b;
+    make_material(E, nu, b.lambda, b.mu);
+    b.E = E;
+    b.nu = nu;
+    b.verts.assign(verts, verts + 3 * nv);
+    b.tets.assign(tets, tets + 4 * nt);
+    for (int64_t i = 0; i < 4 * nt; ++i)
+      if (b.tets[i] < 0 || b.tets[i] >= nv) throw StatusError(GMCP_ERR_ARG, "tet vertex id out of range");
+    b.offset = (int32_t)(S.n_dof / 3);
+    b.nv = (int32_t)nv;
+    build_operators(b);
+    S.rest.insert(S.rest.end(), verts, verts + 3 * nv);
+    S.n_dof = (int64_t)S.rest.size();
+    S.x_host = S.rest;
+    S.f_ext.assign(S.n_dof, 0.0);
+    S.fixed.assign(S.n_dof, 0);
+    S.dirichlet = S.rest;
+    if (vertex_offset) *vertex_offset = b.offset;
+    S.bodies.push_back(std::move(b));
+    S.el_built = false;
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_fix_dofs(gmcp_system* sys, int64_t n, const int64_t* dofs, const double* targets) {
+  return sguard([&] {
+    SystemImpl& S = sys->s;
+    for (int64_t i = 0; i < n; ++i) {
+      if (dofs[i] < 0 || dofs[i] >= S.n_dof) throw StatusError(GMCP_ERR_ARG, "dof out of range");
+      S.fixed[dofs[i]] = 1;
+      S.dirichlet[dofs[i]] = targets[i];
+    }
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_set_external_force(gmcp_system* sys, const double* f, int64_t n_dof) {
+  return sguard([&] {
+    SystemImpl& S = sys->s;
+    if (n_dof != S.n_dof) throw StatusError(GMCP_ERR_ARG, "f_ext size mismatch");
+    S.f_ext.assign(f, f + n_dof);
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_add_contact_pair(gmcp_system* sys, const gmcp_surface* slave, const gmcp_surface* master,
+                                 const gmcp_barrier_params* resolved, int32_t* pair_id) {
+  return sguard([&] {
+    SystemImpl& S = sys->s;
+    if ((int)S.pairs.size() >= kMaxPairs) throw StatusError(GMCP_ERR_CONFIG, "too many contact pairs");
+    auto pr = std::make_unique<PairRt>();
+    pr->c = std::make_unique<Ctx>();
+    Ctx& c = *pr->c;
+    c.device = S.device;
+    c.stream = S.stream;
+    c.params = *resolved;
+    c.have_params = true;
+    pr->params = *resolved;
+    auto up = [&](DevSurface& d, const gmcp_surface* s) {
+      d.n_tris = s->n_tris;
+      d.n_edges = s->n_edges;
+      d.n_verts = s->n_verts;
+      d.h_tris.assign(s->tris, s->tris + 3 * (size_t)s->n_tris);
+      d.h_tri_edges.assign(s->tri_edges, s->tri_edges + 3 * (size_t)s->n_tris);
+      d.h_edges.assign(s->edges, s->edges + 2 * (size_t)s->n_edges);
+      d.h_verts.assign(s->verts, s->verts + s->n_verts);
+      d.tris.upload(d.h_tris, S.stream);
+      d.tri_edges.upload(d.h_tri_edges, S.stream);
+      d.edges.upload(d.h_edges, S.stream);
+      d.verts.upload(d.h_verts, S.stream);
+    };
+    up(c.slave, slave);
+    up(c.master, master);
+    std::vector<int32_t> mv(c.slave.h_verts);
+    mv.insert(mv.end(), c.master.h_verts.begin(), c.master.h_verts.end());
+    pr->motion_verts.upload(mv, S.stream);
+    S.sync();
+    if (pair_id) *pair_id = (int32_t)S.pairs.size();
+    S.pairs.push_back(std::move(pr));
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_solve(gmcp_system* sys, const gmcp_solver_settings* st, gmcp_step_callback cb, void* user,
+                      gmcp_run_stats* out) {
+  return sguard([&] {
+    system_solve(sys->s, *st, cb, user, out);
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_positions(gmcp_system* sys, double* x, int64_t n_dof) {
+  return sguard([&] {
+    if (n_dof != sys->s.n_dof) throw StatusError(GMCP_ERR_ARG, "size mismatch");
+    std::copy(sys->s.x_host.begin(), sys->s.x_host.end(), x);
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_set_positions(gmcp_system* sys, const double* x, int64_t n_dof) {
+  return sguard([&] {
+    if (n_dof != sys->s.n_dof) throw StatusError(GMCP_ERR_ARG, "size mismatch");
+    sys->s.x_host.assign(x, x + n_dof);
+    return GMCP_OK;
+  });
+}
+
+int64_t gmcp_system_num_samples(gmcp_system* sys, int32_t pair) {
+  if (!sys || pair < 0 || pair >= (int)sys->s.pairs.size()) return -1;
+  return sys->s.pairs[pair]->c->ns;
+}
+
+int gmcp_system_pair_force_summary(gmcp_system* sys, int32_t pair, double* out12) {
+  return sguard([&] {
+    SystemImpl& S = sys->s;
+    if (pair < 0 || pair >= (int)S.pairs.size()) throw StatusError(GMCP_ERR_ARG, "no such pair");
+    Ctx& c = *S.pairs[pair]->c;
+    run_force_summary(c, out12);
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_pair_pressure(gmcp_system* sys, int32_t pair, int64_t* n, gmcp_pressure_record* out) {
+  return sguard([&] {
+    SystemImpl& S = sys->s;
+    if (pair < 0 || pair >= (int)S.pairs.size()) throw StatusError(GMCP_ERR_ARG, "no such pair");
+    Ctx& c = *S.pairs[pair]->c;
+    *n = (int64_t)c.face_idx.n;
+    if (out) run_pressure(c, out);
+    return GMCP_OK;
+  });
+}
+
+int64_t gmcp_system_launch_count(const gmcp_system* sys) {
+  if (!sys) return 0;
+  int64_t n = sys->s.launches;
+  for (auto& pr : sys->s.pairs) n += pr->c->launches;
+  return n;
+}
+
+}  // extern "C"

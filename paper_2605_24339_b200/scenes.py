@@ -226,8 +226,8 @@ def slab_scene(nb: int, nt: int, texture_amp: float = 0.0, texture_freq: float =
     rest = np.concatenate([bottom.vertices.ravel(), top.vertices.ravel()]).astype(np.float64)
     sb = extract_boundary_surface(bottom)
     stp = extract_boundary_surface(top)
-    down = [t for t in range(stp.triangles.shape[0])
-            if np.all(np.abs(top.vertices[stp.vertex_map[stp.triangles[t]], 2] - 0.102) < 1e-9)]
+    zt = top.vertices[stp.vertex_map[stp.triangles], 2]
+    down = np.nonzero(np.all(np.abs(zt - 0.102) < 1e-9, axis=1))[0]
     slave = make_contact_surface(stp, off_top, down)
     master = make_contact_surface(sb, 0)
     params = resolve_barrier_params(BarrierParams(kappa_face=kappa_face, eps_max=eps_max),

@@ -1,0 +1,308 @@
+"""Host mirror of gmcp::System (proj/include/gmcp/solver.hpp:63-376) over the
+device-resident solver C-ABI (include/gmcp_solver.h), plus the patch-test
+scene of bench.hpp:44-124 / scene.hpp:381-449.
+
+Same names and argument meaning as the reference: add_body, fix_dof,
+fix_vertex, add_contact_pair, solve(settings, on_step) -> RunStats, with the
+reference exceptions (ConfigError, SolverError{residual}). The linear solve
+is a block-Jacobi PCG on the GPU instead of SimplicialLDLT.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import gmcp as _g
+from . import scenes as S
+
+
+@dataclass
+class SolverSettings:
+    """solver.hpp:35-42 + PCG controls."""
+
+    load_steps: int = 10
+    max_newton_iters: int = 200
+    newton_tol: float = -1.0
+    max_line_search: int = 40
+    pcg_tol: float = 1e-10
+    pcg_max_iters: int = 20000
+
+
+class _Settings(C.Structure):
+    _fields_ = [("load_steps", C.c_int32), ("max_newton_iters", C.c_int32), ("newton_tol", C.c_double),
+                ("max_line_search", C.c_int32), ("pcg_tol", C.c_double), ("pcg_max_iters", C.c_int32)]
+
+
+class _StepStats(C.Structure):
+    _fields_ = [("step", C.c_int32), ("newton_iters", C.c_int32), ("rebuilds", C.c_int32),
+                ("backtracks", C.c_int32), ("pcg_iters", C.c_int64), ("residual", C.c_double),
+                ("energy", C.c_double), ("min_gap", C.c_double), ("energy_monotone", C.c_int32)]
+
+
+class _RunStats(C.Structure):
+    _fields_ = [("total_newton_iters", C.c_int64), ("total_rebuilds", C.c_int64), ("total_pcg_iters", C.c_int64),
+                ("newton_tol_used", C.c_double), ("wall_seconds", C.c_double), ("residual", C.c_double)]
+
+
+_CB = C.CFUNCTYPE(None, C.POINTER(_StepStats), C.POINTER(C.c_double), C.c_int64, C.c_void_p)
+
+
+@dataclass
+class StepStats:
+    step: int
+    newton_iters: int
+    rebuilds: int
+    backtracks: int
+    pcg_iters: int
+    residual: float
+    energy: float
+    min_gap: float
+    energy_monotone: bool
+
+
+@dataclass
+class RunStats:
+    steps: list = field(default_factory=list)
+    newton_tol_used: float = 0.0
+    wall_seconds: float = 0.0
+    total_newton_iters: int = 0
+    total_rebuilds: int = 0
+    total_pcg_iters: int = 0
+
+
+@dataclass
+class Body:
+    mesh: S.TetMesh
+    youngs: float
+    poisson: float
+    name: str
+    vertex_offset: int
+    boundary: S.SurfaceMesh
+
+
+def _lib():
+    L = _g.library()
+    L.gmcp_system_last_error.restype = C.c_char_p
+    L.gmcp_system_launch_count.restype = C.c_int64
+    L.gmcp_system_num_samples.restype = C.c_int64
+    L.gmcp_system_destroy.restype = None
+    L.gmcp_system_destroy.argtypes = [C.c_void_p]
+    return L
+
+
+def _check(L, rc, residual=float("nan")):
+    if rc != 0:
+        msg = L.gmcp_system_last_error().decode()
+        if rc == _g.GMCP_ERR_SOLVER:
+            raise _g.SolverError(msg, residual)
+        raise _g._EXC.get(rc, _g.Error)(msg)
+
+
+class System:
+    def __init__(self, device: int = 0):
+        self.L = _lib()
+        h = C.c_void_p()
+        _check(self.L, self.L.gmcp_system_create(C.c_int(device), C.byref(h)))
+        self.h = h
+        self.bodies: list[Body] = []
+        self.rest = np.zeros(0)
+        self.x = np.zeros(0)
+        self.f_ext = np.zeros(0)
+        self.fixed = np.zeros(0, np.uint8)
+        self.dirichlet = np.zeros(0)
+        self.contacts = []  # (slave ContactSurface, master ContactSurface, resolved params)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.gmcp_system_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def num_vertices(self) -> int:
+        return self.rest.size // 3
+
+    def add_body(self, mesh: S.TetMesh, youngs: float, poisson: float, name: str = "") -> int:
+        v = np.ascontiguousarray(mesh.vertices, np.float64)
+        t = np.ascontiguousarray(mesh.tets, np.int32)
+        off = C.c_int32()
+        _check(self.L, self.L.gmcp_system_add_body(self.h, _g._p(v), C.c_int64(v.shape[0]), _g._p(t),
+                                                   C.c_int64(t.shape[0]), C.c_double(youngs), C.c_double(poisson),
+                                                   C.byref(off)))
+        self.bodies.append(Body(mesh, youngs, poisson, name, off.value, S.extract_boundary_surface(mesh)))
+        self.rest = np.concatenate([self.rest, v.ravel()])
+        self.x = self.rest.copy()
+        self.f_ext = np.zeros_like(self.rest)
+        self.fixed = np.zeros(self.rest.size, np.uint8)
+        self.dirichlet = self.rest.copy()
+        return len(self.bodies) - 1
+
+    def fix_dof(self, gv: int, axis: int, target: float):
+        self.fixed[3 * gv + axis] = 1
+        self.dirichlet[3 * gv + axis] = target
+
+    def fix_vertex(self, gv: int, target):
+        for c in range(3):
+            self.fix_dof(gv, c, target[c])
+
+    def add_contact_pair(self, slave_body: int, master_body: int, params: S.BarrierParams, slave_tris=None,
+                         master_tris=None) -> int:
+        sb, mb = self.bodies[slave_body], self.bodies[master_body]
+        slave = S.make_contact_surface(sb.boundary, sb.vertex_offset, slave_tris)
+        master = S.make_contact_surface(mb.boundary, mb.vertex_offset, master_tris)
+        p = S.resolve_barrier_params(params, S.mean_edge_length(slave, self.rest))
+        self.contacts.append((slave, master, p))
+        return len(self.contacts) - 1
+
+    def _push(self):
+        idx = np.nonzero(self.fixed)[0].astype(np.int64)
+        tg = np.ascontiguousarray(self.dirichlet[idx])
+        _check(self.L, self.L.gmcp_system_fix_dofs(self.h, C.c_int64(idx.size), _g._p(idx), _g._p(tg)))
+        f = np.ascontiguousarray(self.f_ext, np.float64)
+        _check(self.L, self.L.gmcp_system_set_external_force(self.h, _g._p(f), C.c_int64(f.size)))
+        x = np.ascontiguousarray(self.x, np.float64)
+        _check(self.L, self.L.gmcp_system_set_positions(self.h, _g._p(x), C.c_int64(x.size)))
+        for (slave, master, p) in self.contacts[self._pushed_pairs:]:
+            arrs, st = [], []
+            for s in (slave, master):
+                a = [np.ascontiguousarray(v, dtype=np.int32) for v in (s.tris, s.edges, s.tri_edges, s.verts)]
+                arrs += a
+                st.append(_g._Surface(a[0].shape[0], a[0].ctypes.data, a[1].shape[0], a[1].ctypes.data,
+                                      a[2].ctypes.data, a[3].shape[0], a[3].ctypes.data))
+            cp = _g._params(p)
+            pid = C.c_int32()
+            _check(self.L, self.L.gmcp_system_add_contact_pair(self.h, C.byref(st[0]), C.byref(st[1]), C.byref(cp),
+                                                               C.byref(pid)))
+        self._pushed_pairs = len(self.contacts)
+
+    _pushed_pairs = 0
+
+    def solve(self, settings: SolverSettings | None = None, on_step=None) -> RunStats:
+        settings = settings or SolverSettings()
+        self._push()
+        stats = RunStats()
+
+        def cb(ss_p, x_p, n, user):
+            ss = ss_p.contents
+            s = StepStats(ss.step, ss.newton_iters, ss.rebuilds, ss.backtracks, ss.pcg_iters, ss.residual, ss.energy,
+                          ss.min_gap, bool(ss.energy_monotone))
+            stats.steps.append(s)
+            if on_step is not None:
+                on_step(s, np.ctypeslib.as_array(x_p, shape=(n,)).copy())
+
+        cbf = _CB(cb)
+        st = _Settings(settings.load_steps, settings.max_newton_iters, settings.newton_tol, settings.max_line_search,
+                       settings.pcg_tol, settings.pcg_max_iters)
+        out = _RunStats()
+        rc = self.L.gmcp_system_solve(self.h, C.byref(st), cbf, None, C.byref(out))
+        _check(self.L, rc, out.residual)
+        x = np.zeros_like(self.rest)
+        _check(self.L, self.L.gmcp_system_positions(self.h, _g._p(x), C.c_int64(x.size)))
+        self.x = x
+        stats.newton_tol_used = out.newton_tol_used
+        stats.wall_seconds = out.wall_seconds
+        stats.total_newton_iters = out.total_newton_iters
+        stats.total_rebuilds = out.total_rebuilds
+        stats.total_pcg_iters = out.total_pcg_iters
+        return stats
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.gmcp_system_launch_count(self.h))
+
+    def num_samples(self, pair: int = 0) -> int:
+        return int(self.L.gmcp_system_num_samples(self.h, C.c_int32(pair)))
+
+    def contact_force_summary(self, pair: int = 0):
+        out = np.zeros(12)
+        _check(self.L, self.L.gmcp_system_pair_force_summary(self.h, C.c_int32(pair), _g._p(out)))
+        return out.reshape(4, 3)
+
+    def contact_pressure_field(self, pair: int = 0):
+        n = C.c_int64()
+        _check(self.L, self.L.gmcp_system_pair_pressure(self.h, C.c_int32(pair), C.byref(n), None))
+        out = np.zeros(n.value, _g.PRESSURE_DTYPE)
+        if n.value:
+            _check(self.L, self.L.gmcp_system_pair_pressure(self.h, C.c_int32(pair), C.byref(n), _g._p(out)))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# elasticity helpers (elasticity.hpp:20-61, 147-160; bench.hpp:18-25)
+
+def material(E: float, nu: float):
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = E / (2 * (1 + nu))
+    return lam, mu
+
+
+def shape_gradients(verts: np.ndarray, tets: np.ndarray):
+    D = np.stack([verts[tets[:, i + 1]] - verts[tets[:, 0]] for i in range(3)], axis=2)  # columns
+    G = np.linalg.inv(D)  # rows = grads of shape functions 1..3
+    g0 = -G.sum(axis=1)
+    return np.concatenate([g0[:, None, :], G], axis=1), np.linalg.det(D) / 6.0  # (nt,4,3), vol
+
+
+def body_stresses(body: Body, x: np.ndarray, rest: np.ndarray) -> np.ndarray:
+    g, _ = shape_gradients(body.mesh.vertices, body.mesh.tets)
+    off = body.vertex_offset
+    u = (x.reshape(-1, 3) - rest.reshape(-1, 3))[off + body.mesh.tets]  # (nt,4,3)
+    grad_u = np.einsum("tia,tib->tab", u, g)
+    eps = 0.5 * (grad_u + np.swapaxes(grad_u, 1, 2))
+    lam, mu = material(body.youngs, body.poisson)
+    tr = np.trace(eps, axis1=1, axis2=2)
+    return lam * tr[:, None, None] * np.eye(3) + 2 * mu * eps
+
+
+def add_pressure_forces(faces: np.ndarray, rest: np.ndarray, magnitude: float, direction, f: np.ndarray):
+    x3 = rest.reshape(-1, 3)
+    for tri in faces:
+        a, b, c = x3[tri[0]], x3[tri[1]], x3[tri[2]]
+        cr = np.cross(b - a, c - a)
+        area = 0.5 * np.linalg.norm(cr)
+        d = np.asarray(direction, float) if direction is not None else -cr / np.linalg.norm(cr)
+        nf = magnitude * area / 3.0 * d
+        for i in range(3):
+            f[3 * tri[i]:3 * tri[i] + 3] += nf
+
+
+def build_patch_scene(kappa: float = 1e6, div_bottom=(5, 5, 2), div_top=(4, 4, 2), device: int = 0) -> System:
+    """make_patch_scene + build_scene (bench.hpp:44-99, scene.hpp:381-449)."""
+    sys_ = System(device)
+    bottom = S.make_block((1, 1, 0.5), div_bottom)
+    top = S.make_block((1, 1, 0.5), div_top, (0, 0, 0.502))
+    ib = sys_.add_body(bottom, 1000.0, 0.0, "bottom")
+    it = sys_.add_body(top, 1000.0, 0.0, "top")
+
+    def inside(p, lo, hi):
+        return np.all((p >= lo) & (p <= hi), axis=-1)
+
+    r3 = sys_.rest.reshape(-1, 3)
+    for bi, lo, hi, axes in ((ib, (-1, -1, -1), (2, 2, 1e-9), (0, 1, 2)), (it, (-1, -1, 0.5), (2, 2, 2), (0, 1))):
+        b = sys_.bodies[bi]
+        gv = b.vertex_offset + np.arange(b.mesh.vertices.shape[0])
+        sel = gv[inside(r3[gv], np.array(lo), np.array(hi))]
+        for v in sel:
+            for k in axes:
+                sys_.fix_dof(int(v), k, r3[v, k])
+    tb = sys_.bodies[it]
+    gtris = tb.vertex_offset + tb.boundary.vertex_map[tb.boundary.triangles]
+    load = gtris[np.all(inside(r3[gtris], np.array((-1, -1, 1.0019)), np.array((2, 2, 2))), axis=1)]
+    add_pressure_forces(load, sys_.rest, 10.0, (0, 0, -1), sys_.f_ext)
+    slave_sel = np.nonzero(np.all(inside(r3[gtris], np.array((-1, -1, 0.5019)), np.array((2, 2, 0.5021))),
+                                  axis=1))[0]
+    sys_.add_contact_pair(it, ib, S.BarrierParams(kappa_face=kappa, eps_max=0.001), slave_sel, None)
+    return sys_
+
+
+def patch_stress_metrics(sys_: System, pressure: float = 10.0):
+    """bench.hpp:101-111 -> (sigma_zz_max_rel_err, sigma_spur)."""
+    zz, spur = 0.0, 0.0
+    for b in sys_.bodies:
+        s = body_stresses(b, sys_.x, sys_.rest)
+        zz = max(zz, float(np.max(np.abs(s[:, 2, 2] + pressure) / pressure)))
+        spur = max(spur, float(np.max(np.abs(s[:, [0, 1, 0, 1, 0], [0, 1, 1, 2, 2]]))))
+    return zz, spur
