@@ -1,0 +1,514 @@
+// Contact assembly kernels (included once, by contact_eval.cu).
+//
+//  K7 k_tile_partials  one 256-thread block per tile of consecutive slave
+//                      runs (<= 256 samples). Phase A: one thread per sample
+//                      computes gap, barrier and the in-plane vector r into
+//                      shared memory; the tile's incidence lists are staged
+//                      into shared memory alongside. Phase B: one warp per
+//                      run; lanes own the run's moment sums (ascending sample
+//                      order) in a per-warp shared buffer, then finalize the
+//                      run's blocks from the moments and write the partial.
+//  K8 k_row_gather     one warp per vertex row: sums the finalized blocks of
+//                      the runs touching the vertex (ascending run order) in a
+//                      shared-memory row accumulator, then writes the BCSR row
+//                      and the gradient once.
+//
+// Moment form. Within a run (one slave triangle) n, e1, e2 are shared and the
+// slave gap gradients are dg_i = -b_i n + T_i(r) with T_0(v) = v x (e2-e1),
+// T_1(v) = e2 x v, T_2(v) = v x e1 (contact_energy.hpp:67-70), linear in the
+// per-sample r = (d - g n)/|c|. Hence the reference's per-sample Gauss-Newton
+// entries h (dg_v[a] dg_w[c]) (contact_energy.hpp:161-176) sum over a run to
+//   SS(i,j) = Mbb_ij n n^T - n T_j(Mbr_i)^T - T_i(Mbr_j) n^T + T_i Mrr T_j^T
+//   SM(i,m) = a_{m,i} n^T,  a_{m,i} = -Hwb_{m,i} n + T_i(Hwr_m)
+//   MM(m,l) = c_{ml} (n n^T)
+// with moments Mbb = sum h b b^T, Mbr = sum h b r^T, Mrr = sum h r r^T,
+// Hwb_m = sum h w_m b, Hwr_m = sum h w_m r, c_ml = sum h w_m w_l, and the
+// gradient g_i = -Fb_i n + T_i(Fr), g_m = s_m n (Fb = sum f b, Fr = sum f r,
+// s_m = sum f w_m). Upper SS blocks are stored once and mirrored, and every
+// mirror entry is the same product in the same order, so the assembled
+// matrix is exactly symmetric (test_contact.cpp:125).
+#pragma once
+
+#include "ctx.hpp"
+#include "kin.cuh"
+#include "reduce.cuh"
+
+namespace gmcp_b200 {
+namespace {
+
+constexpr int kTileSamples = 256;
+constexpr int kTileRuns = 64;
+constexpr int kRunMasters = 48;         // max local master vertices per run (planner splits)
+constexpr int kTileInc = 4 * kTileSamples;  // staged incidence entries per tile (planner splits)
+constexpr int kTileWarps = kTileSamples / 32;
+constexpr int kCol = kTileSamples + 1;  // padded column stride (bank spread)
+
+// Partial layout (doubles) at pbase[r]:
+//   [0] energy  [1..3] n  [4..12] slave gradients (i*3+k)
+//   [13..66] SS blocks (0,0),(0,1),(0,2),(1,1),(1,2),(2,2), 9 each, row-major
+//   [67 + 10m] s_m, [68 + 10m + 3i + k] a_{m,i}[k]   (m < M local master verts)
+//   [67 + 10M + p] c_p                                 (p < P local master pairs)
+constexpr int kSSBase = 13;
+constexpr int kMBase = 67;
+
+// Per-warp moment buffer layout
+constexpr int kFb = 0, kFr = 3, kMbb = 6, kMbr = 12, kMrr = 21, kMomRun = 27;  // + 7 m: Fw, Hwb(3), Hwr(3)
+constexpr int kRunTasks = 28;  // E, Fb(3), Fr(3), Mbb(6), Mbr(9), Mrr(6)
+
+// ---------------------------------------------------------------------------
+// K0: derived per-sample fields
+
+__global__ void k_derive(int64_t n, const int8_t* __restrict__ type, const double* __restrict__ beta_m,
+                         const double* __restrict__ eta, const double* __restrict__ weight,
+                         const double* __restrict__ gamma, double kf, double ke, double kp,
+                         double* __restrict__ wm, double* __restrict__ coef) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int8_t t = type[i];
+    const double kappa = t == GMCP_FACE ? kf : (t == GMCP_EDGE ? ke : kp);  // contact_energy.hpp:75-84
+    coef[i] = kappa * weight[i] * gamma[i];
+    if (t == GMCP_FACE) {
+      wm[3 * i] = beta_m[3 * i];
+      wm[3 * i + 1] = beta_m[3 * i + 1];
+      wm[3 * i + 2] = beta_m[3 * i + 2];
+    } else if (t == GMCP_EDGE) {  // contact_energy.hpp:47-49
+      wm[3 * i] = 1.0 - eta[i];
+      wm[3 * i + 1] = eta[i];
+      wm[3 * i + 2] = 0;
+    } else {
+      wm[3 * i] = 1;
+      wm[3 * i + 1] = 0;
+      wm[3 * i + 2] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7
+
+struct TileSmem {
+  double xa[3][kCol];  // eb = coef B, f = coef B', h = coef max(B'', 0)
+  double ya[7][kCol];  // 1, b0, b1, b2, r0, r1, r2
+  double w[3][kCol];   // master weights
+  double mom[kTileWarps][kMomRun + 1 + 7 * kRunMasters];  // per-warp run moments (+ energy)
+  double ra[kTileRuns][9];
+  double rn[kTileRuns][3];
+  double re[kTileRuns][6];
+  double rcn[kTileRuns];
+  int rs[kTileRuns + 1];
+  uint16_t im[kTileInc];
+  uint16_t ip[2 * kTileInc];
+};
+
+// Run moment tasks: value = sum_k X[k] * (Y[k] * Z[k]); X: 0 eb, 1 f, 2 h; Y/Z: column of ya;
+// destination index in the warp moment buffer (kMomRun = energy).
+__constant__ unsigned char c_task[kRunTasks][4] = {
+    {0, 0, 0, kMomRun},                                                       // E
+    {1, 1, 0, kFb}, {1, 2, 0, kFb + 1}, {1, 3, 0, kFb + 2},                   // Fb
+    {1, 4, 0, kFr}, {1, 5, 0, kFr + 1}, {1, 6, 0, kFr + 2},                   // Fr
+    {2, 1, 1, kMbb}, {2, 1, 2, kMbb + 1}, {2, 1, 3, kMbb + 2},                // Mbb 00 01 02
+    {2, 2, 2, kMbb + 3}, {2, 2, 3, kMbb + 4}, {2, 3, 3, kMbb + 5},            // Mbb 11 12 22
+    {2, 1, 4, kMbr}, {2, 1, 5, kMbr + 1}, {2, 1, 6, kMbr + 2},                // Mbr b0 r*
+    {2, 2, 4, kMbr + 3}, {2, 2, 5, kMbr + 4}, {2, 2, 6, kMbr + 5},            // Mbr b1 r*
+    {2, 3, 4, kMbr + 6}, {2, 3, 5, kMbr + 7}, {2, 3, 6, kMbr + 8},            // Mbr b2 r*
+    {2, 4, 4, kMrr}, {2, 4, 5, kMrr + 1}, {2, 4, 6, kMrr + 2},                // Mrr 00 01 02
+    {2, 5, 5, kMrr + 3}, {2, 5, 6, kMrr + 4}, {2, 6, 6, kMrr + 5}};           // Mrr 11 12 22
+
+__constant__ unsigned char c_ss_entry[45][3];  // (block, a, c) of the 45 unique SS entries
+__constant__ unsigned char c_ss_blk[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+__constant__ unsigned char c_sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+
+// T_i(v) (see header comment)
+__device__ __forceinline__ d3 Tmap(int i, d3 v, d3 e1, d3 e2) {
+  return i == 0 ? cross(v, e2 - e1) : (i == 1 ? cross(e2, v) : cross(v, e1));
+}
+// row a of the matrix A_i with T_i(v) = A_i v
+__device__ __forceinline__ d3 Trow(int i, int a, d3 e1, d3 e2) {
+  d3 u;
+  double s;
+  if (i == 0) { u = e2 - e1; s = -1.0; }  // v x u = -[u]_x v
+  else if (i == 1) { u = e2; s = 1.0; }   // u x v = [u]_x v
+  else { u = e1; s = -1.0; }
+  if (a == 0) return mk3(0, -s * u.z, s * u.y);
+  if (a == 1) return mk3(s * u.z, 0, -s * u.x);
+  return mk3(-s * u.y, s * u.x, 0);
+}
+__device__ __forceinline__ double comp(d3 v, int a) { return a == 0 ? v.x : (a == 1 ? v.y : v.z); }
+
+template <bool Hess>
+__global__ void __launch_bounds__(kTileSamples, 3) k_tile_partials(
+    DevSamples S, const double* __restrict__ x, int64_t n_tiles, const int32_t* __restrict__ tile_run,
+    const int64_t* __restrict__ run_off, const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm_off,
+    const int32_t* __restrict__ lp_off, const int32_t* __restrict__ im_off, const uint16_t* __restrict__ im,
+    const int32_t* __restrict__ ip_off, const uint16_t* __restrict__ ip, const int64_t* __restrict__ pbase,
+    double* __restrict__ partial, unsigned long long* __restrict__ red) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* mom = sm.mom[wid];
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int r0 = tile_run[tile], nr = tile_run[tile + 1] - r0;
+    const int64_t s0 = run_off[r0];
+    // stage the tile's incidence lists (contiguous across its runs)
+    const int ima = im_off[lm_off[r0]], imb = im_off[lm_off[r0 + nr]];
+    for (int e = ima + tid; e < imb; e += kTileSamples) sm.im[e - ima] = im[e];
+    const int ipa = Hess ? ip_off[lp_off[r0]] : 0, ipb = Hess ? ip_off[lp_off[r0 + nr]] : 0;
+    for (int e = ipa + tid; e < ipb; e += kTileSamples) sm.ip[e - ipa] = ip[e];
+    if (tid < nr) {  // run geometry
+      const int r = r0 + tid;
+      const d3 a0 = ld3(x, run_slave[3 * r]), a1 = ld3(x, run_slave[3 * r + 1]), a2 = ld3(x, run_slave[3 * r + 2]);
+      const d3 e1 = a1 - a0, e2 = a2 - a0;
+      const d3 c = cross(e1, e2);
+      const double cn = norm(c);
+      const d3 n = c / cn;
+      const double av[9] = {a0.x, a0.y, a0.z, a1.x, a1.y, a1.z, a2.x, a2.y, a2.z};
+      for (int q = 0; q < 9; ++q) sm.ra[tid][q] = av[q];
+      sm.rn[tid][0] = n.x;
+      sm.rn[tid][1] = n.y;
+      sm.rn[tid][2] = n.z;
+      const double ev[6] = {e1.x, e1.y, e1.z, e2.x, e2.y, e2.z};
+      for (int q = 0; q < 6; ++q) sm.re[tid][q] = ev[q];
+      sm.rcn[tid] = cn;
+      sm.rs[tid] = (int)(run_off[r] - s0);
+      if (!(cn > 0)) atomicMin(&red[1], (unsigned long long)run_off[r]);
+    }
+    if (tid == 0) sm.rs[nr] = (int)(run_off[r0 + nr] - s0);
+    __syncthreads();
+    // Phase A: one thread per sample
+    const int ns = sm.rs[nr];
+    if (tid < ns) {
+      int q = 0;
+      {
+        int lo = 0, hi = nr;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (sm.rs[mid] <= tid) lo = mid; else hi = mid;
+        }
+        q = lo;
+      }
+      const int64_t i = s0 + tid;
+      double h = 0, f = 0, eb = 0;
+      d3 rr = mk3(0, 0, 0);
+      int nm, mid[3];
+      double w[3];
+      load_master(S, i, nm, w, mid);
+      const double b0 = S.beta_s[3 * i], b1 = S.beta_s[3 * i + 1], b2 = S.beta_s[3 * i + 2];
+      const double cn = sm.rcn[q];
+      if (cn > 0) {
+        const d3 a0 = mk3(sm.ra[q][0], sm.ra[q][1], sm.ra[q][2]);
+        const d3 a1 = mk3(sm.ra[q][3], sm.ra[q][4], sm.ra[q][5]);
+        const d3 a2 = mk3(sm.ra[q][6], sm.ra[q][7], sm.ra[q][8]);
+        const d3 n = mk3(sm.rn[q][0], sm.rn[q][1], sm.rn[q][2]);
+        const d3 xs = (b0 * a0 + b1 * a1) + b2 * a2;
+        d3 xm = mk3(0, 0, 0);
+        for (int j = 0; j < nm; ++j) xm = xm + w[j] * ld3(x, mid[j]);
+        const d3 d = xm - xs;
+        const double g = dot(n, d);
+        if (!(g > 0)) {
+          atomicMin(&red[0], (unsigned long long)i);
+        } else {
+          rr = (d - g * n) / cn;
+          double B, dB, ddB;
+          barrier_eval(g, S.eps[i], B, dB, ddB);
+          const double cf = S.coef[i];
+          eb = cf * B;
+          f = cf * dB;
+          h = cf * dmax(ddB, 0.0);
+        }
+      }
+      sm.xa[0][tid] = eb;
+      sm.xa[1][tid] = f;
+      sm.xa[2][tid] = h;
+      sm.ya[0][tid] = 1.0;
+      sm.ya[1][tid] = b0;
+      sm.ya[2][tid] = b1;
+      sm.ya[3][tid] = b2;
+      sm.ya[4][tid] = rr.x;
+      sm.ya[5][tid] = rr.y;
+      sm.ya[6][tid] = rr.z;
+      for (int j = 0; j < 3; ++j) sm.w[j][tid] = j < nm ? w[j] : 0.0;
+    }
+    __syncthreads();
+    // Phase B: one warp per run, converged passes (every lane of a pass runs
+    // the same task type with the same or a similar trip count)
+    for (int q = wid; q < nr; q += kTileWarps) {
+      const int r = r0 + q;
+      const int k0 = sm.rs[q], k1 = sm.rs[q + 1];
+      const int m0 = lm_off[r], M = lm_off[r + 1] - m0;
+      const int p0 = lp_off[r], NP = lp_off[r + 1] - p0;
+      double* P = partial + pbase[r];
+      // B1: run moments (ascending-sample sums, all lanes same trip count)
+      const int nrt = Hess ? kRunTasks : 7;
+      if (lane < nrt) {
+        const double* X = sm.xa[c_task[lane][0]];
+        const double* Y = sm.ya[c_task[lane][1]];
+        const double* Z = sm.ya[c_task[lane][2]];
+        double s = 0;
+        for (int k = k0; k < k1; ++k) s += X[k] * (Y[k] * Z[k]);
+        mom[c_task[lane][3]] = s;
+      }
+      // B2: per local master vertex (its incidence list, ascending samples)
+      for (int m = lane; m < M; m += 32) {
+        const int ea = im_off[m0 + m] - ima, eb2 = im_off[m0 + m + 1] - ima;
+        double fw = 0, hb0 = 0, hb1 = 0, hb2 = 0, hr0 = 0, hr1 = 0, hr2 = 0;
+        for (int e = ea; e < eb2; ++e) {
+          const int code = sm.im[e];
+          const int k = code >> 2;
+          const double wj = sm.w[code & 3][k];
+          fw += sm.xa[1][k] * wj;
+          if (Hess) {
+            const double hw = sm.xa[2][k] * wj;
+            hb0 += hw * sm.ya[1][k];
+            hb1 += hw * sm.ya[2][k];
+            hb2 += hw * sm.ya[3][k];
+            hr0 += hw * sm.ya[4][k];
+            hr1 += hw * sm.ya[5][k];
+            hr2 += hw * sm.ya[6][k];
+          }
+        }
+        double* o = mom + kMomRun + 1 + 7 * m;
+        o[0] = fw;
+        o[1] = hb0;
+        o[2] = hb1;
+        o[3] = hb2;
+        o[4] = hr0;
+        o[5] = hr1;
+        o[6] = hr2;
+      }
+      // B3: master pairs straight to the partial
+      if (Hess)
+        for (int p = lane; p < NP; p += 32) {
+          const int ea = ip_off[p0 + p] - ipa, eb2 = ip_off[p0 + p + 1] - ipa;
+          double cv = 0;
+          for (int e = ea; e < eb2; ++e) {
+            const int code = sm.ip[e];
+            const int k = code >> 4;
+            cv += sm.xa[2][k] * (sm.w[(code >> 2) & 3][k] * sm.w[code & 3][k]);
+          }
+          P[kMBase + 10 * M + p] = cv;
+        }
+      __syncwarp();
+      // B4: finalize from the moments
+      const double nv[3] = {sm.rn[q][0], sm.rn[q][1], sm.rn[q][2]};
+      const d3 n = mk3(nv[0], nv[1], nv[2]);
+      const d3 e1 = mk3(sm.re[q][0], sm.re[q][1], sm.re[q][2]);
+      const d3 e2 = mk3(sm.re[q][3], sm.re[q][4], sm.re[q][5]);
+      if (lane < 4) {
+        P[lane] = lane == 0 ? mom[kMomRun] : nv[lane - 1];
+      } else if (lane < 13) {  // slave gradients g_i = -Fb_i n + T_i(Fr)
+        const int i = (lane - 4) / 3, a = (lane - 4) % 3;
+        const d3 g = (-mom[kFb + i]) * n + Tmap(i, mk3(mom[kFr], mom[kFr + 1], mom[kFr + 2]), e1, e2);
+        P[lane] = a == 0 ? g.x : (a == 1 ? g.y : g.z);
+      }
+      if (Hess)
+        for (int o = lane; o < 45; o += 32) {  // SS entries
+          const int blk = c_ss_entry[o][0], a = c_ss_entry[o][1], c = c_ss_entry[o][2];
+          const int i = c_ss_blk[blk][0], j = c_ss_blk[blk][1];
+          const d3 tj = Tmap(j, mk3(mom[kMbr + 3 * i], mom[kMbr + 3 * i + 1], mom[kMbr + 3 * i + 2]), e1, e2);
+          const d3 ti = Tmap(i, mk3(mom[kMbr + 3 * j], mom[kMbr + 3 * j + 1], mom[kMbr + 3 * j + 2]), e1, e2);
+          const double tjc = c == 0 ? tj.x : (c == 1 ? tj.y : tj.z);
+          const double tia = a == 0 ? ti.x : (a == 1 ? ti.y : ti.z);
+          // (A_i Mrr A_j^T)_ac = row_a(A_i) . Mrr . row_c(A_j)
+          const d3 ra = Trow(i, a, e1, e2), rc = Trow(j, c, e1, e2);
+          const d3 mr = mk3(mom[kMrr] * rc.x + mom[kMrr + 1] * rc.y + mom[kMrr + 2] * rc.z,
+                            mom[kMrr + 1] * rc.x + mom[kMrr + 3] * rc.y + mom[kMrr + 4] * rc.z,
+                            mom[kMrr + 2] * rc.x + mom[kMrr + 4] * rc.y + mom[kMrr + 5] * rc.z);
+          const double na = nv[a], nc = nv[c];
+          const double v = ((mom[kMbb + c_sym[i][j]] * (na * nc) - na * tjc) - tia * nc) + dot(ra, mr);
+          P[kSSBase + 9 * blk + 3 * a + c] = v;
+          if (i == j && a != c) P[kSSBase + 9 * blk + 3 * c + a] = v;
+        }
+      for (int m = lane; m < M; m += 32) {  // s_m and a_{m,i} = -Hwb_{m,i} n + T_i(Hwr_m)
+        const double* mm = mom + kMomRun + 1 + 7 * m;
+        double* out = P + kMBase + 10 * m;
+        out[0] = mm[0];
+        if (Hess) {
+          const d3 hr = mk3(mm[4], mm[5], mm[6]);
+          for (int i = 0; i < 3; ++i) {
+            const d3 av = (-mm[1 + i]) * n + Tmap(i, hr, e1, e2);
+            out[1 + 3 * i] = av.x;
+            out[2 + 3 * i] = av.y;
+            out[3 + 3 * i] = av.z;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+// Energy of the pass = sum of run energies in run order.
+__global__ void __launch_bounds__(kRedThreads) k_run_energy(int64_t n_runs, const int64_t* __restrict__ pbase,
+                                                             const double* __restrict__ partial,
+                                                             double* __restrict__ parts) {
+  __shared__ double sh[kRedThreads / 32];
+  double e = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_runs; r += (int64_t)gridDim.x * blockDim.x)
+    e += partial[pbase[r]];
+  const double v = block_sum<kRedThreads>(e, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = v;
+}
+
+// ---------------------------------------------------------------------------
+// K8
+
+constexpr int kRowCols = 48;  // shared-memory row accumulator capacity (blocks)
+constexpr int kGatherWarps = 8;
+
+struct RowSmem {
+  int cols[kRowCols];
+  double acc[kRowCols * 9];
+};
+
+__device__ __forceinline__ int find_col(const int32_t* cols, int lo, int hi, int col) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (cols[mid] < col) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Contribution block of entry element b; returns its column or -1.
+__device__ __forceinline__ int entry_block(int role, int b, int64_t r, const double* __restrict__ P, int M,
+                                           const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm,
+                                           const int32_t* __restrict__ lpp, double* blk) {
+  const double nn[3] = {P[1], P[2], P[3]};
+  if (role < 3) {
+    const int i = role;
+    if (b < 3) {
+      const int j = b;
+      const int lo = min(i, j), hi = max(i, j);
+      const int bid = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+      const double* Sb = P + kSSBase + 9 * bid;
+      if (i <= j) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) blk[q] = Sb[q];
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) blk[3 * a + c] = Sb[3 * c + a];
+      }
+      return run_slave[3 * r + j];
+    }
+    const int k = b - 3;
+    const double* A = P + kMBase + 10 * k + 1 + 3 * i;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) blk[3 * a + c] = A[a] * nn[c];
+    return lm[k];
+  }
+  const int m = role - 3;
+  if (b < 3) {
+    const double* A = P + kMBase + 10 * m + 1 + 3 * b;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) blk[3 * a + c] = nn[a] * A[c];
+    return run_slave[3 * r + b];
+  }
+  const int p = b - 3;
+  const int pk = lpp[p];
+  const int la = pk >> 16, lb = pk & 0xffff;
+  if (la != m && lb != m) return -1;
+  const double cv = P[kMBase + 10 * M + p];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) blk[3 * a + c] = cv * (nn[a] * nn[c]);
+  return lm[la == m ? lb : la];
+}
+
+template <bool Hess>
+__global__ void __launch_bounds__(32 * kGatherWarps) k_row_gather(
+    int32_t n_rows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols, double* __restrict__ vals,
+    const int32_t* __restrict__ ent_off, const int64_t* __restrict__ ent, const int32_t* __restrict__ run_slave,
+    const int32_t* __restrict__ lm_off, const int32_t* __restrict__ lm_ids, const int32_t* __restrict__ lp_off,
+    const int32_t* __restrict__ lp, const int64_t* __restrict__ pbase, const double* __restrict__ partial,
+    double* __restrict__ grad) {
+  __shared__ RowSmem rsm[kGatherWarps];
+  const int lane = threadIdx.x & 31;
+  RowSmem& R = rsm[threadIdx.x >> 5];
+  const int64_t nwarps = (int64_t)gridDim.x * kGatherWarps;
+  for (int64_t v = blockIdx.x * (int64_t)kGatherWarps + (threadIdx.x >> 5); v < n_rows; v += nwarps) {
+    const int e0 = ent_off[v], e1 = ent_off[v + 1];
+    const int c0 = Hess ? rowptr[v] : 0, c1 = Hess ? rowptr[v + 1] : 0;
+    const int nc = c1 - c0;
+    const bool in_smem = Hess && nc <= kRowCols;
+    if (Hess) {
+      if (in_smem) {
+        for (int q = lane; q < nc; q += 32) R.cols[q] = cols[c0 + q];
+        for (int q = lane; q < 9 * nc; q += 32) R.acc[q] = 0;
+      } else {
+        for (int q = lane; q < 9 * nc; q += 32) vals[9 * (int64_t)c0 + q] = 0;
+      }
+    }
+    d3 g = mk3(0, 0, 0);
+    __syncwarp();
+    for (int e = e0; e < e1; ++e) {
+      const int64_t en = ent[e];
+      const int64_t r = en >> 20;
+      const int role = (int)(en & 0xfffff);
+      const double* P = partial + pbase[r];
+      if (lane == 0) {
+        if (role < 3) {
+          g = g + mk3(P[4 + 3 * role], P[5 + 3 * role], P[6 + 3 * role]);
+        } else {
+          const double s = P[kMBase + 10 * (role - 3)];
+          g = g + s * mk3(P[1], P[2], P[3]);
+        }
+      }
+      if (Hess) {
+        const int m0 = lm_off[r], M = lm_off[r + 1] - m0;
+        const int p0 = lp_off[r], NP = lp_off[r + 1] - p0;
+        const int nb = 3 + (role < 3 ? M : NP);
+        for (int b = lane; b < nb; b += 32) {
+          double blk[9];
+          const int col = entry_block(role, b, r, P, M, run_slave, lm_ids + m0, lp + p0, blk);
+          if (col < 0) continue;
+          double* out = in_smem ? R.acc + 9 * find_col(R.cols, 0, nc, col)
+                                : vals + 9 * (int64_t)find_col(cols, c0, c1, col);
+#pragma unroll
+          for (int q = 0; q < 9; ++q) out[q] += blk[q];
+        }
+      }
+      __syncwarp();
+    }
+    if (in_smem)
+      for (int q = lane; q < 9 * nc; q += 32) vals[9 * (int64_t)c0 + q] = R.acc[q];
+    if (lane == 0) {
+      grad[3 * v] = g.x;
+      grad[3 * v + 1] = g.y;
+      grad[3 * v + 2] = g.z;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_flush(double* buf, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = buf[i] * 0.5 + 1.0;
+}
+
+void init_ss_table() {
+  static bool done = false;
+  if (done) return;
+  unsigned char tab[45][3];
+  int k = 0;
+  const int blks[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+  for (int b = 0; b < 6; ++b)
+    for (int a = 0; a < 3; ++a)
+      for (int cc = 0; cc < 3; ++cc) {
+        if (blks[b][0] == blks[b][1] && cc < a) continue;
+        tab[k][0] = (unsigned char)b;
+        tab[k][1] = (unsigned char)a;
+        tab[k][2] = (unsigned char)cc;
+        ++k;
+      }
+  GMCP_CUDA(cudaMemcpyToSymbol(c_ss_entry, tab, sizeof tab));
+  done = true;
+}
+
+}  // namespace
+}  // namespace gmcp_b200

@@ -25,6 +25,15 @@ struct AssemblyPlan {
   DBuf<int32_t> lp_off;      // [R+1] local master pair table offsets
   DBuf<int32_t> lp;          // packed (a << 16 | b), local indices, a <= b
   DBuf<int64_t> pbase;       // [R] partial base offset (doubles)
+  // K7 tiles: consecutive runs with <= kTileSamples samples in total
+  int64_t n_tiles = 0;
+  DBuf<int32_t> tile_run;    // [T+1] first run of each tile
+  // incidence lists (sample index within the tile, packed), per flat local
+  // master vertex / local pair, ascending sample order
+  DBuf<int32_t> im_off;      // [lm_ids.n + 1]
+  DBuf<uint16_t> im;         // (k << 2) | j
+  DBuf<int32_t> ip_off;      // [lp.n + 1]
+  DBuf<uint16_t> ip;         // (k << 4) | (ja << 2) | jb
   int64_t partial_len = 0;
   DBuf<double> partial;
   // BCSR pattern over all N vertex rows
