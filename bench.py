@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-newton", action="store_true")
+    ap.add_argument("--newton-iters", type=int, default=5)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -319,13 +321,36 @@ def main():
     e2e = world * n * args.steps / e2e_s
 
     # end-of-run result gather (NCCL): per-rank sample counts and energies
-    summary = torch.tensor([float(n), e0], device="cuda", dtype=torch.float64)
     if dist:
-        gathered = [torch.zeros_like(summary) for _ in range(world)]
-        dist.all_gather(gathered, summary)
-        total_samples = int(sum(float(t[0]) for t in gathered))
+        from paper_2605_24339_b200 import dist as D
+        rows = D.gather_results(np.array([[float(n), e0]]), dist, device=torch.device("cuda", local))
+        total_samples = int(rows[:, 0].sum())
     else:
         total_samples = n
+
+    # Newton steps/s: C3 with patch-test BCs, device-resident
+    # System::solve; each timed iteration = assembly, residual, PCG to
+    # tolerance, filter + cap, every line-search trial, rebuild check.
+    newton = None
+    if not args.no_newton:
+        from paper_2605_24339_b200 import system as SY
+        nsys = SY.build_slab_system(155, 124, texture_amp=2e-4, device=local)
+        settings = SY.SolverSettings(pcg_tol=1e-8, pcg_max_iters=50000)
+        if dist:
+            dist.barrier()
+        ms_it, pcg_it = nsys.time_newton(settings, args.newton_iters + 1)
+        steady = ms_it[1:] if ms_it.size > 1 else ms_it
+        t = float(np.mean(steady))
+        if dist:
+            tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt[0])
+        newton = {"steps_per_s": world * 1e3 / t, "ms_per_iter": t, "per_iter_ms": [round(float(v), 3) for v in ms_it],
+                  "pcg_iters": [int(v) for v in pcg_it], "pcg_tol": settings.pcg_tol,
+                  "first_iter_includes": "load-step rebuild + one-time elastic BCSR build (excluded from the mean)",
+                  "dofs": int(nsys.rest.size), "samples": int(nsys.num_samples(0)),
+                  "clock": "host steady_clock around each iteration (device synchronized)"}
+        del nsys
 
     peak, peak_src = peaks()
     achieved_k7 = ab["k7"] / (ms_k7 / 1e3) / 1e9
@@ -359,6 +384,7 @@ def main():
                     "d2h_bytes_per_step": int(scene.rest.size * 8 + 8),
                     "path": "gmcp.Context.set_positions + gradient(hessian=True) (C-ABI gmcp_set_positions + "
                             "gmcp_gradient_hessian), pinned host buffers"},
+            "newton": newton,
             "gpu_launches": int(launches),
             "clocks": clocks,
             "cpu_baseline": cpu,

@@ -64,6 +64,13 @@ int gmcp_system_add_contact_pair(gmcp_system* sys, const gmcp_surface* slave, co
  * SolverError / ConfigError; out->residual carries SolverError::residual. */
 int gmcp_system_solve(gmcp_system* sys, const gmcp_solver_settings* settings, gmcp_step_callback cb,
                       void* user, gmcp_run_stats* out);
+/* Benchmark hook: runs the solve from the current state and stops after
+ * n_iters Newton iterations (SURVEY.md 8d "Newton steps/s"), returning the
+ * wall milliseconds of each full iteration (assembly, residual, PCG to
+ * tolerance, filter + cap, every line-search trial, rebuild check) and its
+ * PCG iteration count. */
+int gmcp_system_time_newton(gmcp_system* sys, const gmcp_solver_settings* settings, int32_t n_iters,
+                            double* ms_per_iter, int64_t* pcg_per_iter, int32_t* n_done);
 int gmcp_system_positions(gmcp_system* sys, double* x, int64_t n_dof);
 int gmcp_system_set_positions(gmcp_system* sys, const double* x, int64_t n_dof);
 int64_t gmcp_system_num_samples(gmcp_system* sys, int32_t pair);

@@ -392,6 +392,10 @@ struct SystemImpl {
   std::vector<double> x_host;
   // stats of the last solve
   int64_t pcg_iters_total = 0;
+  // Newton-iteration timing (gmcp_system_time_newton): stop after iter_limit
+  int64_t iter_limit = 0;
+  std::vector<double> iter_ms;
+  std::vector<int64_t> iter_pcg;
 
   int nv() const { return (int)(n_dof / 3); }
   void sync() { GMCP_CUDA(cudaStreamSynchronize(stream)); }
@@ -696,6 +700,8 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
     ss.min_gap = std::min(ss.min_gap, ce.min_gap);
     bool converged = false;
     for (int it = 0; it < st.max_newton_iters; ++it) {
+      const auto t_it = std::chrono::steady_clock::now();
+      const int64_t pcg_before = ss.pcg_iters;
       if (it > 0) resid = assemble(S, lambda);
       if (resid <= tol) {
         converged = true;
@@ -766,6 +772,16 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
         ce = contact_energy_at(S, S.x.p);
         if (!ce.feasible) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
         energy = e_el + ce.energy - lambda * work;
+      }
+      if (S.iter_limit > 0) {  // timing mode (gmcp_system_time_newton)
+        S.sync();
+        S.iter_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_it).count());
+        S.iter_pcg.push_back(ss.pcg_iters - pcg_before);
+        if ((int64_t)S.iter_ms.size() >= S.iter_limit) {
+          S.x.download(S.x_host.data(), n, S.stream);
+          S.sync();
+          return;
+        }
       }
     }
     if (!converged) {
@@ -939,6 +955,31 @@ int gmcp_system_solve(gmcp_system* sys, const gmcp_solver_settings* st, gmcp_ste
                       gmcp_run_stats* out) {
   return sguard([&] {
     system_solve(sys->s, *st, cb, user, out);
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_time_newton(gmcp_system* sys, const gmcp_solver_settings* st, int32_t n_iters, double* ms_per_iter,
+                            int64_t* pcg_per_iter, int32_t* n_done) {
+  return sguard([&] {
+    SystemImpl& S = sys->s;
+    if (n_iters < 1) throw StatusError(GMCP_ERR_ARG, "n_iters must be positive");
+    S.iter_limit = n_iters;
+    S.iter_ms.clear();
+    S.iter_pcg.clear();
+    gmcp_run_stats out{};
+    try {
+      system_solve(S, *st, nullptr, nullptr, &out);
+    } catch (...) {
+      S.iter_limit = 0;
+      throw;
+    }
+    S.iter_limit = 0;
+    *n_done = (int32_t)S.iter_ms.size();
+    for (size_t i = 0; i < S.iter_ms.size(); ++i) {
+      ms_per_iter[i] = S.iter_ms[i];
+      pcg_per_iter[i] = S.iter_pcg[i];
+    }
     return GMCP_OK;
   });
 }

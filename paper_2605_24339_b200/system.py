@@ -209,6 +209,19 @@ class System:
         stats.total_pcg_iters = out.total_pcg_iters
         return stats
 
+    def time_newton(self, settings: SolverSettings | None = None, n_iters: int = 3):
+        """Wall ms and PCG iterations of the first n_iters full Newton iterations."""
+        settings = settings or SolverSettings()
+        self._push()
+        st = _Settings(settings.load_steps, settings.max_newton_iters, settings.newton_tol, settings.max_line_search,
+                       settings.pcg_tol, settings.pcg_max_iters)
+        ms = np.zeros(n_iters)
+        pcg = np.zeros(n_iters, np.int64)
+        done = C.c_int32()
+        _check(self.L, self.L.gmcp_system_time_newton(self.h, C.byref(st), C.c_int32(n_iters), _g._p(ms), _g._p(pcg),
+                                                      C.byref(done)))
+        return ms[:done.value], pcg[:done.value]
+
     @property
     def launches(self) -> int:
         return int(self.L.gmcp_system_launch_count(self.h))
@@ -306,3 +319,31 @@ def patch_stress_metrics(sys_: System, pressure: float = 10.0):
         zz = max(zz, float(np.max(np.abs(s[:, 2, 2] + pressure) / pressure)))
         spur = max(spur, float(np.max(np.abs(s[:, [0, 1, 0, 1, 0], [0, 1, 1, 2, 2]]))))
     return zz, spur
+
+
+def build_slab_system(nb: int, nt: int, texture_amp: float = 0.0, texture_freq: float = 20.0,
+                      kappa: float = 1e6, pressure: float = 10.0, device: int = 0) -> System:
+    """SURVEY.md 8d Newton-steps/s scene for C2/C3: slab(nb, nt) with the
+    make_patch_scene boundary conditions (bench.hpp:64-84): master bottom face
+    clamped, slave body u_x = u_y = 0, uniform pressure on the slave top face
+    along -z (lambda-ramped), E = 1000, nu = 0."""
+    sl = S.slab_scene(nb, nt, texture_amp=texture_amp, texture_freq=texture_freq)
+    sys_ = System(device)
+    ib = sys_.add_body(sl.meshes[0], 1000.0, 0.0, "indenter")
+    it = sys_.add_body(sl.meshes[1], 1000.0, 0.0, "pad")
+    r3 = sys_.rest.reshape(-1, 3)
+    b = sys_.bodies[ib]
+    gv = b.vertex_offset + np.arange(b.mesh.vertices.shape[0])
+    for v in gv[r3[gv, 2] < 1e-9]:
+        sys_.fix_vertex(int(v), r3[v])
+    t = sys_.bodies[it]
+    gv = t.vertex_offset + np.arange(t.mesh.vertices.shape[0])
+    for v in gv:
+        sys_.fix_dof(int(v), 0, r3[v, 0])
+        sys_.fix_dof(int(v), 1, r3[v, 1])
+    gtris = t.vertex_offset + t.boundary.vertex_map[t.boundary.triangles]
+    top = gtris[np.all(np.abs(r3[gtris, 2] - 0.202) < 1e-9, axis=1)]
+    add_pressure_forces(top, sys_.rest, pressure, (0, 0, -1), sys_.f_ext)
+    down = np.nonzero(np.all(np.abs(r3[gtris, 2] - 0.102) < 1e-9, axis=1))[0]
+    sys_.add_contact_pair(it, ib, S.BarrierParams(kappa_face=kappa, eps_max=1e-3), down, None)
+    return sys_
