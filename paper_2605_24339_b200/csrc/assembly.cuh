@@ -36,12 +36,11 @@
 namespace gmcp_b200 {
 namespace {
 
-constexpr int kTileSamples = 256;
-constexpr int kTileRuns = 64;
-constexpr int kRunMasters = 48;         // max local master vertices per run (planner splits)
-constexpr int kTileInc = 4 * kTileSamples;  // staged incidence entries per tile (planner splits)
+constexpr int kTileSamples = 128;                       // samples per K7 tile (= block threads)
+constexpr int kTileRuns = 8;
+constexpr int kRunMasters = 8;                          // local master vertices per run (planner splits)
+constexpr int kTileRows = kTileSamples + 3 * kTileRuns;  // runs padded to multiples of 4 rows
 constexpr int kTileWarps = kTileSamples / 32;
-constexpr int kCol = kTileSamples + 1;  // padded column stride (bank spread)
 
 // Partial layout (doubles) at pbase[r]:
 //   [0] energy  [1..3] n  [4..12] slave gradients (i*3+k)
@@ -51,9 +50,6 @@ constexpr int kCol = kTileSamples + 1;  // padded column stride (bank spread)
 constexpr int kSSBase = 13;
 constexpr int kMBase = 67;
 
-// Per-warp moment buffer layout
-constexpr int kFb = 0, kFr = 3, kMbb = 6, kMbr = 12, kMrr = 21, kMomRun = 27;  // + 7 m: Fw, Hwb(3), Hwr(3)
-constexpr int kRunTasks = 28;  // E, Fb(3), Fr(3), Mbb(6), Mbr(9), Mrr(6)
 
 // ---------------------------------------------------------------------------
 // K0: derived per-sample fields
@@ -84,38 +80,40 @@ __global__ void k_derive(int64_t n, const int8_t* __restrict__ type, const doubl
 
 // ---------------------------------------------------------------------------
 // K7
+//
+// All per-run sums are entries of one small Gram product computed on the FP64
+// tensor cores (mma.sync m8n8k4 f64 -> DMMA):
+//   C = U'^T V   over the run's samples k (rows padded to a multiple of 4),
+//   U'[k] = [b0 b1 b2 | r0 r1 r2 | W_0 .. W_{M-1} | 1]              (7 + M <= 16)
+//   V[k]  = [h b0 h b1 h b2 | h r0 h r1 h r2 | h W_0 .. h W_{M-1} | f | eb]
+// where W_m is the master weight of local master vertex m in sample k. So
+//   Mbb = C[b][b], Mbr = C[b][r], Mrr = C[r][r], Fb = C[b][f], Fr = C[r][f],
+//   E = C[1][eb], Fw_m = C[W_m][f], Hwb_m = C[W_m][b], Hwr_m = C[W_m][r],
+//   c_ml = C[W_m][W_l].
+// The accumulation order inside DMMA is fixed by the hardware, so results are
+// bitwise reproducible.
+
+constexpr int kUC = 16;  // U' / V columns
+
+constexpr int kLD = kTileRows + 4;  // column stride (doubles): lanes of a warp hit distinct banks
 
 struct TileSmem {
-  double xa[3][kCol];  // eb = coef B, f = coef B', h = coef max(B'', 0)
-  double ya[7][kCol];  // 1, b0, b1, b2, r0, r1, r2
-  double w[3][kCol];   // master weights
-  double mom[kTileWarps][kMomRun + 1 + 7 * kRunMasters];  // per-warp run moments (+ energy)
+  double u[kUC][kLD];  // U' columns (column-major: consecutive samples are consecutive)
+  double v[kUC][kLD];  // V columns
+  double cbuf[kTileWarps][kUC][kUC + 1];  // per-warp C
+  double tm[kTileWarps][27];  // T_j(Mbr_i): [i][j][comp]
+  double bm[kTileWarps][27];  // Mrr A_j^T: [j][p][c]
   double ra[kTileRuns][9];
   double rn[kTileRuns][3];
   double re[kTileRuns][6];
-  double rcn[kTileRuns];
-  int rs[kTileRuns + 1];
-  uint16_t im[kTileInc];
-  uint16_t ip[2 * kTileInc];
+  double ricn[kTileRuns];   // 1 / |c| (0 for degenerate)
+  int rs[kTileRuns + 1];    // sample offsets of the runs within the tile
+  int rrow[kTileRuns + 1];  // padded row offsets of the runs within the tile
+  int rM[kTileRuns];
 };
-
-// Run moment tasks: value = sum_k X[k] * (Y[k] * Z[k]); X: 0 eb, 1 f, 2 h; Y/Z: column of ya;
-// destination index in the warp moment buffer (kMomRun = energy).
-__constant__ unsigned char c_task[kRunTasks][4] = {
-    {0, 0, 0, kMomRun},                                                       // E
-    {1, 1, 0, kFb}, {1, 2, 0, kFb + 1}, {1, 3, 0, kFb + 2},                   // Fb
-    {1, 4, 0, kFr}, {1, 5, 0, kFr + 1}, {1, 6, 0, kFr + 2},                   // Fr
-    {2, 1, 1, kMbb}, {2, 1, 2, kMbb + 1}, {2, 1, 3, kMbb + 2},                // Mbb 00 01 02
-    {2, 2, 2, kMbb + 3}, {2, 2, 3, kMbb + 4}, {2, 3, 3, kMbb + 5},            // Mbb 11 12 22
-    {2, 1, 4, kMbr}, {2, 1, 5, kMbr + 1}, {2, 1, 6, kMbr + 2},                // Mbr b0 r*
-    {2, 2, 4, kMbr + 3}, {2, 2, 5, kMbr + 4}, {2, 2, 6, kMbr + 5},            // Mbr b1 r*
-    {2, 3, 4, kMbr + 6}, {2, 3, 5, kMbr + 7}, {2, 3, 6, kMbr + 8},            // Mbr b2 r*
-    {2, 4, 4, kMrr}, {2, 4, 5, kMrr + 1}, {2, 4, 6, kMrr + 2},                // Mrr 00 01 02
-    {2, 5, 5, kMrr + 3}, {2, 5, 6, kMrr + 4}, {2, 6, 6, kMrr + 5}};           // Mrr 11 12 22
 
 __constant__ unsigned char c_ss_entry[45][3];  // (block, a, c) of the 45 unique SS entries
 __constant__ unsigned char c_ss_blk[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
-__constant__ unsigned char c_sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
 
 // T_i(v) (see header comment)
 __device__ __forceinline__ d3 Tmap(int i, d3 v, d3 e1, d3 e2) {
@@ -134,25 +132,28 @@ __device__ __forceinline__ d3 Trow(int i, int a, d3 e1, d3 e2) {
 }
 __device__ __forceinline__ double comp(d3 v, int a) { return a == 0 ? v.x : (a == 1 ? v.y : v.z); }
 
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 template <bool Hess>
-__global__ void __launch_bounds__(kTileSamples, 3) k_tile_partials(
+__global__ void __launch_bounds__(kTileSamples, 4) k_tile_partials(
     DevSamples S, const double* __restrict__ x, int64_t n_tiles, const int32_t* __restrict__ tile_run,
     const int64_t* __restrict__ run_off, const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm_off,
-    const int32_t* __restrict__ lp_off, const int32_t* __restrict__ im_off, const uint16_t* __restrict__ im,
-    const int32_t* __restrict__ ip_off, const uint16_t* __restrict__ ip, const int64_t* __restrict__ pbase,
-    double* __restrict__ partial, unsigned long long* __restrict__ red) {
+    const int32_t* __restrict__ lp_off, const int32_t* __restrict__ lp, const uint32_t* __restrict__ li4,
+    const int32_t* __restrict__ run_row, const int64_t* __restrict__ pbase, double* __restrict__ partial,
+    unsigned long long* __restrict__ red) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double* mom = sm.mom[wid];
+  double (*C)[kUC + 1] = sm.cbuf[wid];
+  double* tm = sm.tm[wid];
+  double* bm = sm.bm[wid];
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int r0 = tile_run[tile], nr = tile_run[tile + 1] - r0;
     const int64_t s0 = run_off[r0];
-    // stage the tile's incidence lists (contiguous across its runs)
-    const int ima = im_off[lm_off[r0]], imb = im_off[lm_off[r0 + nr]];
-    for (int e = ima + tid; e < imb; e += kTileSamples) sm.im[e - ima] = im[e];
-    const int ipa = Hess ? ip_off[lp_off[r0]] : 0, ipb = Hess ? ip_off[lp_off[r0 + nr]] : 0;
-    for (int e = ipa + tid; e < ipb; e += kTileSamples) sm.ip[e - ipa] = ip[e];
     if (tid < nr) {  // run geometry
       const int r = r0 + tid;
       const d3 a0 = ld3(x, run_slave[3 * r]), a1 = ld3(x, run_slave[3 * r + 1]), a2 = ld3(x, run_slave[3 * r + 2]);
@@ -167,13 +168,25 @@ __global__ void __launch_bounds__(kTileSamples, 3) k_tile_partials(
       sm.rn[tid][2] = n.z;
       const double ev[6] = {e1.x, e1.y, e1.z, e2.x, e2.y, e2.z};
       for (int q = 0; q < 6; ++q) sm.re[tid][q] = ev[q];
-      sm.rcn[tid] = cn;
+      sm.ricn[tid] = cn > 0 ? 1.0 / cn : 0.0;
       sm.rs[tid] = (int)(run_off[r] - s0);
+      sm.rrow[tid] = run_row[r];
+      sm.rM[tid] = lm_off[r + 1] - lm_off[r];
       if (!(cn > 0)) atomicMin(&red[1], (unsigned long long)run_off[r]);
     }
-    if (tid == 0) sm.rs[nr] = (int)(run_off[r0 + nr] - s0);
+    if (tid == 0) {
+      sm.rs[nr] = (int)(run_off[r0 + nr] - s0);
+      sm.rrow[nr] = run_row[r0 + nr - 1] + (((int)(run_off[r0 + nr] - run_off[r0 + nr - 1]) + 3) & ~3);
+    }
     __syncthreads();
-    // Phase A: one thread per sample
+    // padding rows (<= 3 per run) are zero
+    if (tid < 3 * nr) {
+      const int q = tid / 3;
+      const int row = sm.rrow[q] + (sm.rs[q + 1] - sm.rs[q]) + tid % 3;
+      if (row < sm.rrow[q + 1])
+        for (int c = 0; c < kUC; ++c) sm.u[c][row] = sm.v[c][row] = 0.0;
+    }
+    // Phase A: one thread per sample -> its U' and V rows
     const int ns = sm.rs[nr];
     if (tid < ns) {
       int q = 0;
@@ -186,14 +199,15 @@ __global__ void __launch_bounds__(kTileSamples, 3) k_tile_partials(
         q = lo;
       }
       const int64_t i = s0 + tid;
+      const int row = sm.rrow[q] + (tid - sm.rs[q]);
       double h = 0, f = 0, eb = 0;
       d3 rr = mk3(0, 0, 0);
       int nm, mid[3];
       double w[3];
       load_master(S, i, nm, w, mid);
       const double b0 = S.beta_s[3 * i], b1 = S.beta_s[3 * i + 1], b2 = S.beta_s[3 * i + 2];
-      const double cn = sm.rcn[q];
-      if (cn > 0) {
+      const double icn = sm.ricn[q];
+      if (icn > 0) {
         const d3 a0 = mk3(sm.ra[q][0], sm.ra[q][1], sm.ra[q][2]);
         const d3 a1 = mk3(sm.ra[q][3], sm.ra[q][4], sm.ra[q][5]);
         const d3 a2 = mk3(sm.ra[q][6], sm.ra[q][7], sm.ra[q][8]);
@@ -206,129 +220,120 @@ __global__ void __launch_bounds__(kTileSamples, 3) k_tile_partials(
         if (!(g > 0)) {
           atomicMin(&red[0], (unsigned long long)i);
         } else {
-          rr = (d - g * n) / cn;
-          double B, dB, ddB;
-          barrier_eval(g, S.eps[i], B, dB, ddB);
-          const double cf = S.coef[i];
-          eb = cf * B;
-          f = cf * dB;
-          h = cf * dmax(ddB, 0.0);
+          rr = icn * (d - g * n);
+          const double eps = S.eps[i];
+          if (g < eps) {  // barrier.hpp:55-66 with one reciprocal
+            const double dd = g - eps, ig = 1.0 / g;
+            const double ln = log(g / eps);
+            const double cf = S.coef[i];
+            const double q2 = dd * ig;
+            eb = cf * (-dd * dd * ln);
+            f = cf * (-2.0 * dd * ln - dd * q2);
+            h = cf * dmax(-2.0 * ln - 4.0 * q2 + q2 * q2, 0.0);
+          }
         }
       }
-      sm.xa[0][tid] = eb;
-      sm.xa[1][tid] = f;
-      sm.xa[2][tid] = h;
-      sm.ya[0][tid] = 1.0;
-      sm.ya[1][tid] = b0;
-      sm.ya[2][tid] = b1;
-      sm.ya[3][tid] = b2;
-      sm.ya[4][tid] = rr.x;
-      sm.ya[5][tid] = rr.y;
-      sm.ya[6][tid] = rr.z;
-      for (int j = 0; j < 3; ++j) sm.w[j][tid] = j < nm ? w[j] : 0.0;
+      const int M = sm.rM[q];
+      const double bs[3] = {b0, b1, b2}, rs3[3] = {rr.x, rr.y, rr.z};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        sm.u[c][row] = bs[c];
+        sm.v[c][row] = h * bs[c];
+        sm.u[3 + c][row] = rs3[c];
+        sm.v[3 + c][row] = h * rs3[c];
+      }
+#pragma unroll
+      for (int c = 6; c < kUC; ++c) sm.u[c][row] = sm.v[c][row] = 0.0;
+      sm.u[6 + M][row] = 1.0;
+      sm.v[6 + M][row] = f;
+      sm.v[7 + M][row] = eb;
+      const uint32_t li = li4[i];
+      for (int j = 0; j < nm; ++j) {
+        const int m = (li >> (8 * j)) & 0xff;
+        sm.u[6 + m][row] = w[j];
+        sm.v[6 + m][row] = h * w[j];
+      }
     }
     __syncthreads();
-    // Phase B: one warp per run, converged passes (every lane of a pass runs
-    // the same task type with the same or a similar trip count)
+    // Phase B: one warp per run, C = U'^T V on the tensor cores
     for (int q = wid; q < nr; q += kTileWarps) {
       const int r = r0 + q;
-      const int k0 = sm.rs[q], k1 = sm.rs[q + 1];
-      const int m0 = lm_off[r], M = lm_off[r + 1] - m0;
+      const int M = sm.rM[q];
       const int p0 = lp_off[r], NP = lp_off[r + 1] - p0;
       double* P = partial + pbase[r];
-      // B1: run moments (ascending-sample sums, all lanes same trip count)
-      const int nrt = Hess ? kRunTasks : 7;
-      if (lane < nrt) {
-        const double* X = sm.xa[c_task[lane][0]];
-        const double* Y = sm.ya[c_task[lane][1]];
-        const double* Z = sm.ya[c_task[lane][2]];
-        double s = 0;
-        for (int k = k0; k < k1; ++k) s += X[k] * (Y[k] * Z[k]);
-        mom[c_task[lane][3]] = s;
+      const int ra0 = sm.rrow[q], ra1 = sm.rrow[q + 1];
+      const int g = lane >> 2, t4 = lane & 3;
+      const int colF = 6 + M, colE = 7 + M;
+      double d00 = 0, d01 = 0, d10 = 0, d11 = 0, d20 = 0, d21 = 0, d30 = 0, d31 = 0;
+      for (int k = ra0 + t4; k < ra1; k += 4) {
+        const double a0 = sm.u[g][k], a1 = sm.u[8 + g][k];
+        const double b0 = sm.v[g][k], b1 = sm.v[8 + g][k];
+        dmma(d00, d01, a0, b0);
+        dmma(d10, d11, a0, b1);
+        dmma(d20, d21, a1, b0);
+        dmma(d30, d31, a1, b1);
       }
-      // B2: per local master vertex (its incidence list, ascending samples)
-      for (int m = lane; m < M; m += 32) {
-        const int ea = im_off[m0 + m] - ima, eb2 = im_off[m0 + m + 1] - ima;
-        double fw = 0, hb0 = 0, hb1 = 0, hb2 = 0, hr0 = 0, hr1 = 0, hr2 = 0;
-        for (int e = ea; e < eb2; ++e) {
-          const int code = sm.im[e];
-          const int k = code >> 2;
-          const double wj = sm.w[code & 3][k];
-          fw += sm.xa[1][k] * wj;
-          if (Hess) {
-            const double hw = sm.xa[2][k] * wj;
-            hb0 += hw * sm.ya[1][k];
-            hb1 += hw * sm.ya[2][k];
-            hb2 += hw * sm.ya[3][k];
-            hr0 += hw * sm.ya[4][k];
-            hr1 += hw * sm.ya[5][k];
-            hr2 += hw * sm.ya[6][k];
-          }
-        }
-        double* o = mom + kMomRun + 1 + 7 * m;
-        o[0] = fw;
-        o[1] = hb0;
-        o[2] = hb1;
-        o[3] = hb2;
-        o[4] = hr0;
-        o[5] = hr1;
-        o[6] = hr2;
-      }
-      // B3: master pairs straight to the partial
-      if (Hess)
-        for (int p = lane; p < NP; p += 32) {
-          const int ea = ip_off[p0 + p] - ipa, eb2 = ip_off[p0 + p + 1] - ipa;
-          double cv = 0;
-          for (int e = ea; e < eb2; ++e) {
-            const int code = sm.ip[e];
-            const int k = code >> 4;
-            cv += sm.xa[2][k] * (sm.w[(code >> 2) & 3][k] * sm.w[code & 3][k]);
-          }
-          P[kMBase + 10 * M + p] = cv;
-        }
+      C[g][2 * t4] = d00;
+      C[g][2 * t4 + 1] = d01;
+      C[g][8 + 2 * t4] = d10;
+      C[g][9 + 2 * t4] = d11;
+      C[8 + g][2 * t4] = d20;
+      C[8 + g][2 * t4 + 1] = d21;
+      C[8 + g][8 + 2 * t4] = d30;
+      C[8 + g][9 + 2 * t4] = d31;
       __syncwarp();
-      // B4: finalize from the moments
       const double nv[3] = {sm.rn[q][0], sm.rn[q][1], sm.rn[q][2]};
       const d3 n = mk3(nv[0], nv[1], nv[2]);
       const d3 e1 = mk3(sm.re[q][0], sm.re[q][1], sm.re[q][2]);
       const d3 e2 = mk3(sm.re[q][3], sm.re[q][4], sm.re[q][5]);
+      // shared pieces of the SS blocks: T_j(Mbr_i) and Mrr A_j^T
+      if (Hess && lane < 27) {
+        const int i = lane / 9, j = (lane / 3) % 3, c = lane % 3;
+        tm[lane] = comp(Tmap(j, mk3(C[i][3], C[i][4], C[i][5]), e1, e2), c);
+        // bm[j][p][c] = sum_q Mrr[p][q] A_j[c][q]   (here lane = j*9 + p*3 + c)
+        const int jj = lane / 9, p = (lane / 3) % 3, cc = lane % 3;
+        const d3 rc = Trow(jj, cc, e1, e2);
+        bm[lane] = p == 0 ? C[3][3] * rc.x + C[3][4] * rc.y + C[3][5] * rc.z
+                          : (p == 1 ? C[3][4] * rc.x + C[4][4] * rc.y + C[4][5] * rc.z
+                                    : C[3][5] * rc.x + C[4][5] * rc.y + C[5][5] * rc.z);
+      }
+      __syncwarp();
       if (lane < 4) {
-        P[lane] = lane == 0 ? mom[kMomRun] : nv[lane - 1];
+        P[lane] = lane == 0 ? C[6 + M][colE] : nv[lane - 1];
       } else if (lane < 13) {  // slave gradients g_i = -Fb_i n + T_i(Fr)
         const int i = (lane - 4) / 3, a = (lane - 4) % 3;
-        const d3 g = (-mom[kFb + i]) * n + Tmap(i, mk3(mom[kFr], mom[kFr + 1], mom[kFr + 2]), e1, e2);
-        P[lane] = a == 0 ? g.x : (a == 1 ? g.y : g.z);
+        const d3 gv = (-C[i][colF]) * n + Tmap(i, mk3(C[3][colF], C[4][colF], C[5][colF]), e1, e2);
+        P[lane] = comp(gv, a);
       }
-      if (Hess)
+      if (Hess) {
         for (int o = lane; o < 45; o += 32) {  // SS entries
           const int blk = c_ss_entry[o][0], a = c_ss_entry[o][1], c = c_ss_entry[o][2];
           const int i = c_ss_blk[blk][0], j = c_ss_blk[blk][1];
-          const d3 tj = Tmap(j, mk3(mom[kMbr + 3 * i], mom[kMbr + 3 * i + 1], mom[kMbr + 3 * i + 2]), e1, e2);
-          const d3 ti = Tmap(i, mk3(mom[kMbr + 3 * j], mom[kMbr + 3 * j + 1], mom[kMbr + 3 * j + 2]), e1, e2);
-          const double tjc = c == 0 ? tj.x : (c == 1 ? tj.y : tj.z);
-          const double tia = a == 0 ? ti.x : (a == 1 ? ti.y : ti.z);
-          // (A_i Mrr A_j^T)_ac = row_a(A_i) . Mrr . row_c(A_j)
-          const d3 ra = Trow(i, a, e1, e2), rc = Trow(j, c, e1, e2);
-          const d3 mr = mk3(mom[kMrr] * rc.x + mom[kMrr + 1] * rc.y + mom[kMrr + 2] * rc.z,
-                            mom[kMrr + 1] * rc.x + mom[kMrr + 3] * rc.y + mom[kMrr + 4] * rc.z,
-                            mom[kMrr + 2] * rc.x + mom[kMrr + 4] * rc.y + mom[kMrr + 5] * rc.z);
+          const d3 ra = Trow(i, a, e1, e2);
+          const double* B = bm + 9 * j;
+          const double qv = ra.x * B[c] + ra.y * B[3 + c] + ra.z * B[6 + c];
           const double na = nv[a], nc = nv[c];
-          const double v = ((mom[kMbb + c_sym[i][j]] * (na * nc) - na * tjc) - tia * nc) + dot(ra, mr);
+          const double mbb = i <= j ? C[i][j] : C[j][i];
+          const double v = ((mbb * (na * nc) - na * tm[9 * i + 3 * j + c]) - tm[9 * j + 3 * i + a] * nc) + qv;
           P[kSSBase + 9 * blk + 3 * a + c] = v;
           if (i == j && a != c) P[kSSBase + 9 * blk + 3 * c + a] = v;
         }
-      for (int m = lane; m < M; m += 32) {  // s_m and a_{m,i} = -Hwb_{m,i} n + T_i(Hwr_m)
-        const double* mm = mom + kMomRun + 1 + 7 * m;
+        for (int p = lane; p < NP; p += 32) {  // master pairs
+          const int pk = lp[p0 + p];
+          P[kMBase + 10 * M + p] = C[6 + (pk >> 16)][6 + (pk & 0xffff)];
+        }
+      }
+      for (int t = lane; t < (Hess ? 4 * M : M); t += 32) {  // s_m, a_{m,i} = -Hwb_{m,i} n + T_i(Hwr_m)
+        const int m = Hess ? t >> 2 : t, w = Hess ? t & 3 : 0;
         double* out = P + kMBase + 10 * m;
-        out[0] = mm[0];
-        if (Hess) {
-          const d3 hr = mk3(mm[4], mm[5], mm[6]);
-          for (int i = 0; i < 3; ++i) {
-            const d3 av = (-mm[1 + i]) * n + Tmap(i, hr, e1, e2);
-            out[1 + 3 * i] = av.x;
-            out[2 + 3 * i] = av.y;
-            out[3 + 3 * i] = av.z;
-          }
+        if (w == 0) {
+          out[0] = C[6 + m][colF];
+        } else {
+          const int i = w - 1;
+          const d3 av = (-C[6 + m][i]) * n + Tmap(i, mk3(C[6 + m][3], C[6 + m][4], C[6 + m][5]), e1, e2);
+          out[1 + 3 * i] = av.x;
+          out[2 + 3 * i] = av.y;
+          out[3 + 3 * i] = av.z;
         }
       }
       __syncwarp();

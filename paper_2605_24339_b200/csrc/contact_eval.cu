@@ -37,12 +37,12 @@ void launch_k7(Ctx& c, int mode) {
   const int tb = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, 148 * 64));
   if (mode == 1)
     k_tile_partials<true><<<tb, kTileSamples, sizeof(TileSmem), c.stream>>>(
-        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lp_off.p, P.im_off.p, P.im.p,
-        P.ip_off.p, P.ip.p, P.pbase.p, P.partial.p, c.red_u.p);
+        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lp_off.p, P.lp.p, P.li4.p,
+        P.run_row.p, P.pbase.p, P.partial.p, c.red_u.p);
   else
     k_tile_partials<false><<<tb, kTileSamples, sizeof(TileSmem), c.stream>>>(
-        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lp_off.p, P.im_off.p, P.im.p,
-        P.ip_off.p, P.ip.p, P.pbase.p, P.partial.p, c.red_u.p);
+        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lp_off.p, P.lp.p, P.li4.p,
+        P.run_row.p, P.pbase.p, P.partial.p, c.red_u.p);
   ++c.launches;
 }
 
@@ -149,17 +149,11 @@ void build_assembly_plan(Ctx& c) {
     }
     if (R > 0) tile_run.push_back((int32_t)R);
   }
-  std::vector<int64_t> tile_s0(n > 0 ? n : 1, 0);  // sample -> tile start sample
-  for (size_t t = 0; t + 1 < tile_run.size(); ++t)
-    for (int64_t i = run_off[tile_run[t]]; i < run_off[tile_run[t + 1]]; ++i) tile_s0[i] = run_off[tile_run[t]];
-
-  std::vector<int32_t> lm_off{0}, lm_ids, lp_off{0}, lp, im_off{0}, ip_off{0};
-  std::vector<uint16_t> im, ip;
+  std::vector<int32_t> lm_off{0}, lm_ids, lp_off{0}, lp;
+  std::vector<uint32_t> li4(n > 0 ? n : 1, 0xffffffffu);  // per sample local master indices (u8 x 3)
   std::vector<int64_t> pbase(R);
   int64_t plen = 0;
   std::vector<int32_t> loc;
-  std::vector<std::vector<uint16_t>> mi;
-  std::vector<std::pair<int32_t, uint16_t>> pin;
   for (int64_t r = 0; r < R; ++r) {
     loc.clear();
     for (int64_t i = run_off[r]; i < run_off[r + 1]; ++i)
@@ -170,36 +164,35 @@ void build_assembly_plan(Ctx& c) {
     if (loc.size() >= 65535) throw StatusError(GMCP_ERR_CONFIG, "slave triangle touches too many master vertices");
     lm_ids.insert(lm_ids.end(), loc.begin(), loc.end());
     lm_off.push_back((int32_t)lm_ids.size());
-    mi.assign(loc.size(), {});
-    pin.clear();
+    std::vector<int32_t> pr;  // local master pairs (a << 16 | b), a <= b
     for (int64_t i = run_off[r]; i < run_off[r + 1]; ++i) {
-      const int k = (int)(i - tile_s0[i]);
       const int nm = ty[i] == GMCP_FACE ? 3 : (ty[i] == GMCP_EDGE ? 2 : 1);
       int li[3];
+      uint32_t packed = 0xffffffffu;
       for (int j = 0; j < nm; ++j) {
         li[j] = (int)(std::lower_bound(loc.begin(), loc.end(), ms[3 * i + j]) - loc.begin());
-        mi[li[j]].push_back((uint16_t)((k << 2) | j));
+        packed = (packed & ~(0xffu << (8 * j))) | ((uint32_t)li[j] << (8 * j));
       }
+      li4[i] = packed;
       for (int a = 0; a < nm; ++a)
         for (int b = 0; b < nm; ++b)
-          if (li[a] <= li[b]) pin.push_back({(li[a] << 16) | li[b], (uint16_t)((k << 4) | (a << 2) | b)});
+          if (li[a] <= li[b]) pr.push_back((li[a] << 16) | li[b]);
     }
-    for (auto& v : mi) {
-      im.insert(im.end(), v.begin(), v.end());
-      im_off.push_back((int32_t)im.size());
-    }
-    std::stable_sort(pin.begin(), pin.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    for (size_t e = 0; e < pin.size(); ++e) {
-      if (e == 0 || pin[e].first != pin[e - 1].first) {
-        if (e > 0) ip_off.push_back((int32_t)ip.size());
-        lp.push_back(pin[e].first);
-      }
-      ip.push_back(pin[e].second);
-    }
-    if (!pin.empty()) ip_off.push_back((int32_t)ip.size());
+    std::sort(pr.begin(), pr.end());
+    pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+    lp.insert(lp.end(), pr.begin(), pr.end());
     lp_off.push_back((int32_t)lp.size());
     pbase[r] = plen;
     plen += kMBase + 10 * (int64_t)loc.size() + (int64_t)(lp_off[r + 1] - lp_off[r]);
+  }
+  // K7 row offsets of the runs within their tile (each run padded to 4 rows)
+  std::vector<int32_t> run_row(R > 0 ? R : 1, 0);
+  for (size_t t = 0; t + 1 < tile_run.size(); ++t) {
+    int32_t acc = 0;
+    for (int32_t r = tile_run[t]; r < tile_run[t + 1]; ++r) {
+      run_row[r] = acc;
+      acc += ((int32_t)(run_off[r + 1] - run_off[r]) + 3) & ~3;
+    }
   }
   // BCSR pattern + row entries over all N vertex rows
   const int64_t N = c.n_vertices();
@@ -245,10 +238,8 @@ void build_assembly_plan(Ctx& c) {
   P.lm_ids.upload(lm_ids, s);
   P.lp_off.upload(lp_off, s);
   P.lp.upload(lp, s);
-  P.im_off.upload(im_off, s);
-  P.im.upload(im, s);
-  P.ip_off.upload(ip_off, s);
-  P.ip.upload(ip, s);
+  P.li4.upload(li4, s);
+  P.run_row.upload(run_row, s);
   P.pbase.upload(pbase, s);
   P.partial_len = plen;
   P.partial.resize(std::max<int64_t>(plen, 1));

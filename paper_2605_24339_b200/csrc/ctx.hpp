@@ -28,12 +28,8 @@ struct AssemblyPlan {
   // K7 tiles: consecutive runs with <= kTileSamples samples in total
   int64_t n_tiles = 0;
   DBuf<int32_t> tile_run;    // [T+1] first run of each tile
-  // incidence lists (sample index within the tile, packed), per flat local
-  // master vertex / local pair, ascending sample order
-  DBuf<int32_t> im_off;      // [lm_ids.n + 1]
-  DBuf<uint16_t> im;         // (k << 2) | j
-  DBuf<int32_t> ip_off;      // [lp.n + 1]
-  DBuf<uint16_t> ip;         // (k << 4) | (ja << 2) | jb
+  DBuf<uint32_t> li4;        // per sample: local master index of each slot (u8 x 3, 0xff = none)
+  DBuf<int32_t> run_row;     // per run: first K7 row within its tile (runs padded to 4 rows)
   int64_t partial_len = 0;
   DBuf<double> partial;
   // BCSR pattern over all N vertex rows
