@@ -105,57 +105,90 @@ __device__ __forceinline__ d3 row_mv(const Bcsr& A, int v, const double* __restr
   return acc;
 }
 
-// K9a: q = mask .* (H p), partial dot p.q -> alpha = rz / pq (last block).
-__global__ void __launch_bounds__(kThreads) k_spmv_pq(int nv, MatSet M, const double* __restrict__ mask,
-                                                      const double* __restrict__ p, double* __restrict__ q,
+// K9 -- preconditioned CG, two kernels per iteration. The SpMV forms the new
+// search direction on the fly from double-buffered p (p_new = z + beta p_old
+// for every row it touches, written only for its own rows), so the separate
+// p-update pass disappears while the arithmetic stays standard PCG:
+//   p = z + beta p, q = A p, alpha = rz / (p.q), x += alpha p, r -= alpha q,
+//   z = Minv r, beta = rz_new / rz.
+// scal: [0] rz [1] pq [2] alpha [3] beta [4] rr [5] bb
+
+constexpr int kRowLanes = 8;  // lanes per BCSR row in the SpMV
+
+// y_v = sum_j A_vj (z_j + beta p_j) over one row by kRowLanes lanes (fixed butterfly: deterministic)
+__device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __restrict__ z,
+                                      const double* __restrict__ p, double beta, int sub) {
+  d3 acc = mk3(0, 0, 0);
+  const int a = A.rowptr[v], b = A.rowptr[v + 1];
+  for (int k = a + sub; k < b; k += kRowLanes) {
+    const int j = A.cols[k];
+    acc = acc + bmv(A.vals + 9 * (int64_t)k, ld3(z, j) + beta * ld3(p, j));
+  }
+  return acc;
+}
+
+// K9a: p_new = z + beta p_old (own rows), q = mask .* (H p_new), pq -> alpha (last block).
+__global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const double* __restrict__ mask,
+                                                      const double* __restrict__ z, const double* __restrict__ p_old,
+                                                      double* __restrict__ p_new, double* __restrict__ q,
                                                       double* scal, RedSlot rs) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, sub = lane & (kRowLanes - 1);
+  const double beta = scal[3];
   double dots[1] = {0};
-  const int nw = gridDim.x * (kThreads / 32);
-  for (int v = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); v < nv; v += nw) {
-    d3 acc = row_mv(M.el, v, p, lane);
-    for (int k = 0; k < M.np; ++k) acc = acc + row_mv(M.c[k], v, p, lane);
-    acc.x = warp_sum(acc.x);
-    acc.y = warp_sum(acc.y);
-    acc.z = warp_sum(acc.z);
-    if (lane == 0) {
+  const int rows_per_block = kThreads / kRowLanes;
+  // the loop bound is uniform per warp (all lanes reach the shuffles)
+  for (int v0 = blockIdx.x * rows_per_block + (threadIdx.x >> 5) * (32 / kRowLanes); v0 < nv;
+       v0 += gridDim.x * rows_per_block) {
+    const int v = v0 + (lane / kRowLanes);
+    d3 acc = mk3(0, 0, 0);
+    if (v < nv) {
+      acc = row_mv8(M.el, v, z, p_old, beta, sub);
+      for (int k = 0; k < M.np; ++k) acc = acc + row_mv8(M.c[k], v, z, p_old, beta, sub);
+    }
+#pragma unroll
+    for (int o = kRowLanes / 2; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    }
+    if (sub == 0 && v < nv) {
       const d3 m = ld3(mask, v);
       const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
+      const d3 pv = ld3(z, v) + beta * ld3(p_old, v);
       q[3 * v] = y.x;
       q[3 * v + 1] = y.y;
       q[3 * v + 2] = y.z;
-      dots[0] += dot(ld3(p, v), y);
+      p_new[3 * v] = pv.x;
+      p_new[3 * v + 1] = pv.y;
+      p_new[3 * v + 2] = pv.z;
+      dots[0] += dot(pv, y);
     }
   }
   double out[1];
   if (block_reduce_last<1>(dots, rs, out) && threadIdx.x == 0) {
-    scal[1] = out[0];                                    // pq
-    scal[2] = out[0] != 0 ? scal[0] / out[0] : 0.0;      // alpha = rz / pq
+    scal[1] = out[0];                                // pq
+    scal[2] = out[0] != 0 ? scal[0] / out[0] : 0.0;  // alpha = rz / pq
   }
 }
 
-// K9b: x += a p, r -= a q, z = Minv r, partial r.z, r.r -> beta (last block).
-__global__ void __launch_bounds__(kThreads) k_update(int nv, const double* __restrict__ p, const double* __restrict__ q,
-                                                     double* __restrict__ x, double* __restrict__ r,
-                                                     double* __restrict__ z, const double* __restrict__ minv,
-                                                     double* scal, RedSlot rs) {
+// K9b: x += alpha p, r -= alpha q, z = Minv r; rz_new, rr -> beta (last block).
+__global__ void __launch_bounds__(kThreads) k_update_cg(int nv, const double* __restrict__ p,
+                                                        const double* __restrict__ q, double* __restrict__ x,
+                                                        double* __restrict__ r, double* __restrict__ z,
+                                                        const double* __restrict__ minv, double* scal, RedSlot rs) {
   const double a = scal[2];
   double dots[2] = {0, 0};
   for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
-    const d3 pv = ld3nc(p, v), qv = ld3nc(q, v);
-    d3 xv = ld3nc(x, v), rv = ld3nc(r, v);
-    xv = xv + a * pv;
-    rv = rv - a * qv;
+    const d3 xv = ld3nc(x, v) + a * ld3nc(p, v);
+    const d3 rv = ld3nc(r, v) - a * ld3nc(q, v);
     const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
-    x[3 * v] = xv.x;
-    x[3 * v + 1] = xv.y;
-    x[3 * v + 2] = xv.z;
-    r[3 * v] = rv.x;
-    r[3 * v + 1] = rv.y;
-    r[3 * v + 2] = rv.z;
-    z[3 * v] = zv.x;
-    z[3 * v + 1] = zv.y;
-    z[3 * v + 2] = zv.z;
+    const double xa[3] = {xv.x, xv.y, xv.z}, ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      x[3 * v + c] = xa[c];
+      r[3 * v + c] = ra[c];
+      z[3 * v + c] = za[c];
+    }
     dots[0] += dot(rv, zv);
     dots[1] += dot(rv, rv);
   }
@@ -168,14 +201,7 @@ __global__ void __launch_bounds__(kThreads) k_update(int nv, const double* __res
   }
 }
 
-// K9c: p = z + beta p
-__global__ void k_pupdate(int64_t n, const double* __restrict__ z, double* __restrict__ p, const double* scal) {
-  const double b = scal[3];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = z[i] + b * p[i];
-}
-
-// PCG init: r = b = -mask.*grad, z = Minv r, p = z, x = 0; rz, rr, bb.
+// PCG init: x = p = 0, r = b = -mask.*grad, z = Minv r; rz, rr, bb; beta = 0.
 __global__ void __launch_bounds__(kThreads) k_pcg_init(int nv, const double* __restrict__ grad,
                                                        const double* __restrict__ mask, const double* __restrict__ minv,
                                                        double* __restrict__ x, double* __restrict__ r,
@@ -186,19 +212,20 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(int nv, const double* __r
     const d3 m = ld3(mask, v), g = ld3(grad, v);
     const d3 rv = mk3(-m.x * g.x, -m.y * g.y, -m.z * g.z);
     const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
-    for (int k = 0; k < 3; ++k) x[3 * v + k] = 0;
-    r[3 * v] = rv.x;
-    r[3 * v + 1] = rv.y;
-    r[3 * v + 2] = rv.z;
-    z[3 * v] = p[3 * v] = zv.x;
-    z[3 * v + 1] = p[3 * v + 1] = zv.y;
-    z[3 * v + 2] = p[3 * v + 2] = zv.z;
+    const double ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
+    for (int k = 0; k < 3; ++k) {
+      x[3 * v + k] = 0;
+      p[3 * v + k] = 0;
+      r[3 * v + k] = ra[k];
+      z[3 * v + k] = za[k];
+    }
     dots[0] += dot(rv, zv);
     dots[1] += dot(rv, rv);
   }
   double out[2];
   if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
     scal[0] = out[0];  // rz
+    scal[3] = 0;       // beta: first direction p = z
     scal[4] = out[1];  // rr
     scal[5] = out[1];  // bb
   }
@@ -381,7 +408,7 @@ struct SystemImpl {
   std::vector<uint8_t> fixed;
   std::vector<std::unique_ptr<PairRt>> pairs;
   // device
-  DBuf<double> x, dx, xtry, rest_d, fext_d, mask_d, grad, gel, r, z, p, q, minv, scal, parts, lsco, eel;
+  DBuf<double> x, dx, xtry, rest_d, fext_d, mask_d, grad, gel, r, z, p, q, w, minv, scal, parts, lsco, eel;
   DBuf<unsigned int> counter;
   DBuf<unsigned long long> redu;
   DBuf<int32_t> k_rowptr, k_cols;
@@ -594,7 +621,8 @@ double assemble(SystemImpl& S, double lambda) {
   return from_ord_bits(u);
 }
 
-// Block-Jacobi PCG on the masked system. Returns iterations; dx in S.dx.
+// Block-Jacobi PCG on the masked system (chunks of iterations replayed as one
+// CUDA graph). Returns iterations; dx in S.dx.
 int pcg(SystemImpl& S, double tol, int maxit, double* rel_out) {
   const int nv = S.nv();
   const MatSet M = mats(S);
@@ -602,7 +630,7 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out) {
   k_pcg_init<<<kBlocks, kThreads, 0, S.stream>>>(nv, S.grad.p, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p, S.p.p,
                                                  S.scal.p, S.slot(0));
   S.launches += 2;
-  double h[6];
+  double h[9];
   GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
   S.sync();
   const double bb = h[5];
@@ -611,23 +639,37 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out) {
     return 0;
   }
   const double target = tol * tol * bb;
+  const int chunk = 16;
+  const int gsp = std::min(grid_for((int64_t)nv * kRowLanes, kThreads), kBlocks);
+  // one chunk of iterations as a CUDA graph (pointers fixed for this solve)
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  GMCP_CUDA(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
+  for (int k = 0; k < chunk; ++k) {  // p ping-pongs between S.p and S.w (chunk is even)
+    double* p_old = (k & 1) ? S.w.p : S.p.p;
+    double* p_new = (k & 1) ? S.p.p : S.w.p;
+    k_spmv_cg<<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p, S.slot(1));
+    k_update_cg<<<kBlocks, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
+                                                    S.slot(2));
+  }
+  GMCP_CUDA(cudaStreamEndCapture(S.stream, &graph));
+  GMCP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   int it = 0;
-  const int chunk = 8;
-  const int gsp = grid_for((int64_t)nv * 32, kThreads);
   while (it < maxit) {
-    for (int k = 0; k < chunk && it < maxit; ++k, ++it) {
-      k_spmv_pq<<<std::min(gsp, kBlocks), kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.p.p, S.q.p, S.scal.p,
-                                                                    S.slot(1));
-      k_update<<<kBlocks, kThreads, 0, S.stream>>>(nv, S.p.p, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
-                                                  S.slot(2));
-      k_pupdate<<<grid_for(S.n_dof, 256), 256, 0, S.stream>>>(S.n_dof, S.z.p, S.p.p, S.scal.p);
-      S.launches += 3;
-    }
+    GMCP_CUDA(cudaGraphLaunch(exec, S.stream));
+    S.launches += 2 * chunk;
+    it += chunk;
     GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
     S.sync();
-    if (!(h[4] > target)) break;  // rr <= tol^2 bb (or NaN guard below)
-    if (!std::isfinite(h[4])) throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
+    if (!std::isfinite(h[4])) {
+      cudaGraphExecDestroy(exec);
+      cudaGraphDestroy(graph);
+      throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
+    }
+    if (!(h[4] > target)) break;  // rr <= tol^2 bb
   }
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
   *rel_out = std::sqrt(h[4] / bb);
   GMCP_CUDA(cudaGetLastError());
   return it;
@@ -654,7 +696,7 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
   for (int64_t d = 0; d < S.n_dof; ++d)
     if (S.fixed[d]) S.x_host[d] = S.dirichlet[d];
   const int64_t n = S.n_dof;
-  for (auto* b : {&S.x, &S.dx, &S.xtry, &S.grad, &S.gel, &S.r, &S.z, &S.p, &S.q}) b->resize(n);
+  for (auto* b : {&S.x, &S.dx, &S.xtry, &S.grad, &S.gel, &S.r, &S.z, &S.p, &S.q, &S.w}) b->resize(n);
   S.minv.resize(3 * n);
   S.scal.resize(16);
   S.eel.resize(4);
