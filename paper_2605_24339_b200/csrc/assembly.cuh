@@ -42,13 +42,19 @@ constexpr int kRunMasters = 8;                          // local master vertices
 constexpr int kTileRows = kTileSamples + 3 * kTileRuns;  // runs padded to multiples of 4 rows
 constexpr int kTileWarps = kTileSamples / 32;
 
-// Partial layout (doubles) at pbase[r]:
+// Partial layout (doubles) at pbase[r] -- self-describing, so K8 needs no
+// other per-run index:
 //   [0] energy  [1..3] n  [4..12] slave gradients (i*3+k)
 //   [13..66] SS blocks (0,0),(0,1),(0,2),(1,1),(1,2),(2,2), 9 each, row-major
-//   [67 + 10m] s_m, [68 + 10m + 3i + k] a_{m,i}[k]   (m < M local master verts)
-//   [67 + 10M + p] c_p                                 (p < P local master pairs)
+//   [67] M   [68..70] slave vertex ids   [71 .. 71+M) local master vertex ids
+//   [71 + M + 10m] s_m, [+1 + 3i + k] a_{m,i}[k]          (m < M)
+//   [71 + 11M + tri(m,l)] c_ml, dense upper triangle m <= l (0 when no sample has both)
 constexpr int kSSBase = 13;
-constexpr int kMBase = 67;
+constexpr int kMcnt = 67, kSlv = 68, kHdr = 71;
+__host__ __device__ constexpr int m_base(int M) { return kHdr + M; }
+__host__ __device__ constexpr int pair_base(int M) { return kHdr + 11 * M; }
+__host__ __device__ constexpr int partial_size(int M) { return kHdr + 11 * M + M * (M + 1) / 2; }
+__host__ __device__ constexpr int tri_index(int m, int l, int M) { return m * M - m * (m - 1) / 2 + (l - m); }
 
 
 // ---------------------------------------------------------------------------
@@ -142,9 +148,8 @@ template <bool Hess>
 __global__ void __launch_bounds__(kTileSamples, 4) k_tile_partials(
     DevSamples S, const double* __restrict__ x, int64_t n_tiles, const int32_t* __restrict__ tile_run,
     const int64_t* __restrict__ run_off, const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm_off,
-    const int32_t* __restrict__ lp_off, const int32_t* __restrict__ lp, const uint32_t* __restrict__ li4,
-    const int32_t* __restrict__ run_row, const int64_t* __restrict__ pbase, double* __restrict__ partial,
-    unsigned long long* __restrict__ red) {
+    const int32_t* __restrict__ lm_ids, const uint32_t* __restrict__ li4, const int32_t* __restrict__ run_row,
+    const int64_t* __restrict__ pbase, double* __restrict__ partial, unsigned long long* __restrict__ red) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -259,7 +264,6 @@ __global__ void __launch_bounds__(kTileSamples, 4) k_tile_partials(
     for (int q = wid; q < nr; q += kTileWarps) {
       const int r = r0 + q;
       const int M = sm.rM[q];
-      const int p0 = lp_off[r], NP = lp_off[r + 1] - p0;
       double* P = partial + pbase[r];
       const int ra0 = sm.rrow[q], ra1 = sm.rrow[q + 1];
       const int g = lane >> 2, t4 = lane & 3;
@@ -318,14 +322,21 @@ __global__ void __launch_bounds__(kTileSamples, 4) k_tile_partials(
           P[kSSBase + 9 * blk + 3 * a + c] = v;
           if (i == j && a != c) P[kSSBase + 9 * blk + 3 * c + a] = v;
         }
-        for (int p = lane; p < NP; p += 32) {  // master pairs
-          const int pk = lp[p0 + p];
-          P[kMBase + 10 * M + p] = C[6 + (pk >> 16)][6 + (pk & 0xffff)];
+        for (int t = lane; t < M * (M + 1) / 2; t += 32) {  // master pairs, dense upper triangle
+          int m = 0, l = t;
+          while (l >= M - m) {
+            l -= M - m;
+            ++m;
+          }
+          P[pair_base(M) + t] = C[6 + m][6 + m + l];
         }
       }
+      if (lane < M) P[kHdr + lane] = (double)lm_ids[lm_off[r] + lane];  // header: local master ids
+      else if (lane >= 28 && lane < 31) P[kSlv + lane - 28] = (double)run_slave[3 * r + lane - 28];
+      else if (lane == 31) P[kMcnt] = (double)M;
       for (int t = lane; t < (Hess ? 4 * M : M); t += 32) {  // s_m, a_{m,i} = -Hwb_{m,i} n + T_i(Hwr_m)
         const int m = Hess ? t >> 2 : t, w = Hess ? t & 3 : 0;
-        double* out = P + kMBase + 10 * m;
+        double* out = P + m_base(M) + 10 * m;
         if (w == 0) {
           out[0] = C[6 + m][colF];
         } else {
@@ -357,8 +368,9 @@ __global__ void __launch_bounds__(kRedThreads) k_run_energy(int64_t n_runs, cons
 // ---------------------------------------------------------------------------
 // K8
 
-constexpr int kRowCols = 48;  // shared-memory row accumulator capacity (blocks)
-constexpr int kGatherWarps = 8;
+constexpr int kRowCols = 40;  // shared-memory row accumulator capacity (blocks)
+constexpr int kGatherWarps = 4;
+constexpr int kRowGroup = 16;  // lanes per row (16 beats 8 and 32 on C3)
 
 struct RowSmem {
   int cols[kRowCols];
@@ -373,10 +385,9 @@ __device__ __forceinline__ int find_col(const int32_t* cols, int lo, int hi, int
   return lo;
 }
 
-// Contribution block of entry element b; returns its column or -1.
-__device__ __forceinline__ int entry_block(int role, int b, int64_t r, const double* __restrict__ P, int M,
-                                           const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm,
-                                           const int32_t* __restrict__ lpp, double* blk) {
+// Contribution block of element b of a row entry (run partial P, role); returns
+// its column, or -1 when the block is identically zero (absent master pair).
+__device__ __forceinline__ int entry_block(int role, int b, const double* __restrict__ P, int M, double* blk) {
   const double nn[3] = {P[1], P[2], P[3]};
   if (role < 3) {
     const int i = role;
@@ -394,83 +405,84 @@ __device__ __forceinline__ int entry_block(int role, int b, int64_t r, const dou
 #pragma unroll
           for (int c = 0; c < 3; ++c) blk[3 * a + c] = Sb[3 * c + a];
       }
-      return run_slave[3 * r + j];
+      return (int)P[kSlv + j];
     }
     const int k = b - 3;
-    const double* A = P + kMBase + 10 * k + 1 + 3 * i;
+    const double* A = P + m_base(M) + 10 * k + 1 + 3 * i;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int c = 0; c < 3; ++c) blk[3 * a + c] = A[a] * nn[c];
-    return lm[k];
+    return (int)P[kHdr + k];
   }
   const int m = role - 3;
   if (b < 3) {
-    const double* A = P + kMBase + 10 * m + 1 + 3 * b;
+    const double* A = P + m_base(M) + 10 * m + 1 + 3 * b;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int c = 0; c < 3; ++c) blk[3 * a + c] = nn[a] * A[c];
-    return run_slave[3 * r + b];
+    return (int)P[kSlv + b];
   }
-  const int p = b - 3;
-  const int pk = lpp[p];
-  const int la = pk >> 16, lb = pk & 0xffff;
-  if (la != m && lb != m) return -1;
-  const double cv = P[kMBase + 10 * M + p];
+  const int l = b - 3;
+  const double cv = P[pair_base(M) + (m <= l ? tri_index(m, l, M) : tri_index(l, m, M))];
+  if (cv == 0) return -1;  // nonzero only if some sample holds both m and l (a listed pair)
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int c = 0; c < 3; ++c) blk[3 * a + c] = cv * (nn[a] * nn[c]);
-  return lm[la == m ? lb : la];
+  return (int)P[kHdr + l];
 }
 
 template <bool Hess>
-__global__ void __launch_bounds__(32 * kGatherWarps) k_row_gather(
-    int32_t n_rows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols, double* __restrict__ vals,
-    const int32_t* __restrict__ ent_off, const int64_t* __restrict__ ent, const int32_t* __restrict__ run_slave,
-    const int32_t* __restrict__ lm_off, const int32_t* __restrict__ lm_ids, const int32_t* __restrict__ lp_off,
-    const int32_t* __restrict__ lp, const int64_t* __restrict__ pbase, const double* __restrict__ partial,
-    double* __restrict__ grad) {
-  __shared__ RowSmem rsm[kGatherWarps];
-  const int lane = threadIdx.x & 31;
-  RowSmem& R = rsm[threadIdx.x >> 5];
-  const int64_t nwarps = (int64_t)gridDim.x * kGatherWarps;
-  for (int64_t v = blockIdx.x * (int64_t)kGatherWarps + (threadIdx.x >> 5); v < n_rows; v += nwarps) {
+__global__ void __launch_bounds__(32 * kGatherWarps) k_row_gather(int32_t n_rows, const int32_t* __restrict__ rowptr,
+                                                                  const int32_t* __restrict__ cols,
+                                                                  double* __restrict__ vals,
+                                                                  const int32_t* __restrict__ ent_off,
+                                                                  const int64_t* __restrict__ ent,
+                                                                  const double* __restrict__ partial,
+                                                                  double* __restrict__ grad) {
+  // kRowGroup lanes per vertex row: a row entry has 3 + M <= 11 blocks
+  __shared__ RowSmem rsm[(32 / kRowGroup) * kGatherWarps];
+  const int lane = threadIdx.x & 31, hl = lane & (kRowGroup - 1);
+  const unsigned hmask = (kRowGroup == 32 ? 0xffffffffu : ((1u << kRowGroup) - 1u)) << (lane & ~(kRowGroup - 1));
+  RowSmem& R = rsm[threadIdx.x / kRowGroup];
+  const int64_t ngroups = (int64_t)gridDim.x * (32 / kRowGroup) * kGatherWarps;
+  for (int64_t v = blockIdx.x * (int64_t)((32 / kRowGroup) * kGatherWarps) + (threadIdx.x / kRowGroup); v < n_rows;
+       v += ngroups) {
     const int e0 = ent_off[v], e1 = ent_off[v + 1];
     const int c0 = Hess ? rowptr[v] : 0, c1 = Hess ? rowptr[v + 1] : 0;
     const int nc = c1 - c0;
     const bool in_smem = Hess && nc <= kRowCols;
     if (Hess) {
       if (in_smem) {
-        for (int q = lane; q < nc; q += 32) R.cols[q] = cols[c0 + q];
-        for (int q = lane; q < 9 * nc; q += 32) R.acc[q] = 0;
+        for (int q = hl; q < nc; q += kRowGroup) R.cols[q] = cols[c0 + q];
+        for (int q = hl; q < 9 * nc; q += kRowGroup) R.acc[q] = 0;
       } else {
-        for (int q = lane; q < 9 * nc; q += 32) vals[9 * (int64_t)c0 + q] = 0;
+        for (int q = hl; q < 9 * nc; q += kRowGroup) vals[9 * (int64_t)c0 + q] = 0;
       }
     }
     d3 g = mk3(0, 0, 0);
-    __syncwarp();
+    __syncwarp(hmask);
+    int64_t en_next = e0 < e1 ? ent[e0] : 0;
     for (int e = e0; e < e1; ++e) {
-      const int64_t en = ent[e];
-      const int64_t r = en >> 20;
-      const int role = (int)(en & 0xfffff);
-      const double* P = partial + pbase[r];
-      if (lane == 0) {
+      const int64_t en = en_next;
+      if (e + 1 < e1) en_next = ent[e + 1];  // prefetch the next entry
+      const double* P = partial + (en >> 8);
+      const int role = (int)(en & 0xff);
+      const int M = (int)P[kMcnt];
+      if (hl == 0) {
         if (role < 3) {
           g = g + mk3(P[4 + 3 * role], P[5 + 3 * role], P[6 + 3 * role]);
         } else {
-          const double s = P[kMBase + 10 * (role - 3)];
-          g = g + s * mk3(P[1], P[2], P[3]);
+          g = g + P[m_base(M) + 10 * (role - 3)] * mk3(P[1], P[2], P[3]);
         }
       }
       if (Hess) {
-        const int m0 = lm_off[r], M = lm_off[r + 1] - m0;
-        const int p0 = lp_off[r], NP = lp_off[r + 1] - p0;
-        const int nb = 3 + (role < 3 ? M : NP);
-        for (int b = lane; b < nb; b += 32) {
+        const int nb = 3 + M;
+        for (int b = hl; b < nb; b += kRowGroup) {
           double blk[9];
-          const int col = entry_block(role, b, r, P, M, run_slave, lm_ids + m0, lp + p0, blk);
+          const int col = entry_block(role, b, P, M, blk);
           if (col < 0) continue;
           double* out = in_smem ? R.acc + 9 * find_col(R.cols, 0, nc, col)
                                 : vals + 9 * (int64_t)find_col(cols, c0, c1, col);
@@ -478,16 +490,16 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_row_gather(
           for (int q = 0; q < 9; ++q) out[q] += blk[q];
         }
       }
-      __syncwarp();
+      __syncwarp(hmask);
     }
     if (in_smem)
-      for (int q = lane; q < 9 * nc; q += 32) vals[9 * (int64_t)c0 + q] = R.acc[q];
-    if (lane == 0) {
+      for (int q = hl; q < 9 * nc; q += kRowGroup) vals[9 * (int64_t)c0 + q] = R.acc[q];
+    if (hl == 0) {
       grad[3 * v] = g.x;
       grad[3 * v + 1] = g.y;
       grad[3 * v + 2] = g.z;
     }
-    __syncwarp();
+    __syncwarp(hmask);
   }
 }
 

@@ -37,29 +37,25 @@ void launch_k7(Ctx& c, int mode) {
   const int tb = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, 148 * 64));
   if (mode == 1)
     k_tile_partials<true><<<tb, kTileSamples, sizeof(TileSmem), c.stream>>>(
-        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lp_off.p, P.lp.p, P.li4.p,
+        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lm_ids.p, P.li4.p,
         P.run_row.p, P.pbase.p, P.partial.p, c.red_u.p);
   else
     k_tile_partials<false><<<tb, kTileSamples, sizeof(TileSmem), c.stream>>>(
-        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lp_off.p, P.lp.p, P.li4.p,
+        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lm_ids.p, P.li4.p,
         P.run_row.p, P.pbase.p, P.partial.p, c.red_u.p);
   ++c.launches;
 }
 
 void launch_k8(Ctx& c, int mode) {
   AssemblyPlan& P = c.plan;
-  const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P.n_rows + kGatherWarps - 1) / kGatherWarps,
+  const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P.n_rows + (32 / kRowGroup) * kGatherWarps - 1) / ((32 / kRowGroup) * kGatherWarps),
                                                              148 * 32));
   if (mode == 1)
     k_row_gather<true><<<gb, 32 * kGatherWarps, 0, c.stream>>>(P.n_rows, P.rowptr.p, P.cols.p, P.vals.p,
-                                                                P.row_ent_off.p, P.row_ent.p, P.run_slave.p,
-                                                                P.lm_off.p, P.lm_ids.p, P.lp_off.p, P.lp.p, P.pbase.p,
-                                                                P.partial.p, c.grad.p);
+                                                                P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   else
     k_row_gather<false><<<gb, 32 * kGatherWarps, 0, c.stream>>>(P.n_rows, P.rowptr.p, P.cols.p, P.vals.p,
-                                                                 P.row_ent_off.p, P.row_ent.p, P.run_slave.p,
-                                                                 P.lm_off.p, P.lm_ids.p, P.lp_off.p, P.lp.p, P.pbase.p,
-                                                                 P.partial.p, c.grad.p);
+                                                                 P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   ++c.launches;
 }
 
@@ -183,7 +179,7 @@ void build_assembly_plan(Ctx& c) {
     lp.insert(lp.end(), pr.begin(), pr.end());
     lp_off.push_back((int32_t)lp.size());
     pbase[r] = plen;
-    plen += kMBase + 10 * (int64_t)loc.size() + (int64_t)(lp_off[r + 1] - lp_off[r]);
+    plen += partial_size((int)loc.size());
   }
   // K7 row offsets of the runs within their tile (each run padded to 4 rows)
   std::vector<int32_t> run_row(R > 0 ? R : 1, 0);
@@ -203,12 +199,12 @@ void build_assembly_plan(Ctx& c) {
     const int32_t* L = lm_ids.data() + lm_off[r];
     const int M = lm_off[r + 1] - lm_off[r];
     for (int i = 0; i < 3; ++i) {
-      rent[s[i]].push_back((r << 20) | i);
+      rent[s[i]].push_back((pbase[r] << 8) | i);
       for (int j = 0; j < 3; ++j) rc[s[i]].push_back(s[j]);
       for (int k = 0; k < M; ++k) rc[s[i]].push_back(L[k]);
     }
     for (int k = 0; k < M; ++k) {
-      rent[L[k]].push_back((r << 20) | (3 + k));
+      rent[L[k]].push_back((pbase[r] << 8) | (3 + k));
       for (int j = 0; j < 3; ++j) rc[L[k]].push_back(s[j]);
     }
     for (int p = lp_off[r]; p < lp_off[r + 1]; ++p) {
