@@ -1,14 +1,12 @@
 // Contact assembly kernels (included once, by contact_eval.cu).
 //
-//  K7 k_tile_partials  one 256-thread block per tile of consecutive slave
-//                      runs (<= 256 samples). Phase A: one thread per sample
-//                      computes gap, barrier and the in-plane vector r into
-//                      shared memory; the tile's incidence lists are staged
-//                      into shared memory alongside. Phase B: one warp per
-//                      run; lanes own the run's moment sums (ascending sample
-//                      order) in a per-warp shared buffer, then finalize the
-//                      run's blocks from the moments and write the partial.
-//  K8 k_row_gather     one warp per vertex row: sums the finalized blocks of
+//  K7 k_run_partials  one warp per slave run (consecutive samples sharing a
+//                      slave triangle), no block-level synchronisation. Lanes
+//                      own samples: gap, barrier and the in-plane vector r go
+//                      into a per-warp staging tile, the run's moments are one
+//                      Gram product on the FP64 tensor cores, and the warp
+//                      finalizes the run's blocks into its partial.
+//  K8 k_row_gather     16 lanes per vertex row: sums the finalized blocks of
 //                      the runs touching the vertex (ascending run order) in a
 //                      shared-memory row accumulator, then writes the BCSR row
 //                      and the gradient once.
@@ -36,11 +34,8 @@
 namespace gmcp_b200 {
 namespace {
 
-constexpr int kTileSamples = 128;                       // samples per K7 tile (= block threads)
-constexpr int kTileRuns = 8;
-constexpr int kRunMasters = 8;                          // local master vertices per run (planner splits)
-constexpr int kTileRows = kTileSamples + 3 * kTileRuns;  // runs padded to multiples of 4 rows
-constexpr int kTileWarps = kTileSamples / 32;
+constexpr int kRunSamples = 128;  // planner splits longer runs (bounds per-warp work)
+constexpr int kRunMasters = 8;    // local master vertices per run (planner splits)
 
 // Partial layout (doubles) at pbase[r] -- self-describing, so K8 needs no
 // other per-run index:
@@ -99,23 +94,27 @@ __global__ void k_derive(int64_t n, const int8_t* __restrict__ type, const doubl
 // The accumulation order inside DMMA is fixed by the hardware, so results are
 // bitwise reproducible.
 
-constexpr int kUC = 16;  // U' / V columns
+constexpr int kUC = 16;               // U' / V columns
+constexpr int kRunWarps = 4;          // warps (= runs in flight) per K7 block
+#ifndef K7_MINB
+#define K7_MINB 4
+#endif
+constexpr int kStage = 16;            // sample rows staged per tensor-core pass
+constexpr int kLDS = kStage + 4;      // column stride (doubles): conflict-free fragment loads
 
-constexpr int kLD = kTileRows + 4;  // column stride (doubles): lanes of a warp hit distinct banks
-
-struct TileSmem {
-  double u[kUC][kLD];  // U' columns (column-major: consecutive samples are consecutive)
-  double v[kUC][kLD];  // V columns
-  double cbuf[kTileWarps][kUC][kUC + 1];  // per-warp C
-  double tm[kTileWarps][27];  // T_j(Mbr_i): [i][j][comp]
-  double bm[kTileWarps][27];  // Mrr A_j^T: [j][p][c]
-  double ra[kTileRuns][9];
-  double rn[kTileRuns][3];
-  double re[kTileRuns][6];
-  double ricn[kTileRuns];   // 1 / |c| (0 for degenerate)
-  int rs[kTileRuns + 1];    // sample offsets of the runs within the tile
-  int rrow[kTileRuns + 1];  // padded row offsets of the runs within the tile
-  int rM[kTileRuns];
+// Per-warp shared memory: staged U' / V rows (column-major); after the last
+// pass the same space holds C.
+struct RunSmem {
+  union {
+    struct {
+      double u[kUC][kLDS];
+      double v[kUC][kLDS];
+    };
+    double C[kUC][kUC + 1];
+  };
+  double tm[27];  // T_j(Mbr_i): [i][j][comp]
+  double bm[27];  // Mrr A_j^T: [j][p][c]
+  double geo[19];  // a0 a1 a2 | e1 e2 | n | 1/|c|
 };
 
 __constant__ unsigned char c_ss_entry[45][3];  // (block, a, c) of the 45 unique SS entries
@@ -144,212 +143,228 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// K7: one warp per run, no block-level synchronisation. Lanes own samples
+// (32 per chunk); each chunk is staged 16 rows at a time and multiplied into
+// the warp's C = U'^T V accumulators on the tensor cores (rows in ascending
+// sample order, padded with zero rows to a multiple of 4). The run's blocks
+// are then finalized from C and written as its self-describing partial.
 template <bool Hess>
-__global__ void __launch_bounds__(kTileSamples, 4) k_tile_partials(
-    DevSamples S, const double* __restrict__ x, int64_t n_tiles, const int32_t* __restrict__ tile_run,
-    const int64_t* __restrict__ run_off, const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm_off,
-    const int32_t* __restrict__ lm_ids, const uint32_t* __restrict__ li4, const int32_t* __restrict__ run_row,
-    const int64_t* __restrict__ pbase, double* __restrict__ partial, unsigned long long* __restrict__ red) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double (*C)[kUC + 1] = sm.cbuf[wid];
-  double* tm = sm.tm[wid];
-  double* bm = sm.bm[wid];
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int r0 = tile_run[tile], nr = tile_run[tile + 1] - r0;
-    const int64_t s0 = run_off[r0];
-    if (tid < nr) {  // run geometry
-      const int r = r0 + tid;
-      const d3 a0 = ld3(x, run_slave[3 * r]), a1 = ld3(x, run_slave[3 * r + 1]), a2 = ld3(x, run_slave[3 * r + 2]);
+__global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
+    DevSamples S, const double* __restrict__ x, int64_t n_runs, const int64_t* __restrict__ run_off,
+    const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm_off, const int32_t* __restrict__ lm_ids,
+    const uint32_t* __restrict__ li4, const int64_t* __restrict__ pbase, double* __restrict__ partial,
+    unsigned long long* __restrict__ red) {
+  __shared__ RunSmem wsm[kRunWarps];
+  const int lane = threadIdx.x & 31;
+  RunSmem& W = wsm[threadIdx.x >> 5];
+  const int g = lane >> 2, t4 = lane & 3;
+  // lane-constant SS entry assignments (o = lane, lane + 32), packed
+  // blk | a << 3 | c << 5 | i << 7 | j << 9
+  int ss_pk[2] = {0, 0};
+#pragma unroll
+  for (int h2 = 0; h2 < 2; ++h2) {
+    const int o = lane + 32 * h2;
+    if (o < 45) {
+      const int blk = c_ss_entry[o][0];
+      ss_pk[h2] = blk | (c_ss_entry[o][1] << 3) | (c_ss_entry[o][2] << 5) | (c_ss_blk[blk][0] << 7) |
+                  (c_ss_blk[blk][1] << 9);
+    }
+  }
+  // persistent warps; the next run's metadata loads during this run
+  struct Meta {
+    int64_t s0, s1, pb;
+    int M, sid0, sid1, sid2, my_lm;
+  };
+  auto load_meta = [&](int64_t r, Meta& m) {
+    m.s0 = run_off[r];
+    m.s1 = run_off[r + 1];
+    const int L0 = lm_off[r];
+    m.M = lm_off[r + 1] - L0;
+    m.sid0 = run_slave[3 * r];
+    m.sid1 = run_slave[3 * r + 1];
+    m.sid2 = run_slave[3 * r + 2];
+    m.pb = pbase[r];
+    m.my_lm = lane < m.M ? lm_ids[L0 + lane] : 0;
+  };
+  const int64_t stride = (int64_t)gridDim.x * kRunWarps;
+  int64_t r = blockIdx.x * (int64_t)kRunWarps + (threadIdx.x >> 5);
+  Meta nxt;
+  if (r < n_runs) load_meta(r, nxt);
+  for (; r < n_runs; r += stride) {
+    const Meta cur = nxt;
+    if (r + stride < n_runs) load_meta(r + stride, nxt);
+    const int64_t s0 = cur.s0, s1 = cur.s1, pb = cur.pb;
+    const int M = cur.M, sid0 = cur.sid0, sid1 = cur.sid1, sid2 = cur.sid2, my_lm = cur.my_lm;
+    {
+      const d3 a0 = ld3(x, sid0), a1 = ld3(x, sid1), a2 = ld3(x, sid2);
       const d3 e1 = a1 - a0, e2 = a2 - a0;
-      const d3 c = cross(e1, e2);
-      const double cn = norm(c);
-      const d3 n = c / cn;
-      const double av[9] = {a0.x, a0.y, a0.z, a1.x, a1.y, a1.z, a2.x, a2.y, a2.z};
-      for (int q = 0; q < 9; ++q) sm.ra[tid][q] = av[q];
-      sm.rn[tid][0] = n.x;
-      sm.rn[tid][1] = n.y;
-      sm.rn[tid][2] = n.z;
-      const double ev[6] = {e1.x, e1.y, e1.z, e2.x, e2.y, e2.z};
-      for (int q = 0; q < 6; ++q) sm.re[tid][q] = ev[q];
-      sm.ricn[tid] = cn > 0 ? 1.0 / cn : 0.0;
-      sm.rs[tid] = (int)(run_off[r] - s0);
-      sm.rrow[tid] = run_row[r];
-      sm.rM[tid] = lm_off[r + 1] - lm_off[r];
-      if (!(cn > 0)) atomicMin(&red[1], (unsigned long long)run_off[r]);
-    }
-    if (tid == 0) {
-      sm.rs[nr] = (int)(run_off[r0 + nr] - s0);
-      sm.rrow[nr] = run_row[r0 + nr - 1] + (((int)(run_off[r0 + nr] - run_off[r0 + nr - 1]) + 3) & ~3);
-    }
-    __syncthreads();
-    // padding rows (<= 3 per run) are zero
-    if (tid < 3 * nr) {
-      const int q = tid / 3;
-      const int row = sm.rrow[q] + (sm.rs[q + 1] - sm.rs[q]) + tid % 3;
-      if (row < sm.rrow[q + 1])
-        for (int c = 0; c < kUC; ++c) sm.u[c][row] = sm.v[c][row] = 0.0;
-    }
-    // Phase A: one thread per sample -> its U' and V rows
-    const int ns = sm.rs[nr];
-    if (tid < ns) {
-      int q = 0;
-      {
-        int lo = 0, hi = nr;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (sm.rs[mid] <= tid) lo = mid; else hi = mid;
-        }
-        q = lo;
+      const d3 cr = cross(e1, e2);
+      const double cn = norm(cr);
+      const d3 n = cr / cn;
+      if (lane == 0) {
+        const double gv[19] = {a0.x, a0.y, a0.z, a1.x, a1.y, a1.z, a2.x, a2.y, a2.z, e1.x,
+                               e1.y, e1.z, e2.x, e2.y, e2.z, n.x,  n.y,  n.z,  cn > 0 ? 1.0 / cn : 0.0};
+#pragma unroll
+        for (int q = 0; q < 19; ++q) W.geo[q] = gv[q];
+        if (!(cn > 0)) atomicMin(&red[1], (unsigned long long)s0);
       }
-      const int64_t i = s0 + tid;
-      const int row = sm.rrow[q] + (tid - sm.rs[q]);
+    }
+    __syncwarp();
+    double d00 = 0, d01 = 0, d10 = 0, d11 = 0, d20 = 0, d21 = 0, d30 = 0, d31 = 0;
+    for (int64_t base = s0; base < s1; base += 32) {
+      const int64_t i = base + lane;
+      const int rows = s1 - base < 32 ? (int)(s1 - base) : 32;
+      double ub[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, w[3] = {0, 0, 0};
       double h = 0, f = 0, eb = 0;
-      d3 rr = mk3(0, 0, 0);
-      int nm, mid[3];
-      double w[3];
-      load_master(S, i, nm, w, mid);
-      const double b0 = S.beta_s[3 * i], b1 = S.beta_s[3 * i + 1], b2 = S.beta_s[3 * i + 2];
-      const double icn = sm.ricn[q];
-      if (icn > 0) {
-        const d3 a0 = mk3(sm.ra[q][0], sm.ra[q][1], sm.ra[q][2]);
-        const d3 a1 = mk3(sm.ra[q][3], sm.ra[q][4], sm.ra[q][5]);
-        const d3 a2 = mk3(sm.ra[q][6], sm.ra[q][7], sm.ra[q][8]);
-        const d3 n = mk3(sm.rn[q][0], sm.rn[q][1], sm.rn[q][2]);
-        const d3 xs = (b0 * a0 + b1 * a1) + b2 * a2;
-        d3 xm = mk3(0, 0, 0);
-        for (int j = 0; j < nm; ++j) xm = xm + w[j] * ld3(x, mid[j]);
-        const d3 d = xm - xs;
-        const double g = dot(n, d);
-        if (!(g > 0)) {
-          atomicMin(&red[0], (unsigned long long)i);
-        } else {
-          rr = icn * (d - g * n);
-          const double eps = S.eps[i];
-          if (g < eps) {  // barrier.hpp:55-66 with one reciprocal
-            const double dd = g - eps, ig = 1.0 / g;
-            const double ln = log(g / eps);
-            const double cf = S.coef[i];
-            const double q2 = dd * ig;
-            eb = cf * (-dd * dd * ln);
-            f = cf * (-2.0 * dd * ln - dd * q2);
-            h = cf * dmax(-2.0 * ln - 4.0 * q2 + q2 * q2, 0.0);
+      uint32_t li = 0xffffffffu;
+      int nm = 0;
+      if (lane < rows) {
+        const double icn = W.geo[18];
+        int mid[3];
+        load_master(S, i, nm, w, mid);
+        ub[0] = S.beta_s[3 * i];
+        ub[1] = S.beta_s[3 * i + 1];
+        ub[2] = S.beta_s[3 * i + 2];
+        li = li4[i];
+        const double eps = S.eps[i], cf = S.coef[i];
+        if (icn > 0) {
+          const d3 a0 = mk3(W.geo[0], W.geo[1], W.geo[2]), a1 = mk3(W.geo[3], W.geo[4], W.geo[5]);
+          const d3 a2 = mk3(W.geo[6], W.geo[7], W.geo[8]), n = mk3(W.geo[15], W.geo[16], W.geo[17]);
+          const d3 xs = (ub[0] * a0 + ub[1] * a1) + ub[2] * a2;
+          d3 xm = mk3(0, 0, 0);
+          for (int j = 0; j < nm; ++j) xm = xm + w[j] * ld3(x, mid[j]);
+          const d3 d = xm - xs;
+          const double gap = dot(n, d);
+          if (!(gap > 0)) {
+            atomicMin(&red[0], (unsigned long long)i);
+          } else {
+            const d3 rv = icn * (d - gap * n);
+            rr[0] = rv.x;
+            rr[1] = rv.y;
+            rr[2] = rv.z;
+            if (gap < eps) {  // barrier.hpp:55-66 with one reciprocal
+              const double dd = gap - eps, ig = 1.0 / gap;
+              const double ln = log(gap / eps);
+              const double q2 = dd * ig;
+              eb = cf * (-dd * dd * ln);
+              f = cf * (-2.0 * dd * ln - dd * q2);
+              h = cf * dmax(-2.0 * ln - 4.0 * q2 + q2 * q2, 0.0);
+            }
           }
         }
       }
-      const int M = sm.rM[q];
-      const double bs[3] = {b0, b1, b2}, rs3[3] = {rr.x, rr.y, rr.z};
+      const int prow = (rows + 3) & ~3;  // rows incl. zero padding
+      for (int half = 0; half * kStage < prow; ++half) {
+        const int row = lane - half * kStage;
+        __syncwarp();
+        if (row >= 0 && row < kStage) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        sm.u[c][row] = bs[c];
-        sm.v[c][row] = h * bs[c];
-        sm.u[3 + c][row] = rs3[c];
-        sm.v[3 + c][row] = h * rs3[c];
-      }
+          for (int c = 0; c < 3; ++c) {
+            W.u[c][row] = ub[c];
+            W.v[c][row] = h * ub[c];
+            W.u[3 + c][row] = rr[c];
+            W.v[3 + c][row] = h * rr[c];
+          }
 #pragma unroll
-      for (int c = 6; c < kUC; ++c) sm.u[c][row] = sm.v[c][row] = 0.0;
-      sm.u[6 + M][row] = 1.0;
-      sm.v[6 + M][row] = f;
-      sm.v[7 + M][row] = eb;
-      const uint32_t li = li4[i];
-      for (int j = 0; j < nm; ++j) {
-        const int m = (li >> (8 * j)) & 0xff;
-        sm.u[6 + m][row] = w[j];
-        sm.v[6 + m][row] = h * w[j];
+          for (int c = 6; c < kUC; ++c) W.u[c][row] = W.v[c][row] = 0.0;
+          if (lane < rows) W.u[6 + M][row] = 1.0;
+          W.v[6 + M][row] = f;
+          W.v[7 + M][row] = eb;
+          for (int j = 0; j < nm; ++j) {
+            const int m = (li >> (8 * j)) & 0xff;
+            W.u[6 + m][row] = w[j];
+            W.v[6 + m][row] = h * w[j];
+          }
+        }
+        __syncwarp();
+        const int kk = min(kStage, prow - half * kStage);
+        for (int k = t4; k < kk; k += 4) {
+          const double ua = W.u[g][k], ub8 = W.u[8 + g][k];
+          const double va = W.v[g][k], vb = W.v[8 + g][k];
+          dmma(d00, d01, ua, va);
+          dmma(d10, d11, ua, vb);
+          dmma(d20, d21, ub8, va);
+          dmma(d30, d31, ub8, vb);
+        }
       }
     }
-    __syncthreads();
-    // Phase B: one warp per run, C = U'^T V on the tensor cores
-    for (int q = wid; q < nr; q += kTileWarps) {
-      const int r = r0 + q;
-      const int M = sm.rM[q];
-      double* P = partial + pbase[r];
-      const int ra0 = sm.rrow[q], ra1 = sm.rrow[q + 1];
-      const int g = lane >> 2, t4 = lane & 3;
-      const int colF = 6 + M, colE = 7 + M;
-      double d00 = 0, d01 = 0, d10 = 0, d11 = 0, d20 = 0, d21 = 0, d30 = 0, d31 = 0;
-      for (int k = ra0 + t4; k < ra1; k += 4) {
-        const double a0 = sm.u[g][k], a1 = sm.u[8 + g][k];
-        const double b0 = sm.v[g][k], b1 = sm.v[8 + g][k];
-        dmma(d00, d01, a0, b0);
-        dmma(d10, d11, a0, b1);
-        dmma(d20, d21, a1, b0);
-        dmma(d30, d31, a1, b1);
-      }
-      C[g][2 * t4] = d00;
-      C[g][2 * t4 + 1] = d01;
-      C[g][8 + 2 * t4] = d10;
-      C[g][9 + 2 * t4] = d11;
-      C[8 + g][2 * t4] = d20;
-      C[8 + g][2 * t4 + 1] = d21;
-      C[8 + g][8 + 2 * t4] = d30;
-      C[8 + g][9 + 2 * t4] = d31;
-      __syncwarp();
-      const double nv[3] = {sm.rn[q][0], sm.rn[q][1], sm.rn[q][2]};
-      const d3 n = mk3(nv[0], nv[1], nv[2]);
-      const d3 e1 = mk3(sm.re[q][0], sm.re[q][1], sm.re[q][2]);
-      const d3 e2 = mk3(sm.re[q][3], sm.re[q][4], sm.re[q][5]);
-      // shared pieces of the SS blocks: T_j(Mbr_i) and Mrr A_j^T
-      if (Hess && lane < 27) {
-        const int i = lane / 9, j = (lane / 3) % 3, c = lane % 3;
-        tm[lane] = comp(Tmap(j, mk3(C[i][3], C[i][4], C[i][5]), e1, e2), c);
-        // bm[j][p][c] = sum_q Mrr[p][q] A_j[c][q]   (here lane = j*9 + p*3 + c)
-        const int jj = lane / 9, p = (lane / 3) % 3, cc = lane % 3;
-        const d3 rc = Trow(jj, cc, e1, e2);
-        bm[lane] = p == 0 ? C[3][3] * rc.x + C[3][4] * rc.y + C[3][5] * rc.z
-                          : (p == 1 ? C[3][4] * rc.x + C[4][4] * rc.y + C[4][5] * rc.z
+    __syncwarp();
+    const d3 e1 = mk3(W.geo[9], W.geo[10], W.geo[11]), e2 = mk3(W.geo[12], W.geo[13], W.geo[14]);
+    const d3 n = mk3(W.geo[15], W.geo[16], W.geo[17]);
+    double (*C)[kUC + 1] = W.C;
+    C[g][2 * t4] = d00;
+    C[g][2 * t4 + 1] = d01;
+    C[g][8 + 2 * t4] = d10;
+    C[g][9 + 2 * t4] = d11;
+    C[8 + g][2 * t4] = d20;
+    C[8 + g][2 * t4 + 1] = d21;
+    C[8 + g][8 + 2 * t4] = d30;
+    C[8 + g][9 + 2 * t4] = d31;
+    __syncwarp();
+    double* P = partial + pb;
+    const int colF = 6 + M, colE = 7 + M;
+    // shared pieces of the SS blocks: T_j(Mbr_i) and Mrr A_j^T
+    if (Hess && lane < 27) {
+      const int i = lane / 9, j = (lane / 3) % 3, c = lane % 3;
+      W.tm[lane] = comp(Tmap(j, mk3(C[i][3], C[i][4], C[i][5]), e1, e2), c);
+      // bm[j][p][c] = sum_q Mrr[p][q] A_j[c][q]   (here lane = j*9 + p*3 + c)
+      const d3 rc = Trow(i, c, e1, e2);
+      W.bm[lane] = j == 0 ? C[3][3] * rc.x + C[3][4] * rc.y + C[3][5] * rc.z
+                          : (j == 1 ? C[3][4] * rc.x + C[4][4] * rc.y + C[4][5] * rc.z
                                     : C[3][5] * rc.x + C[4][5] * rc.y + C[5][5] * rc.z);
-      }
-      __syncwarp();
-      if (lane < 4) {
-        P[lane] = lane == 0 ? C[6 + M][colE] : nv[lane - 1];
-      } else if (lane < 13) {  // slave gradients g_i = -Fb_i n + T_i(Fr)
-        const int i = (lane - 4) / 3, a = (lane - 4) % 3;
-        const d3 gv = (-C[i][colF]) * n + Tmap(i, mk3(C[3][colF], C[4][colF], C[5][colF]), e1, e2);
-        P[lane] = comp(gv, a);
-      }
-      if (Hess) {
-        for (int o = lane; o < 45; o += 32) {  // SS entries
-          const int blk = c_ss_entry[o][0], a = c_ss_entry[o][1], c = c_ss_entry[o][2];
-          const int i = c_ss_blk[blk][0], j = c_ss_blk[blk][1];
+    }
+    __syncwarp();
+    if (lane < 4) {
+      P[lane] = lane == 0 ? C[6 + M][colE] : comp(n, lane - 1);
+    } else if (lane < 13) {  // slave gradients g_i = -Fb_i n + T_i(Fr)
+      const int i = (lane - 4) / 3, a = (lane - 4) % 3;
+      const d3 gv = (-C[i][colF]) * n + Tmap(i, mk3(C[3][colF], C[4][colF], C[5][colF]), e1, e2);
+      P[lane] = comp(gv, a);
+    }
+    if (Hess) {
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {  // SS entries
+        if (lane + 32 * h2 < 45) {
+          const int pk = ss_pk[h2];
+          const int blk = pk & 7, a = (pk >> 3) & 3, c = (pk >> 5) & 3, i = (pk >> 7) & 3, j = (pk >> 9) & 3;
           const d3 ra = Trow(i, a, e1, e2);
-          const double* B = bm + 9 * j;
+          const double* B = W.bm + 9 * j;
           const double qv = ra.x * B[c] + ra.y * B[3 + c] + ra.z * B[6 + c];
-          const double na = nv[a], nc = nv[c];
+          const double na = comp(n, a), nc = comp(n, c);
           const double mbb = i <= j ? C[i][j] : C[j][i];
-          const double v = ((mbb * (na * nc) - na * tm[9 * i + 3 * j + c]) - tm[9 * j + 3 * i + a] * nc) + qv;
+          const double v = ((mbb * (na * nc) - na * W.tm[9 * i + 3 * j + c]) - W.tm[9 * j + 3 * i + a] * nc) + qv;
           P[kSSBase + 9 * blk + 3 * a + c] = v;
           if (i == j && a != c) P[kSSBase + 9 * blk + 3 * c + a] = v;
         }
-        for (int t = lane; t < M * (M + 1) / 2; t += 32) {  // master pairs, dense upper triangle
-          int m = 0, l = t;
-          while (l >= M - m) {
-            l -= M - m;
-            ++m;
-          }
-          P[pair_base(M) + t] = C[6 + m][6 + m + l];
-        }
       }
-      if (lane < M) P[kHdr + lane] = (double)lm_ids[lm_off[r] + lane];  // header: local master ids
-      else if (lane >= 28 && lane < 31) P[kSlv + lane - 28] = (double)run_slave[3 * r + lane - 28];
-      else if (lane == 31) P[kMcnt] = (double)M;
-      for (int t = lane; t < (Hess ? 4 * M : M); t += 32) {  // s_m, a_{m,i} = -Hwb_{m,i} n + T_i(Hwr_m)
-        const int m = Hess ? t >> 2 : t, w = Hess ? t & 3 : 0;
-        double* out = P + m_base(M) + 10 * m;
-        if (w == 0) {
-          out[0] = C[6 + m][colF];
-        } else {
-          const int i = w - 1;
-          const d3 av = (-C[6 + m][i]) * n + Tmap(i, mk3(C[6 + m][3], C[6 + m][4], C[6 + m][5]), e1, e2);
-          out[1 + 3 * i] = av.x;
-          out[2 + 3 * i] = av.y;
-          out[3 + 3 * i] = av.z;
+      for (int t = lane; t < M * (M + 1) / 2; t += 32) {  // master pairs, dense upper triangle
+        int m = 0, l = t;
+        while (l >= M - m) {
+          l -= M - m;
+          ++m;
         }
+        P[pair_base(M) + t] = C[6 + m][6 + m + l];
       }
-      __syncwarp();
     }
-    __syncthreads();
+    if (lane < M) P[kHdr + lane] = (double)my_lm;  // header: local master ids
+    else if (lane == 28) P[kSlv] = (double)sid0;
+    else if (lane == 29) P[kSlv + 1] = (double)sid1;
+    else if (lane == 30) P[kSlv + 2] = (double)sid2;
+    else if (lane == 31) P[kMcnt] = (double)M;
+    for (int t = lane; t < (Hess ? 4 * M : M); t += 32) {  // s_m, a_{m,i} = -Hwb_{m,i} n + T_i(Hwr_m)
+      const int m = Hess ? t >> 2 : t, wq = Hess ? t & 3 : 0;
+      double* out = P + m_base(M) + 10 * m;
+      if (wq == 0) {
+        out[0] = C[6 + m][colF];
+      } else {
+        const int i = wq - 1;
+        const d3 av = (-C[6 + m][i]) * n + Tmap(i, mk3(C[6 + m][3], C[6 + m][4], C[6 + m][5]), e1, e2);
+        out[1 + 3 * i] = av.x;
+        out[2 + 3 * i] = av.y;
+        out[3 + 3 * i] = av.z;
+      }
+    }
+    __syncwarp();
   }
 }
 

@@ -24,25 +24,30 @@ void init_kernels() {
   static bool done = false;
   if (done) return;
   init_ss_table();
-  GMCP_CUDA(cudaFuncSetAttribute(k_tile_partials<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(TileSmem)));
-  GMCP_CUDA(cudaFuncSetAttribute(k_tile_partials<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(TileSmem)));
   done = true;
 }
 
 void launch_k7(Ctx& c, int mode) {
   AssemblyPlan& P = c.plan;
   const DevSamples S = c.samples();
-  const int tb = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, 148 * 64));
+  static int resident = 0;  // persistent grid: resident blocks on all SMs
+  if (!resident) {
+    int occ = 0, dev = 0, sms = 148;
+    GMCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_run_partials<true>, 32 * kRunWarps, 0));
+    GMCP_CUDA(cudaGetDevice(&dev));
+    GMCP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    resident = std::max(1, occ) * sms;
+  }
+  const int64_t blocks = (P.n_runs + kRunWarps - 1) / kRunWarps;
+  const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, resident));
   if (mode == 1)
-    k_tile_partials<true><<<tb, kTileSamples, sizeof(TileSmem), c.stream>>>(
-        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lm_ids.p, P.li4.p,
-        P.run_row.p, P.pbase.p, P.partial.p, c.red_u.p);
+    k_run_partials<true><<<gb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
+                                                              P.lm_off.p, P.lm_ids.p, P.li4.p, P.pbase.p,
+                                                              P.partial.p, c.red_u.p);
   else
-    k_tile_partials<false><<<tb, kTileSamples, sizeof(TileSmem), c.stream>>>(
-        S, c.X(), P.n_tiles, P.tile_run.p, P.run_off.p, P.run_slave.p, P.lm_off.p, P.lm_ids.p, P.li4.p,
-        P.run_row.p, P.pbase.p, P.partial.p, c.red_u.p);
+    k_run_partials<false><<<gb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
+                                                               P.lm_off.p, P.lm_ids.p, P.li4.p, P.pbase.p,
+                                                               P.partial.p, c.red_u.p);
   ++c.launches;
 }
 
@@ -96,8 +101,8 @@ void derive_sample_fields(Ctx& c) {
 }
 
 // Host-side assembly plan from the device sample set (per rebuild): runs
-// (consecutive samples sharing a slave triangle, split at the tile size),
-// tiles, local master tables, incidence lists, BCSR pattern, row entries.
+// (consecutive samples sharing a slave triangle, split at kRunSamples samples
+// or kRunMasters local masters), local master tables, incidence lists, BCSR pattern, row entries.
 void build_assembly_plan(Ctx& c) {
   AssemblyPlan& P = c.plan;
   const int64_t n = c.ns;
@@ -115,7 +120,7 @@ void build_assembly_plan(Ctx& c) {
       const int32_t m = ms[3 * i + j];
       if (m >= 0 && std::find(run_masters.begin(), run_masters.end(), m) == run_masters.end()) ++add;
     }
-    if (new_tri || i - run_off.back() >= kTileSamples || (int)run_masters.size() + add > kRunMasters) {
+    if (new_tri || i - run_off.back() >= kRunSamples || (int)run_masters.size() + add > kRunMasters) {
       if (i > 0) run_off.push_back(i);
       run_slave.insert(run_slave.end(), {sl[3 * i], sl[3 * i + 1], sl[3 * i + 2]});
       run_masters.clear();
@@ -128,23 +133,6 @@ void build_assembly_plan(Ctx& c) {
   }
   if (n > 0) run_off.push_back(n);
   const int64_t R = (int64_t)run_slave.size() / 3;
-  // tiles: greedy over runs
-  std::vector<int32_t> tile_run{0};
-  {
-    int64_t cur = 0;
-    int runs = 0;
-    for (int64_t r = 0; r < R; ++r) {
-      const int64_t len = run_off[r + 1] - run_off[r];
-      if (runs > 0 && (cur + len > kTileSamples || runs >= kTileRuns)) {
-        tile_run.push_back((int32_t)r);
-        cur = 0;
-        runs = 0;
-      }
-      cur += len;
-      ++runs;
-    }
-    if (R > 0) tile_run.push_back((int32_t)R);
-  }
   std::vector<int32_t> lm_off{0}, lm_ids, lp_off{0}, lp;
   std::vector<uint32_t> li4(n > 0 ? n : 1, 0xffffffffu);  // per sample local master indices (u8 x 3)
   std::vector<int64_t> pbase(R);
@@ -180,15 +168,6 @@ void build_assembly_plan(Ctx& c) {
     lp_off.push_back((int32_t)lp.size());
     pbase[r] = plen;
     plen += partial_size((int)loc.size());
-  }
-  // K7 row offsets of the runs within their tile (each run padded to 4 rows)
-  std::vector<int32_t> run_row(R > 0 ? R : 1, 0);
-  for (size_t t = 0; t + 1 < tile_run.size(); ++t) {
-    int32_t acc = 0;
-    for (int32_t r = tile_run[t]; r < tile_run[t + 1]; ++r) {
-      run_row[r] = acc;
-      acc += ((int32_t)(run_off[r + 1] - run_off[r]) + 3) & ~3;
-    }
   }
   // BCSR pattern + row entries over all N vertex rows
   const int64_t N = c.n_vertices();
@@ -228,14 +207,11 @@ void build_assembly_plan(Ctx& c) {
   P.n_runs = R;
   P.run_off.upload(run_off, s);
   P.run_slave.upload(run_slave, s);
-  P.n_tiles = (int64_t)tile_run.size() - 1;
-  P.tile_run.upload(tile_run, s);
   P.lm_off.upload(lm_off, s);
   P.lm_ids.upload(lm_ids, s);
   P.lp_off.upload(lp_off, s);
   P.lp.upload(lp, s);
   P.li4.upload(li4, s);
-  P.run_row.upload(run_row, s);
   P.pbase.upload(pbase, s);
   P.partial_len = plen;
   P.partial.resize(std::max<int64_t>(plen, 1));

@@ -25,11 +25,7 @@ struct AssemblyPlan {
   DBuf<int32_t> lp_off;      // [R+1] local master pair table offsets
   DBuf<int32_t> lp;          // packed (a << 16 | b), local indices, a <= b
   DBuf<int64_t> pbase;       // [R] partial base offset (doubles)
-  // K7 tiles: consecutive runs with <= kTileSamples samples in total
-  int64_t n_tiles = 0;
-  DBuf<int32_t> tile_run;    // [T+1] first run of each tile
   DBuf<uint32_t> li4;        // per sample: local master index of each slot (u8 x 3, 0xff = none)
-  DBuf<int32_t> run_row;     // per run: first K7 row within its tile (runs padded to 4 rows)
   int64_t partial_len = 0;
   DBuf<double> partial;
   // BCSR pattern over all N vertex rows

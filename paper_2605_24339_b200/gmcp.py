@@ -30,7 +30,7 @@ import numpy as np
 from . import scenes as _scenes
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgmcp_b200.so")
+LIB_PATH = os.environ.get("GMCP_B200_LIB") or os.path.join(HERE, "libgmcp_b200.so")  # env: dev variants
 
 GMCP_OK, GMCP_ERR_INFEASIBLE, GMCP_ERR_DEGENERATE, GMCP_ERR_CONFIG, GMCP_ERR_SOLVER, GMCP_ERR_CUDA, \
     GMCP_ERR_ARG, GMCP_ERR_PARSE = range(8)
