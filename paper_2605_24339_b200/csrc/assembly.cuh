@@ -6,10 +6,10 @@
 //                      into a per-warp staging tile, the run's moments are one
 //                      Gram product on the FP64 tensor cores, and the warp
 //                      finalizes the run's blocks into its partial.
-//  K8 k_row_gather     16 lanes per vertex row: sums the finalized blocks of
-//                      the runs touching the vertex (ascending run order) in a
-//                      shared-memory row accumulator, then writes the BCSR row
-//                      and the gradient once.
+//  K8 k_gather         one thread per BCSR block: sums the block's
+//                      contributions from the run partials in ascending run
+//                      order (listed by the plan); one thread per vertex row
+//                      does the same for the gradient.
 //
 // Moment form. Within a run (one slave triangle) n, e1, e2 are shared and the
 // slave gap gradients are dg_i = -b_i n + T_i(r) with T_0(v) = v x (e2-e1),
@@ -381,140 +381,106 @@ __global__ void __launch_bounds__(kRedThreads) k_run_energy(int64_t n_runs, cons
 }
 
 // ---------------------------------------------------------------------------
-// K8
+// K8: gather. The plan lists, for every BCSR block, its contributions
+// (run partial, row role, block index) in ascending run order; one thread per
+// block sums them in that order (bitwise deterministic, no atomics), and one
+// thread per vertex row sums its gradient the same way.
+//   contribution code = (pbase << 12) | (M << 8) | (role << 4) | b
+//   row entry code    = (pbase << 12) | (M << 8) | role
+// role < 3: slave vertex i of the run, else local master role - 3; b indexes
+// the run's columns the same way.
 
-constexpr int kRowCols = 40;  // shared-memory row accumulator capacity (blocks)
-constexpr int kGatherWarps = 4;
-constexpr int kRowGroup = 16;  // lanes per row (16 beats 8 and 32 on C3)
-
-struct RowSmem {
-  int cols[kRowCols];
-  double acc[kRowCols * 9];
-};
-
-__device__ __forceinline__ int find_col(const int32_t* cols, int lo, int hi, int col) {
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (cols[mid] < col) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// Contribution block of element b of a row entry (run partial P, role); returns
-// its column, or -1 when the block is identically zero (absent master pair).
-__device__ __forceinline__ int entry_block(int role, int b, const double* __restrict__ P, int M, double* blk) {
-  const double nn[3] = {P[1], P[2], P[3]};
-  if (role < 3) {
-    const int i = role;
-    if (b < 3) {
-      const int j = b;
-      const int lo = min(i, j), hi = max(i, j);
-      const int bid = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
-      const double* Sb = P + kSSBase + 9 * bid;
-      if (i <= j) {
+// Block (role, b) of a run partial P.
+__device__ __forceinline__ void contrib_block(int role, int b, const double* __restrict__ P, int M, double* blk) {
+  if (role < 3 && b < 3) {  // SS: upper blocks stored, lower = transpose
+    const int lo = min(role, b), hi = max(role, b);
+    const int bid = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+    const double* Sb = P + kSSBase + 9 * bid;
+    if (role <= b) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) blk[q] = Sb[q];
-      } else {
+      for (int q = 0; q < 9; ++q) blk[q] = Sb[q];
+    } else {
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
+      for (int a = 0; a < 3; ++a)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) blk[3 * a + c] = Sb[3 * c + a];
-      }
-      return (int)P[kSlv + j];
+        for (int c = 0; c < 3; ++c) blk[3 * a + c] = Sb[3 * c + a];
     }
-    const int k = b - 3;
-    const double* A = P + m_base(M) + 10 * k + 1 + 3 * i;
+    return;
+  }
+  const double nn[3] = {P[1], P[2], P[3]};
+  if (role < 3) {  // SM(i, m) = a_{m,i} n^T
+    const double* A = P + m_base(M) + 10 * (b - 3) + 1 + 3 * role;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int c = 0; c < 3; ++c) blk[3 * a + c] = A[a] * nn[c];
-    return (int)P[kHdr + k];
+    return;
   }
   const int m = role - 3;
-  if (b < 3) {
+  if (b < 3) {  // MS(m, i) = n a_{m,i}^T
     const double* A = P + m_base(M) + 10 * m + 1 + 3 * b;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int c = 0; c < 3; ++c) blk[3 * a + c] = nn[a] * A[c];
-    return (int)P[kSlv + b];
+    return;
   }
-  const int l = b - 3;
+  const int l = b - 3;  // MM(m, l) = c_ml n n^T
   const double cv = P[pair_base(M) + (m <= l ? tri_index(m, l, M) : tri_index(l, m, M))];
-  if (cv == 0) return -1;  // nonzero only if some sample holds both m and l (a listed pair)
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int c = 0; c < 3; ++c) blk[3 * a + c] = cv * (nn[a] * nn[c]);
-  return (int)P[kHdr + l];
 }
 
+constexpr int kGatherThreads = 256;
+
+// Items [0, nnzb) are BCSR blocks (Hess only), then one item per vertex row.
 template <bool Hess>
-__global__ void __launch_bounds__(32 * kGatherWarps) k_row_gather(int32_t n_rows, const int32_t* __restrict__ rowptr,
-                                                                  const int32_t* __restrict__ cols,
-                                                                  double* __restrict__ vals,
-                                                                  const int32_t* __restrict__ ent_off,
-                                                                  const int64_t* __restrict__ ent,
-                                                                  const double* __restrict__ partial,
-                                                                  double* __restrict__ grad) {
-  // kRowGroup lanes per vertex row: a row entry has 3 + M <= 11 blocks
-  __shared__ RowSmem rsm[(32 / kRowGroup) * kGatherWarps];
-  const int lane = threadIdx.x & 31, hl = lane & (kRowGroup - 1);
-  const unsigned hmask = (kRowGroup == 32 ? 0xffffffffu : ((1u << kRowGroup) - 1u)) << (lane & ~(kRowGroup - 1));
-  RowSmem& R = rsm[threadIdx.x / kRowGroup];
-  const int64_t ngroups = (int64_t)gridDim.x * (32 / kRowGroup) * kGatherWarps;
-  for (int64_t v = blockIdx.x * (int64_t)((32 / kRowGroup) * kGatherWarps) + (threadIdx.x / kRowGroup); v < n_rows;
-       v += ngroups) {
-    const int e0 = ent_off[v], e1 = ent_off[v + 1];
-    const int c0 = Hess ? rowptr[v] : 0, c1 = Hess ? rowptr[v + 1] : 0;
-    const int nc = c1 - c0;
-    const bool in_smem = Hess && nc <= kRowCols;
-    if (Hess) {
-      if (in_smem) {
-        for (int q = hl; q < nc; q += kRowGroup) R.cols[q] = cols[c0 + q];
-        for (int q = hl; q < 9 * nc; q += kRowGroup) R.acc[q] = 0;
-      } else {
-        for (int q = hl; q < 9 * nc; q += kRowGroup) vals[9 * (int64_t)c0 + q] = 0;
-      }
-    }
-    d3 g = mk3(0, 0, 0);
-    __syncwarp(hmask);
-    int64_t en_next = e0 < e1 ? ent[e0] : 0;
-    for (int e = e0; e < e1; ++e) {
-      const int64_t en = en_next;
-      if (e + 1 < e1) en_next = ent[e + 1];  // prefetch the next entry
-      const double* P = partial + (en >> 8);
-      const int role = (int)(en & 0xff);
-      const int M = (int)P[kMcnt];
-      if (hl == 0) {
-        if (role < 3) {
-          g = g + mk3(P[4 + 3 * role], P[5 + 3 * role], P[6 + 3 * role]);
-        } else {
-          g = g + P[m_base(M) + 10 * (role - 3)] * mk3(P[1], P[2], P[3]);
-        }
-      }
-      if (Hess) {
-        const int nb = 3 + M;
-        for (int b = hl; b < nb; b += kRowGroup) {
-          double blk[9];
-          const int col = entry_block(role, b, P, M, blk);
-          if (col < 0) continue;
-          double* out = in_smem ? R.acc + 9 * find_col(R.cols, 0, nc, col)
-                                : vals + 9 * (int64_t)find_col(cols, c0, c1, col);
+__global__ void __launch_bounds__(kGatherThreads) k_gather(int64_t nnzb, int32_t n_rows,
+                                                           const int32_t* __restrict__ blk_off,
+                                                           const int64_t* __restrict__ contrib,
+                                                           double* __restrict__ vals,
+                                                           const int32_t* __restrict__ ent_off,
+                                                           const int64_t* __restrict__ ent,
+                                                           const double* __restrict__ partial,
+                                                           double* __restrict__ grad) {
+  const int64_t nb = Hess ? nnzb : 0;
+  const int64_t items = nb + n_rows;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < items; k += (int64_t)gridDim.x * blockDim.x) {
+    if (k < nb) {
+      double acc[9];
 #pragma unroll
-          for (int q = 0; q < 9; ++q) out[q] += blk[q];
-        }
+      for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+      const int c1 = blk_off[k + 1];
+      for (int c = blk_off[k]; c < c1; ++c) {
+        const int64_t code = contrib[c];
+        double blk[9];
+        contrib_block((int)((code >> 4) & 0xf), (int)(code & 0xf), partial + (code >> 12), (int)((code >> 8) & 0xf),
+                      blk);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q] += blk[q];
       }
-      __syncwarp(hmask);
-    }
-    if (in_smem)
-      for (int q = hl; q < 9 * nc; q += kRowGroup) vals[9 * (int64_t)c0 + q] = R.acc[q];
-    if (hl == 0) {
+      double* out = vals + 9 * k;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) out[q] = acc[q];
+    } else {
+      const int64_t v = k - nb;
+      d3 g = mk3(0, 0, 0);
+      const int e1 = ent_off[v + 1];
+      for (int e = ent_off[v]; e < e1; ++e) {
+        const int64_t en = ent[e];
+        const double* P = partial + (en >> 12);
+        const int role = (int)(en & 0xff), M = (int)((en >> 8) & 0xf);
+        if (role < 3)
+          g = g + mk3(P[4 + 3 * role], P[5 + 3 * role], P[6 + 3 * role]);
+        else
+          g = g + P[m_base(M) + 10 * (role - 3)] * mk3(P[1], P[2], P[3]);
+      }
       grad[3 * v] = g.x;
       grad[3 * v + 1] = g.y;
       grad[3 * v + 2] = g.z;
     }
-    __syncwarp(hmask);
   }
 }
 

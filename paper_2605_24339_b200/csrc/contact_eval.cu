@@ -53,14 +53,14 @@ void launch_k7(Ctx& c, int mode) {
 
 void launch_k8(Ctx& c, int mode) {
   AssemblyPlan& P = c.plan;
-  const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P.n_rows + (32 / kRowGroup) * kGatherWarps - 1) / ((32 / kRowGroup) * kGatherWarps),
-                                                             148 * 32));
+  const int64_t items = (mode == 1 ? P.nnzb : 0) + P.n_rows;
+  const int gb = grid_for(items, kGatherThreads);
   if (mode == 1)
-    k_row_gather<true><<<gb, 32 * kGatherWarps, 0, c.stream>>>(P.n_rows, P.rowptr.p, P.cols.p, P.vals.p,
-                                                                P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
+    k_gather<true><<<gb, kGatherThreads, 0, c.stream>>>(P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.vals.p,
+                                                        P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   else
-    k_row_gather<false><<<gb, 32 * kGatherWarps, 0, c.stream>>>(P.n_rows, P.rowptr.p, P.cols.p, P.vals.p,
-                                                                 P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
+    k_gather<false><<<gb, kGatherThreads, 0, c.stream>>>(P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.vals.p,
+                                                         P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   ++c.launches;
 }
 
@@ -169,40 +169,55 @@ void build_assembly_plan(Ctx& c) {
     pbase[r] = plen;
     plen += partial_size((int)loc.size());
   }
-  // BCSR pattern + row entries over all N vertex rows
+  // BCSR pattern, per-block contribution lists and row entries over all N
+  // vertex rows. Runs are visited in ascending order and the per-row sort is
+  // stable, so every block lists its contributions in ascending run order.
   const int64_t N = c.n_vertices();
-  std::vector<std::vector<int32_t>> rc(N);
+  struct Contrib {
+    int32_t col;
+    int64_t code;
+  };
+  std::vector<std::vector<Contrib>> rc(N);
   std::vector<std::vector<int64_t>> rent(N);
   for (int64_t r = 0; r < R; ++r) {
     const int32_t* s = &run_slave[3 * r];
     const int32_t* L = lm_ids.data() + lm_off[r];
     const int M = lm_off[r + 1] - lm_off[r];
+    const int64_t head = (pbase[r] << 12) | ((int64_t)M << 8);
+    auto col_of = [&](int b) { return b < 3 ? s[b] : L[b - 3]; };
     for (int i = 0; i < 3; ++i) {
-      rent[s[i]].push_back((pbase[r] << 8) | i);
-      for (int j = 0; j < 3; ++j) rc[s[i]].push_back(s[j]);
-      for (int k = 0; k < M; ++k) rc[s[i]].push_back(L[k]);
+      rent[s[i]].push_back(head | i);
+      for (int b = 0; b < 3 + M; ++b) rc[s[i]].push_back({col_of(b), head | (i << 4) | b});
     }
     for (int k = 0; k < M; ++k) {
-      rent[L[k]].push_back((pbase[r] << 8) | (3 + k));
-      for (int j = 0; j < 3; ++j) rc[L[k]].push_back(s[j]);
+      rent[L[k]].push_back(head | (3 + k));
+      for (int b = 0; b < 3; ++b) rc[L[k]].push_back({s[b], head | ((3 + k) << 4) | b});
     }
-    for (int p = lp_off[r]; p < lp_off[r + 1]; ++p) {
+    for (int p = lp_off[r]; p < lp_off[r + 1]; ++p) {  // listed master pairs only
       const int a = lp[p] >> 16, b = lp[p] & 0xffff;
-      rc[L[a]].push_back(L[b]);
-      rc[L[b]].push_back(L[a]);
+      rc[L[a]].push_back({L[b], head | ((3 + a) << 4) | (3 + b)});
+      if (a != b) rc[L[b]].push_back({L[a], head | ((3 + b) << 4) | (3 + a)});
     }
   }
-  std::vector<int32_t> rowptr(N + 1, 0), cols, eoff(N + 1, 0);
-  std::vector<int64_t> ents;
+  std::vector<int32_t> rowptr(N + 1, 0), cols, eoff(N + 1, 0), boff{0};
+  std::vector<int64_t> ents, contrib;
   for (int64_t v = 0; v < N; ++v) {
     auto& cv = rc[v];
-    std::sort(cv.begin(), cv.end());
-    cv.erase(std::unique(cv.begin(), cv.end()), cv.end());
-    cols.insert(cols.end(), cv.begin(), cv.end());
+    std::stable_sort(cv.begin(), cv.end(), [](const Contrib& a, const Contrib& b) { return a.col < b.col; });
+    for (size_t q = 0; q < cv.size(); ++q) {
+      if (q == 0 || cv[q].col != cv[q - 1].col) {
+        if (q > 0) boff.push_back((int32_t)contrib.size());
+        cols.push_back(cv[q].col);
+      }
+      contrib.push_back(cv[q].code);
+    }
+    if (!cv.empty()) boff.push_back((int32_t)contrib.size());
     rowptr[v + 1] = (int32_t)cols.size();
     ents.insert(ents.end(), rent[v].begin(), rent[v].end());
     eoff[v + 1] = (int32_t)ents.size();
+    std::vector<Contrib>().swap(cv);
   }
+  if (contrib.size() >= (size_t)INT32_MAX) throw StatusError(GMCP_ERR_CONFIG, "contact Hessian too large");
   cudaStream_t s = c.stream;
   P.n_runs = R;
   P.run_off.upload(run_off, s);
@@ -222,6 +237,8 @@ void build_assembly_plan(Ctx& c) {
   P.vals.resize(std::max<int64_t>(9 * P.nnzb, 1));
   P.row_ent_off.upload(eoff, s);
   P.row_ent.upload(ents, s);
+  P.blk_off.upload(boff, s);
+  P.contrib.upload(contrib, s);
   c.sync();
   P.valid = true;
 }

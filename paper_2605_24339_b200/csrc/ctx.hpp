@@ -13,9 +13,9 @@ struct DevSurface {
 
 // Contact-Hessian assembly plan, rebuilt whenever the sample set changes.
 // Level 1 (K7, one warp per slave run) reduces each run of samples sharing a
-// slave triangle into a compact partial; level 2 (K8, one warp per vertex
-// row) gathers the partials of the runs touching that vertex into its BCSR
-// row and gradient. Both levels sum in a fixed order: bitwise deterministic.
+// slave triangle into a compact partial; level 2 (K8, one thread per BCSR
+// block / vertex row) gathers the partials' contributions to that block or
+// gradient row. Both levels sum in a fixed order: bitwise deterministic.
 struct AssemblyPlan {
   int64_t n_runs = 0;
   DBuf<int64_t> run_off;     // [R+1] sample range of each run
@@ -35,7 +35,9 @@ struct AssemblyPlan {
   DBuf<int32_t> cols;        // [nnzb]
   DBuf<double> vals;         // [nnzb][9]
   DBuf<int32_t> row_ent_off; // [N+1]
-  DBuf<int64_t> row_ent;     // (run << 20) | role ; role < 3 slave i, else 3 + local master
+  DBuf<int32_t> blk_off;     // [nnzb+1] contribution list of each BCSR block
+  DBuf<int64_t> contrib;     // (pbase << 12) | (M << 8) | (role << 4) | b, ascending run per block
+  DBuf<int64_t> row_ent;     // (pbase << 12) | (M << 8) | role ; role < 3 slave i, else 3 + local master
   bool valid = false;
 };
 
