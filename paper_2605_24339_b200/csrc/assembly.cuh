@@ -114,16 +114,13 @@ struct RunSmem {
   };
   double tm[27];  // T_j(Mbr_i): [i][j][comp]
   double bm[27];  // Mrr A_j^T: [j][p][c]
+  double A[27];   // A_i with T_i(v) = A_i v: [i][row][col]
   double geo[19];  // a0 a1 a2 | e1 e2 | n | 1/|c|
 };
 
 __constant__ unsigned char c_ss_entry[45][3];  // (block, a, c) of the 45 unique SS entries
 __constant__ unsigned char c_ss_blk[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
 
-// T_i(v) (see header comment)
-__device__ __forceinline__ d3 Tmap(int i, d3 v, d3 e1, d3 e2) {
-  return i == 0 ? cross(v, e2 - e1) : (i == 1 ? cross(e2, v) : cross(v, e1));
-}
 // row a of the matrix A_i with T_i(v) = A_i v
 __device__ __forceinline__ d3 Trow(int i, int a, d3 e1, d3 e2) {
   d3 u;
@@ -155,6 +152,13 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     const uint32_t* __restrict__ li4, const int64_t* __restrict__ pbase, double* __restrict__ partial,
     unsigned long long* __restrict__ red) {
   __shared__ RunSmem wsm[kRunWarps];
+  __shared__ unsigned char pair_tab[kRunMasters + 1][kRunMasters * (kRunMasters + 1) / 2];  // t -> m | l << 4
+  for (int q = threadIdx.x; q < (kRunMasters + 1) * kRunMasters; q += blockDim.x) {
+    const int Mq = q / kRunMasters, m = q % kRunMasters;
+    if (m < Mq)
+      for (int l = m; l < Mq; ++l) pair_tab[Mq][tri_index(m, l, Mq)] = (unsigned char)(m | (l << 4));
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   RunSmem& W = wsm[threadIdx.x >> 5];
   const int g = lane >> 2, t4 = lane & 3;
@@ -207,6 +211,11 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
 #pragma unroll
         for (int q = 0; q < 19; ++q) W.geo[q] = gv[q];
         if (!(cn > 0)) atomicMin(&red[1], (unsigned long long)s0);
+      }
+      if (lane < 27) {  // A_i = s_i [u_i]_x: T_0(v) = v x (e2-e1), T_1(v) = e2 x v, T_2(v) = v x e1
+        const int ti = lane / 9, ta = (lane / 3) % 3, tc = lane % 3;
+        const d3 tr = Trow(ti, ta, e1, e2);
+        W.A[lane] = comp(tr, tc);
       }
     }
     __syncwarp();
@@ -289,8 +298,6 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
       }
     }
     __syncwarp();
-    const d3 e1 = mk3(W.geo[9], W.geo[10], W.geo[11]), e2 = mk3(W.geo[12], W.geo[13], W.geo[14]);
-    const d3 n = mk3(W.geo[15], W.geo[16], W.geo[17]);
     double (*C)[kUC + 1] = W.C;
     C[g][2 * t4] = d00;
     C[g][2 * t4 + 1] = d01;
@@ -303,23 +310,28 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     __syncwarp();
     double* P = partial + pb;
     const int colF = 6 + M, colE = 7 + M;
-    // shared pieces of the SS blocks: T_j(Mbr_i) and Mrr A_j^T
+
+    const double* A = W.A;
+    const double* nn = W.geo + 15;
+    // shared pieces of the SS blocks: T_j(Mbr_i) and Mrr A_j^T (upper entries of C)
     if (Hess && lane < 27) {
       const int i = lane / 9, j = (lane / 3) % 3, c = lane % 3;
-      W.tm[lane] = comp(Tmap(j, mk3(C[i][3], C[i][4], C[i][5]), e1, e2), c);
-      // bm[j][p][c] = sum_q Mrr[p][q] A_j[c][q]   (here lane = j*9 + p*3 + c)
-      const d3 rc = Trow(i, c, e1, e2);
-      W.bm[lane] = j == 0 ? C[3][3] * rc.x + C[3][4] * rc.y + C[3][5] * rc.z
-                          : (j == 1 ? C[3][4] * rc.x + C[4][4] * rc.y + C[4][5] * rc.z
-                                    : C[3][5] * rc.x + C[4][5] * rc.y + C[5][5] * rc.z);
+      const double* Ajc = A + 9 * j + 3 * c;  // tm[i][j][c] = (A_j Mbr_i)[c]
+      W.tm[lane] = (Ajc[0] * C[i][3] + Ajc[1] * C[i][4]) + Ajc[2] * C[i][5];
+      // bm[i][j][c] = sum_q Mrr[j][q] A_i[c][q]
+      const double* Aic = A + 9 * i + 3 * c;
+      const double m0 = j == 0 ? C[3][3] : (j == 1 ? C[3][4] : C[3][5]);
+      const double m1 = j == 0 ? C[3][4] : (j == 1 ? C[4][4] : C[4][5]);
+      const double m2 = j == 0 ? C[3][5] : (j == 1 ? C[4][5] : C[5][5]);
+      W.bm[lane] = (m0 * Aic[0] + m1 * Aic[1]) + m2 * Aic[2];
     }
     __syncwarp();
     if (lane < 4) {
-      P[lane] = lane == 0 ? C[6 + M][colE] : comp(n, lane - 1);
+      P[lane] = lane == 0 ? C[6 + M][colE] : nn[lane - 1];
     } else if (lane < 13) {  // slave gradients g_i = -Fb_i n + T_i(Fr)
       const int i = (lane - 4) / 3, a = (lane - 4) % 3;
-      const d3 gv = (-C[i][colF]) * n + Tmap(i, mk3(C[3][colF], C[4][colF], C[5][colF]), e1, e2);
-      P[lane] = comp(gv, a);
+      const double* Aia = A + 9 * i + 3 * a;
+      P[lane] = (-C[i][colF]) * nn[a] + ((Aia[0] * C[3][colF] + Aia[1] * C[4][colF]) + Aia[2] * C[5][colF]);
     }
     if (Hess) {
 #pragma unroll
@@ -327,23 +339,20 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
         if (lane + 32 * h2 < 45) {
           const int pk = ss_pk[h2];
           const int blk = pk & 7, a = (pk >> 3) & 3, c = (pk >> 5) & 3, i = (pk >> 7) & 3, j = (pk >> 9) & 3;
-          const d3 ra = Trow(i, a, e1, e2);
+          const double* ra = A + 9 * i + 3 * a;
           const double* B = W.bm + 9 * j;
-          const double qv = ra.x * B[c] + ra.y * B[3 + c] + ra.z * B[6 + c];
-          const double na = comp(n, a), nc = comp(n, c);
-          const double mbb = i <= j ? C[i][j] : C[j][i];
+          const double qv = (ra[0] * B[c] + ra[1] * B[3 + c]) + ra[2] * B[6 + c];
+          const double na = nn[a], nc = nn[c];
+          const double mbb = C[i][j];  // i <= j
           const double v = ((mbb * (na * nc) - na * W.tm[9 * i + 3 * j + c]) - W.tm[9 * j + 3 * i + a] * nc) + qv;
           P[kSSBase + 9 * blk + 3 * a + c] = v;
           if (i == j && a != c) P[kSSBase + 9 * blk + 3 * c + a] = v;
         }
       }
       for (int t = lane; t < M * (M + 1) / 2; t += 32) {  // master pairs, dense upper triangle
-        int m = 0, l = t;
-        while (l >= M - m) {
-          l -= M - m;
-          ++m;
-        }
-        P[pair_base(M) + t] = C[6 + m][6 + m + l];
+        const int pr = pair_tab[M][t];
+        const int m = pr & 15, l = pr >> 4;
+        P[pair_base(M) + t] = C[6 + m][6 + l];
       }
     }
     if (lane < M) P[kHdr + lane] = (double)my_lm;  // header: local master ids
@@ -351,18 +360,22 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     else if (lane == 29) P[kSlv + 1] = (double)sid1;
     else if (lane == 30) P[kSlv + 2] = (double)sid2;
     else if (lane == 31) P[kMcnt] = (double)M;
-    for (int t = lane; t < (Hess ? 4 * M : M); t += 32) {  // s_m, a_{m,i} = -Hwb_{m,i} n + T_i(Hwr_m)
-      const int m = Hess ? t >> 2 : t, wq = Hess ? t & 3 : 0;
-      double* out = P + m_base(M) + 10 * m;
-      if (wq == 0) {
-        out[0] = C[6 + m][colF];
-      } else {
-        const int i = wq - 1;
-        const d3 av = (-C[6 + m][i]) * n + Tmap(i, mk3(C[6 + m][3], C[6 + m][4], C[6 + m][5]), e1, e2);
-        out[1 + 3 * i] = av.x;
-        out[2 + 3 * i] = av.y;
-        out[3 + 3 * i] = av.z;
+    if (Hess) {
+      for (int t = lane; t < 10 * M; t += 32) {  // s_m, a_{m,i}[a] = -Hwb_{m,i} n_a + (A_i Hwr_m)[a]
+        const int m = t / 10, q = t % 10;
+        const double* Cm = C[6 + m];
+        double val;
+        if (q == 0) {
+          val = Cm[colF];
+        } else {
+          const int i = (q - 1) / 3, a = (q - 1) % 3;
+          const double* Aia = A + 9 * i + 3 * a;
+          val = (-Cm[i]) * nn[a] + ((Aia[0] * Cm[3] + Aia[1] * Cm[4]) + Aia[2] * Cm[5]);
+        }
+        P[m_base(M) + t] = val;
       }
+    } else {
+      if (lane < M) P[m_base(M) + 10 * lane] = C[6 + lane][colF];
     }
     __syncwarp();
   }
