@@ -54,6 +54,14 @@ int gmcp_set_surfaces(gmcp_ctx* ctx, const gmcp_surface* slave, const gmcp_surfa
 /* x: flat 3N positions. n_dof fixes N for the context (may change). */
 int gmcp_set_positions(gmcp_ctx* ctx, const double* x, int64_t n_dof);
 int gmcp_set_step(gmcp_ctx* ctx, const double* dx, int64_t n_dof);
+/* Batched independent scenes (no reference equivalent -- the
+ * reference runs one scene per System): scene[v] is the scene of vertex v
+ * (n_vertices = N, scenes numbered 0..S-1, S <= 2^20), or NULL for one scene.
+ * The broadphase then pairs a slave triangle only with master triangles of
+ * its own scene (scene taken from the triangle's first vertex), so a packed
+ * batch yields exactly the concatenation of the per-scene candidate sets and
+ * samples. Every later stage is per sample / per vertex and needs no change. */
+int gmcp_set_vertex_scenes(gmcp_ctx* ctx, const int32_t* scene, int64_t n_vertices);
 /* Device-resident fast path: the context's own x / dx buffers (3N doubles,
  * valid after gmcp_set_positions / gmcp_set_step sized them). */
 double* gmcp_positions_device(gmcp_ctx* ctx);

@@ -541,4 +541,45 @@ int ref_patch_test(double kappa, const int32_t* div_bottom, const int32_t* div_t
   });
 }
 
+// Hertz indentation meshes (bench.hpp:178-193) at a given refine.
+static void put_mesh(const TetMesh& m, int64_t* nv, double* v, int64_t* nt, int32_t* t) {
+  *nv = static_cast<int64_t>(m.vertices.size());
+  *nt = static_cast<int64_t>(m.tets.size());
+  if (v)
+    for (size_t i = 0; i < m.vertices.size(); ++i)
+      for (int k = 0; k < 3; ++k) v[3 * i + k] = m.vertices[i][k];
+  if (t)
+    for (size_t i = 0; i < m.tets.size(); ++i)
+      for (int k = 0; k < 4; ++k) t[4 * i + k] = m.tets[i][k];
+}
+
+int ref_hertz_meshes(double refine, int64_t* nvb, double* vb, int64_t* ntb, int32_t* tb, int64_t* nvh,
+                     double* vh, int64_t* nth, int32_t* th) {
+  return guarded([&] {
+    HertzConfig cfg;
+    cfg.refine = refine;
+    put_mesh(make_hertz_block(cfg), nvb, vb, ntb, tb);
+    put_mesh(make_hertz_ball(cfg), nvh, vh, nth, th);
+    return GMCP_OK;
+  });
+}
+
+// run_hertz (bench.hpp:210-303). out[0..13]: peak, p0, contact_radius,
+// alpha_H, outside_max, peak_rel_err, contact_radius_rel_err, applied_force,
+// total_newton_iters, steps, kappa_face, wall_seconds, samples, total_rebuilds.
+int ref_run_hertz(double refine, int32_t load_steps, double* out) {
+  return guarded([&] {
+    HertzConfig cfg;
+    cfg.refine = refine;
+    cfg.load_steps = load_steps;
+    const HertzResult r = run_hertz(cfg);
+    const double v[14] = {r.peak, r.oracle.p0, r.contact_radius, r.oracle.alpha_H, r.outside_max,
+                          r.peak_rel_err, r.contact_radius_rel_err, r.applied_force,
+                          (double)r.stats.total_newton_iters, (double)r.steps.size(), r.params.kappa_face,
+                          r.stats.wall_seconds, (double)r.profile.size(), (double)r.stats.total_rebuilds};
+    for (int k = 0; k < 14; ++k) out[k] = v[k];
+    return GMCP_OK;
+  });
+}
+
 }  // extern "C"

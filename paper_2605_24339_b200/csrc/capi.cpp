@@ -147,6 +147,29 @@ int gmcp_set_surfaces(gmcp_ctx* ctx, const gmcp_surface* slave, const gmcp_surfa
   });
 }
 
+int gmcp_set_vertex_scenes(gmcp_ctx* ctx, const int32_t* scene, int64_t n_vertices) {
+  return guarded([&] {
+    check_ctx(ctx);
+    Ctx& c = ctx->c;
+    c.have_pairs = false;
+    if (!scene) {
+      c.vscene.resize(0);
+      c.n_scenes = 1;
+      return GMCP_OK;
+    }
+    need(n_vertices >= 0, "vertex scenes: negative count");
+    int32_t mx = -1;
+    for (int64_t v = 0; v < n_vertices; ++v) {
+      need(scene[v] >= 0 && scene[v] < (1 << 20), "vertex scenes: ids must lie in [0, 2^20)");
+      mx = std::max(mx, scene[v]);
+    }
+    c.vscene.upload(scene, n_vertices, c.stream);
+    c.n_scenes = mx + 1;
+    c.sync();
+    return GMCP_OK;
+  });
+}
+
 int gmcp_set_positions(gmcp_ctx* ctx, const double* x, int64_t n_dof) {
   return guarded([&] {
     check_ctx(ctx);

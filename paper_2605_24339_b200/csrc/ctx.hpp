@@ -57,6 +57,10 @@ struct Ctx {
   double* X() const { return x_ext ? x_ext : x.p; }
   double* DX() const { return dx_ext ? dx_ext : dx.p; }
 
+  // batched scenes: scene id per vertex (empty = one scene)
+  DBuf<int32_t> vscene;
+  int32_t n_scenes = 1;
+
   // candidate pairs (CSR per slave tri)
   DBuf<int64_t> pair_off[3];
   DBuf<int32_t> pair_ids[3];

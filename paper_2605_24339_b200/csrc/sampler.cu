@@ -135,7 +135,11 @@ __device__ __forceinline__ unsigned int expand_bits(unsigned int v) {
   return v;
 }
 
+// Keys: Morton code of the AABB centroid (30 bits) above the triangle index
+// (ib bits, unique keys). With batched scenes the scene id sits above both,
+// so the hierarchy separates scenes before space.
 __global__ void k_morton(int32_t n, const Box* __restrict__ boxes, const unsigned long long* __restrict__ bounds,
+                         const int32_t* __restrict__ tris, const int32_t* __restrict__ vscene, int ib,
                          unsigned long long* __restrict__ keys, int32_t* __restrict__ idx) {
   double lo[3], ext[3];
   for (int k = 0; k < 3; ++k) {
@@ -152,7 +156,8 @@ __global__ void k_morton(int32_t n, const Box* __restrict__ boxes, const unsigne
       q[k] = (unsigned int)(u * 1023.0);
     }
     const unsigned long long m = (expand_bits(q[0]) << 2) | (expand_bits(q[1]) << 1) | expand_bits(q[2]);
-    keys[t] = (m << 32) | (unsigned int)t;  // unique keys: index breaks ties
+    const unsigned long long sc = vscene ? (unsigned long long)vscene[tris[3 * t]] : 0ull;
+    keys[t] = (sc << (30 + ib)) | (m << ib) | (unsigned long long)t;  // unique keys: index breaks ties
     idx[t] = (int32_t)t;
   }
 }
@@ -203,25 +208,39 @@ __device__ __forceinline__ Box ldcg_box(const Box* b) {  // L2 view: written by 
   return r;
 }
 
+// Bottom-up AABB refit (one thread per leaf; the second child to arrive
+// merges). With batched scenes each node also records its [min, max] scene.
 __global__ void k_refit(int n, const int32_t* __restrict__ sorted_idx, const Box* __restrict__ tri_boxes,
                         const int32_t* __restrict__ left, const int32_t* __restrict__ right,
-                        const int32_t* __restrict__ parent, Box* nodes, int32_t* flags) {
+                        const int32_t* __restrict__ parent, Box* nodes, int32_t* flags,
+                        const int32_t* __restrict__ tris, const int32_t* __restrict__ vscene, int2* srange) {
   GRID_LOOP(t, n) {
     int node = n - 1 + (int)t;
-    nodes[node] = tri_boxes[sorted_idx[t]];
+    const int32_t tri = sorted_idx[t];
+    nodes[node] = tri_boxes[tri];
+    if (vscene) {
+      const int sc = vscene[tris[3 * tri]];
+      srange[node] = make_int2(sc, sc);
+    }
     if (n == 1) continue;
     __threadfence();
     int p = parent[node];
     while (p >= 0) {
       if (atomicAdd(&flags[p], 1) == 0) break;  // first arrival: sibling not ready
       __threadfence();
-      const Box a = ldcg_box(nodes + __ldcg(left + p)), b = ldcg_box(nodes + __ldcg(right + p));
+      const int lc = __ldcg(left + p), rc = __ldcg(right + p);
+      const Box a = ldcg_box(nodes + lc), b = ldcg_box(nodes + rc);
       Box u;
       for (int k2 = 0; k2 < 3; ++k2) {
         u.lo[k2] = dmin(a.lo[k2], b.lo[k2]);
         u.hi[k2] = dmax(a.hi[k2], b.hi[k2]);
       }
       nodes[p] = u;
+      if (vscene) {
+        const int* ra = reinterpret_cast<const int*>(srange + lc);
+        const int* rb = reinterpret_cast<const int*>(srange + rc);
+        srange[p] = make_int2(min(__ldcg(ra), __ldcg(rb)), max(__ldcg(ra + 1), __ldcg(rb + 1)));
+      }
       __threadfence();
       p = p == 0 ? -1 : parent[p];
     }
@@ -256,8 +275,9 @@ __global__ void k_query(int32_t nst, const int32_t* __restrict__ stris, const do
                         int n_leaf, const Box* __restrict__ nodes, const int32_t* __restrict__ left,
                         const int32_t* __restrict__ right, const int32_t* __restrict__ sorted_idx,
                         int64_t* __restrict__ cnt, const int64_t* __restrict__ off, int32_t* __restrict__ out,
-                        int* overflow) {
+                        int* overflow, const int32_t* __restrict__ vscene, const int2* __restrict__ srange) {
   GRID_LOOP(st, nst) {
+    const int qs = vscene ? vscene[stris[3 * st]] : -1;  // batched scenes: own scene only
     Box q = tri_box(x, stris + 3 * st);
     for (int k = 0; k < 3; ++k) {  // Aabb::inflated, core.hpp:77-82
       q.lo[k] = q.lo[k] - r;
@@ -270,6 +290,10 @@ __global__ void k_query(int32_t nst, const int32_t* __restrict__ stris, const do
     const int64_t base = Mode ? off[st] : 0;
     while (top > 0) {
       const int node = stack[--top];
+      if (qs >= 0) {
+        const int2 sr = srange[node];
+        if (qs < sr.x || qs > sr.y) continue;
+      }
       if (!overlaps(nodes[node], q)) continue;
       if (node >= n_leaf - 1) {
         if (Mode) out[base + c] = sorted_idx[node - (n_leaf - 1)];
@@ -864,7 +888,18 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   keys_sorted.resize(nmt);
   idx.resize(nmt);
   idx_sorted.resize(nmt);
-  k_morton<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, tboxes.p, bounds.p, keys.p, idx.p);
+  const int32_t* vsc = c.vscene.n ? c.vscene.p : nullptr;
+  if (vsc && (int64_t)c.vscene.n != c.n_vertices())
+    throw StatusError(GMCP_ERR_CONFIG, "batched broadphase: vertex scene ids do not cover the positions");
+  int ib = 32;  // index bits of the key; fewer when a scene id must fit above the Morton code
+  if (vsc) {
+    ib = 1;
+    while ((1ll << ib) < nmt) ++ib;
+    int sb = 1;
+    while ((1 << sb) < c.n_scenes) ++sb;
+    if (sb + 30 + ib > 64) throw StatusError(GMCP_ERR_CONFIG, "batched broadphase: too many scenes x triangles");
+  }
+  k_morton<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, tboxes.p, bounds.p, c.master.tris.p, vsc, ib, keys.p, idx.p);
   sort_pairs(keys.p, keys_sorted.p, idx.p, idx_sorted.p, nmt, s, 64);
   const int nnodes = 2 * nmt - 1;
   nodes.resize(nnodes);
@@ -875,7 +910,10 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   flags.zero(s);
   GMCP_CUDA(cudaMemsetAsync(parent.p, 0xff, nnodes * sizeof(int32_t), s));
   if (nmt > 1) k_karras<<<grid_for(nmt - 1, 256), 256, 0, s>>>(nmt, keys_sorted.p, left.p, right.p, parent.p);
-  k_refit<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, idx_sorted.p, tboxes.p, left.p, right.p, parent.p, nodes.p, flags.p);
+  DBuf<int2> srange;
+  if (vsc) srange.resize(nnodes);
+  k_refit<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, idx_sorted.p, tboxes.p, left.p, right.p, parent.p, nodes.p, flags.p,
+                                             c.master.tris.p, vsc, srange.p);
   c.launches += 3 + (nmt > 1 ? 1 : 0) + 2;
   // K2: count, scan, emit+sort
   DBuf<int64_t> cnt;
@@ -885,12 +923,13 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   ovf.resize(1);
   ovf.zero(s);
   k_query<0><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
-                                                 idx_sorted.p, cnt.p, nullptr, nullptr, ovf.p);
+                                                 idx_sorted.p, cnt.p, nullptr, nullptr, ovf.p, vsc, srange.p);
   exclusive_scan(cnt.p, c.pair_off[0].p, nst + 1, s);
   const int64_t ntri = last_of(c.pair_off[0], nst, s);
   c.pair_ids[0].resize(std::max<int64_t>(ntri, 1));
   k_query<1><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
-                                                 idx_sorted.p, nullptr, c.pair_off[0].p, c.pair_ids[0].p, ovf.p);
+                                                 idx_sorted.p, nullptr, c.pair_off[0].p, c.pair_ids[0].p, ovf.p, vsc,
+                                                 srange.p);
   c.pair_ids[0].n = ntri;
   // K3: candidate edges / verts
   DBuf<int32_t> tmp_e, tmp_v;

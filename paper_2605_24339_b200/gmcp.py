@@ -189,6 +189,14 @@ class Context:
         _check(self.L.gmcp_set_positions(self.h, _p(x), C.c_int64(x.size)))
         self.n_dof = x.size
 
+    def set_vertex_scenes(self, scene):
+        """Batched independent scenes (C5): scene id per vertex, or None."""
+        if scene is None:
+            _check(self.L.gmcp_set_vertex_scenes(self.h, None, C.c_int64(0)))
+            return
+        sc = np.ascontiguousarray(scene, np.int32)
+        _check(self.L.gmcp_set_vertex_scenes(self.h, _p(sc), C.c_int64(sc.size)))
+
     def set_step(self, dx):
         dx = _f64(dx)
         _check(self.L.gmcp_set_step(self.h, _p(dx), C.c_int64(dx.size)))

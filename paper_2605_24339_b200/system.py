@@ -270,16 +270,7 @@ def body_stresses(body: Body, x: np.ndarray, rest: np.ndarray) -> np.ndarray:
     return lam * tr[:, None, None] * np.eye(3) + 2 * mu * eps
 
 
-def add_pressure_forces(faces: np.ndarray, rest: np.ndarray, magnitude: float, direction, f: np.ndarray):
-    x3 = rest.reshape(-1, 3)
-    for tri in faces:
-        a, b, c = x3[tri[0]], x3[tri[1]], x3[tri[2]]
-        cr = np.cross(b - a, c - a)
-        area = 0.5 * np.linalg.norm(cr)
-        d = np.asarray(direction, float) if direction is not None else -cr / np.linalg.norm(cr)
-        nf = magnitude * area / 3.0 * d
-        for i in range(3):
-            f[3 * tri[i]:3 * tri[i] + 3] += nf
+add_pressure_forces = S.add_pressure_forces
 
 
 def build_patch_scene(kappa: float = 1e6, div_bottom=(5, 5, 2), div_top=(4, 4, 2), device: int = 0) -> System:
@@ -347,3 +338,62 @@ def build_slab_system(nb: int, nt: int, texture_amp: float = 0.0, texture_freq: 
     down = np.nonzero(np.all(np.abs(r3[gtris, 2] - 0.102) < 1e-9, axis=1))[0]
     sys_.add_contact_pair(it, ib, S.BarrierParams(kappa_face=kappa, eps_max=1e-3), down, None)
     return sys_
+
+
+# ---------------------------------------------------------------------------
+# Hertz sphere-on-block indentation (C1), bench.hpp:195-303
+
+@dataclass
+class HertzResult:
+    oracle: S.HertzOracle
+    params: S.BarrierParams
+    block_tets: int = 0
+    ball_tets: int = 0
+    applied_force: float = 0.0
+    peak: float = 0.0
+    contact_radius: float = 0.0
+    outside_max: float = 0.0
+    peak_rel_err: float = 0.0
+    contact_radius_rel_err: float = 0.0
+    profile: np.ndarray | None = None  # (n, 3): radius, pressure, analytic pressure
+    stats: RunStats | None = None
+    face_samples: int = 0
+
+
+def build_hertz_system(cfg: S.HertzConfig | None = None, device: int = 0, scene: S.HertzScene | None = None):
+    """run_hertz set-up (bench.hpp:210-272) on a device System. Returns
+    (System, HertzResult skeleton)."""
+    sc = scene or S.hertz_scene(cfg)
+    sys_ = System(device)
+    ib = sys_.add_body(sc.block, sc.cfg.E, sc.cfg.nu, "block")
+    ih = sys_.add_body(sc.ball, sc.cfg.E, sc.cfg.nu, "ball")
+    for (v, ax), t in zip(sc.fixed.tolist(), sc.fixed_target.tolist()):
+        sys_.fix_dof(v, ax, t)
+    sys_.f_ext[:] = sc.f_ext
+    sys_.add_contact_pair(ib, ih, sc.params, sc.slave_tris, None)
+    res = HertzResult(sc.oracle, sys_.contacts[0][2], sc.block.tets.shape[0], sc.ball.tets.shape[0],
+                      sc.applied_force)
+    return sys_, res
+
+
+def run_hertz(cfg: S.HertzConfig | None = None, settings: SolverSettings | None = None, device: int = 0,
+              on_step=None) -> HertzResult:
+    """bench.hpp:210-303 on the device: solve, then the pressure profile metrics."""
+    cfg = cfg or S.HertzConfig()
+    sys_, res = build_hertz_system(cfg, device)
+    settings = settings or SolverSettings()
+    settings.load_steps = cfg.load_steps
+    res.stats = sys_.solve(settings, on_step)
+    field = sys_.contact_pressure_field(0)
+    res.face_samples = int(field.size)
+    r, p = field["radius"].astype(np.float64), field["pressure"].astype(np.float64)
+    res.peak = max(0.0, float(p.max())) if p.size else 0.0
+    order = np.argsort(r, kind="stable")
+    res.profile = np.stack([r[order], p[order], res.oracle.pressure(r[order])], axis=1)
+    act = p >= 0.05 * res.peak
+    res.contact_radius = float(r[act].max()) if np.any(act) else 0.0
+    out = r > 1.2 * res.oracle.alpha_H
+    res.outside_max = max(0.0, float(p[out].max())) if np.any(out) else 0.0
+    res.peak_rel_err = abs(res.peak - res.oracle.p0) / res.oracle.p0
+    res.contact_radius_rel_err = abs(res.contact_radius - res.oracle.alpha_H) / res.oracle.alpha_H
+    return res

@@ -146,3 +146,37 @@ def test_resolve_params_match(ref):
     cp = ref.resolve_params(S.BarrierParams(kappa_face=1e6, eps_max=1e-3), m)
     p = pi["params"]
     assert (cp.kappa_edge, cp.kappa_point, cp.detection_radius) == (p.kappa_edge, p.kappa_point, p.detection_radius)
+
+
+def test_hertz_generators_match_reference(ref):
+    """graded lattices, cylinder sector, sphere octant and the Hertz meshes
+    (mesh_gen.hpp, bench.hpp:178-193) bitwise against the reference."""
+    import ctypes as C
+    L = ref.lib
+    for refine in (0.7, 1.0):
+        n = [C.c_int64() for _ in range(4)]
+        L.ref_hertz_meshes(C.c_double(refine), C.byref(n[0]), None, C.byref(n[1]), None, C.byref(n[2]), None,
+                           C.byref(n[3]), None)
+        vb, tb = np.zeros((n[0].value, 3)), np.zeros((n[1].value, 4), np.int32)
+        vh, th = np.zeros((n[2].value, 3)), np.zeros((n[3].value, 4), np.int32)
+        assert L.ref_hertz_meshes(C.c_double(refine), C.byref(n[0]), C.c_void_p(vb.ctypes.data), C.byref(n[1]),
+                                  C.c_void_p(tb.ctypes.data), C.byref(n[2]), C.c_void_p(vh.ctypes.data),
+                                  C.byref(n[3]), C.c_void_p(th.ctypes.data)) == 0
+        cfg = S.HertzConfig(refine=refine)
+        b, h = S.make_hertz_block(cfg), S.make_hertz_ball(cfg)
+        assert _same(vb, b.vertices) and _same(tb, b.tets) and _same(vh, h.vertices) and _same(th, h.tets)
+
+
+@pytest.mark.parametrize("refine,count", [(0.7, 4112), (1.0, 9495)])
+def test_c1_hertz_sample_anchor(orc, refine, count):
+    """SURVEY 8 C1: Hertz at refine 0.7 -> 4,112 samples (9,495 at refine 1.0);
+    kappa_face and the oracle constants as the reference's run_hertz."""
+    sc = S.hertz_scene(S.HertzConfig(refine=refine))
+    assert (sc.rest.size // 3, sc.slave.tris.shape[0], sc.master.tris.shape[0]) == \
+        ((1253, 72, 720) if refine == 0.7 else (sc.rest.size // 3, sc.slave.tris.shape[0], sc.master.tris.shape[0]))
+    st = orc.contact_state(sc.slave, sc.master, orc.candidate_pairs(sc.slave, sc.master, sc.rest,
+                                                                    sc.params.detection_radius), sc.rest, sc.params)
+    assert len(st) == count
+    g = F.golden("hertz_ref.json")[str(refine)]
+    assert sc.params.kappa_face == g["kappa_face"] and sc.oracle.p0 == g["p0"] and sc.oracle.alpha_H == g["alpha_H"]
+    assert sc.applied_force == pytest.approx(g["applied_force"], rel=1e-14)
