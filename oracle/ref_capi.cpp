@@ -582,4 +582,52 @@ int ref_run_hertz(double refine, int32_t load_steps, double* out) {
   });
 }
 
+// parse_scene + build_scene + System::solve (scene.hpp:155-449, solver.hpp:125)
+// on a scene file. x_out (n_dof) may be null to query n_dof. stats[0..5]:
+// total_newton_iters, total_rebuilds, steps, wall_seconds, newton_tol_used,
+// final min gap; force_z_out[pair] = contact_force_summary(...).total per pair
+// (3 doubles each, up to max_pairs pairs).
+int ref_run_scene(const char* path, int64_t* n_dof, double* x_out, double* stats, double* force_out,
+                  int32_t max_pairs) {
+  return guarded([&] {
+    const SceneConfig cfg = parse_scene(path);
+    System sys = build_scene(cfg);
+    *n_dof = sys.x.size();
+    if (!x_out) return GMCP_OK;
+    const RunStats rs = sys.solve(cfg.solver);
+    for (Eigen::Index d = 0; d < sys.x.size(); ++d) x_out[d] = sys.x[d];
+    stats[0] = rs.total_newton_iters;
+    stats[1] = rs.total_rebuilds;
+    stats[2] = (double)rs.steps.size();
+    stats[3] = rs.wall_seconds;
+    stats[4] = rs.newton_tol_used;
+    stats[5] = rs.steps.empty() ? 0.0 : rs.steps.back().min_gap;
+    for (int p = 0; p < (int)sys.contacts.size() && p < max_pairs; ++p) {
+      const ContactForceSummary f = contact_force_summary(sys.contacts[p].state, sys.contacts[p].params, sys.x);
+      for (int k = 0; k < 3; ++k) force_out[3 * p + k] = f.total[k];
+    }
+    return GMCP_OK;
+  });
+}
+
+// build_scene arrays of a scene file (scene.hpp:382-449): f_ext, fixed mask,
+// Dirichlet targets and the slave triangle count of each contact pair.
+int ref_scene_arrays(const char* path, int64_t* n_dof, double* f_ext, uint8_t* fixed, double* dirichlet,
+                     int64_t* slave_tris, int32_t max_pairs) {
+  return guarded([&] {
+    const SceneConfig cfg = parse_scene(path);
+    System sys = build_scene(cfg);
+    *n_dof = sys.x.size();
+    if (!f_ext) return GMCP_OK;
+    for (Eigen::Index d = 0; d < sys.x.size(); ++d) {
+      f_ext[d] = sys.f_ext[d];
+      fixed[d] = sys.fixed[d];
+      dirichlet[d] = sys.dirichlet[d];
+    }
+    for (int p = 0; p < (int)sys.contacts.size() && p < max_pairs; ++p)
+      slave_tris[p] = (int64_t)sys.contacts[p].slave.tris.size();
+    return GMCP_OK;
+  });
+}
+
 }  // extern "C"

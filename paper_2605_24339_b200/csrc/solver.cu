@@ -89,6 +89,7 @@ struct MatSet {
   Bcsr el;
   Bcsr c[kMaxPairs];
   int np = 0;
+  double shift = 0;  // regularization added to every diagonal entry (solver.hpp:352-356)
 };
 
 __device__ __forceinline__ d3 bmv(const double* b, d3 p) {
@@ -114,6 +115,7 @@ __device__ __forceinline__ d3 row_mv(const Bcsr& A, int v, const double* __restr
 // scal: [0] rz [1] pq [2] alpha [3] beta [4] rr [5] bb
 
 constexpr int kRowLanes = 8;  // lanes per BCSR row in the SpMV
+constexpr double kRegularization = 1e-8;  // SolverSettings::regularization (solver.hpp:40)
 
 // y_v = sum_j A_vj (z_j + beta p_j) over one row by kRowLanes lanes (fixed butterfly: deterministic)
 __device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __restrict__ z,
@@ -153,8 +155,9 @@ __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const do
     }
     if (sub == 0 && v < nv) {
       const d3 m = ld3(mask, v);
-      const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
       const d3 pv = ld3(z, v) + beta * ld3(p_old, v);
+      if (M.shift != 0) acc = acc + M.shift * pv;
+      const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
       q[3 * v] = y.x;
       q[3 * v + 1] = y.y;
       q[3 * v + 2] = y.z;
@@ -252,6 +255,9 @@ __global__ void k_block_jacobi(int nv, MatSet M, const double* __restrict__ mask
       if (c)
         for (int q = 0; q < 9; ++q) D[q] += c[q];
     }
+    D[0] += M.shift;
+    D[4] += M.shift;
+    D[8] += M.shift;
     const double m[3] = {mask[3 * v], mask[3 * v + 1], mask[3 * v + 2]};
     for (int a = 0; a < 3; ++a)
       for (int b = 0; b < 3; ++b) {
@@ -272,6 +278,28 @@ __global__ void k_block_jacobi(int nv, MatSet M, const double* __restrict__ mask
       for (int a = 0; a < 3; ++a) o[4 * a] = D[4 * a] != 0 ? 1.0 / D[4 * a] : 1.0;
     }
   }
+}
+
+// Sum of the free-dof diagonal entries of H (elastic + contact) -> out[0]
+// (solver.hpp:333-336, the regularization scale).
+__global__ void __launch_bounds__(kThreads) k_diag_sum(int nv, MatSet M, const double* __restrict__ mask,
+                                                       double* out, RedSlot rs) {
+  double acc[1] = {0};
+  for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
+    double d[3] = {0, 0, 0};
+    const double* e = find_diag(M.el, v);
+    if (e)
+      for (int a = 0; a < 3; ++a) d[a] = e[4 * a];
+    for (int k = 0; k < M.np; ++k) {
+      const double* c = find_diag(M.c[k], v);
+      if (c)
+        for (int a = 0; a < 3; ++a) d[a] += c[4 * a];
+    }
+    for (int a = 0; a < 3; ++a)
+      if (mask[3 * v + a] != 0) acc[0] += d[a];
+  }
+  double o[1];
+  if (block_reduce_last<1>(acc, rs, o) && threadIdx.x == 0) out[0] = o[0];
 }
 
 // Elastic gradient K_el (x - rest) -> grad = g_el + sum_pairs g_c - lambda f_ext.
@@ -623,9 +651,10 @@ double assemble(SystemImpl& S, double lambda) {
 
 // Block-Jacobi PCG on the masked system (chunks of iterations replayed as one
 // CUDA graph). Returns iterations; dx in S.dx.
-int pcg(SystemImpl& S, double tol, int maxit, double* rel_out) {
+int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.0) {
   const int nv = S.nv();
-  const MatSet M = mats(S);
+  MatSet M = mats(S);
+  M.shift = shift;
   k_block_jacobi<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, M, S.mask_d.p, S.minv.p);
   k_pcg_init<<<kBlocks, kThreads, 0, S.stream>>>(nv, S.grad.p, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p, S.p.p,
                                                  S.scal.p, S.slot(0));
@@ -750,7 +779,25 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
         break;
       }
       double rel;
-      const int pit = pcg(S, st.pcg_tol, st.pcg_max_iters, &rel);
+      int pit = pcg(S, st.pcg_tol, st.pcg_max_iters, &rel);
+      if (!(rel <= st.pcg_tol)) {
+        // solver.hpp:352-361: not solved (singular: an unconstrained rigid mode
+        // before contact engages) -> retry with the diagonal shifted by
+        // regularization (1e-8) x the mean free diagonal entry.
+        k_diag_sum<<<kBlocks, kThreads, 0, S.stream>>>(S.nv(), mats(S), S.mask_d.p, S.scal.p + 10, S.slot(4));
+        ++S.launches;
+        double dsum;
+        GMCP_CUDA(cudaMemcpyAsync(&dsum, S.scal.p + 10, sizeof dsum, cudaMemcpyDeviceToHost, S.stream));
+        S.sync();
+        const double shift = kRegularization * dsum / (double)n_free;
+        pit += pcg(S, st.pcg_tol, st.pcg_max_iters, &rel, shift);
+        if (!(rel <= st.pcg_tol)) {
+          out->residual = resid;
+          throw StatusError(GMCP_ERR_SOLVER,
+                            "linear solve failed even with regularization; the system is insufficiently "
+                            "constrained (unfixed rigid body modes?)");
+        }
+      }
       ss.pcg_iters += pit;
       ss.newton_iters += 1;
       double alpha = 1.0;

@@ -439,17 +439,28 @@ def make_hertz_ball(c: HertzConfig) -> TetMesh:
 
 
 def add_pressure_forces(faces: np.ndarray, rest: np.ndarray, magnitude: float, direction, f: np.ndarray):
-    """bench.hpp:18-25: magnitude * area / 3 per face vertex along direction
-    (or the inward normal when direction is None)."""
+    """elasticity.hpp:147-160: magnitude * area / 3 per face vertex along
+    direction (default: inward normal -cr.normalized()), faces in order, in the
+    reference's scalar op order (bitwise the reference's f_ext)."""
     x3 = rest.reshape(-1, 3)
-    for tri in faces:
-        a, b, c = x3[tri[0]], x3[tri[1]], x3[tri[2]]
-        cr = np.cross(b - a, c - a)
-        area = 0.5 * np.linalg.norm(cr)
-        d = np.asarray(direction, float) if direction is not None else -cr / np.linalg.norm(cr)
-        nf = magnitude * area / 3.0 * d
+    for tri in np.asarray(faces).tolist():
+        a, b, c = x3[tri[0]].tolist(), x3[tri[1]].tolist(), x3[tri[2]].tolist()
+        u = (b[0] - a[0], b[1] - a[1], b[2] - a[2])
+        v = (c[0] - a[0], c[1] - a[1], c[2] - a[2])
+        cr = (u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0])
+        sq = (cr[0] * cr[0] + cr[1] * cr[1]) + cr[2] * cr[2]
+        area = 0.5 * math.sqrt(sq)
+        if direction is not None:
+            d = tuple(float(t) for t in direction)
+        else:
+            nrm = math.sqrt(sq)
+            d = (-(cr[0] / nrm), -(cr[1] / nrm), -(cr[2] / nrm)) if sq > 0 else (-cr[0], -cr[1], -cr[2])
+        s_ = magnitude * area / 3.0
         for i in range(3):
-            f[3 * tri[i]:3 * tri[i] + 3] += nf
+            g = 3 * tri[i]
+            f[g] += s_ * d[0]
+            f[g + 1] += s_ * d[1]
+            f[g + 2] += s_ * d[2]
 
 
 @dataclass

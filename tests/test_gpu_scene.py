@@ -1,0 +1,34 @@
+"""Scene files solved on the device (parse_scene + build_scene + System::solve
+on B200) against the reference's own solve of the same file
+(tests/golden/<scene>_ref.npz, made by tests/golden/make_scene_golden.py):
+the patch test and C4, the two-pad fingertip squeeze (2 contact pairs, 20
+load steps)."""
+import os
+
+import numpy as np
+import pytest
+
+import fixtures as F  # noqa: F401  (sys.path set-up)
+from paper_2605_24339_b200 import scene as SC
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,tol", [("patch_test", 1e-4), ("fingertip", 1e-9)])
+def test_scene_matches_reference_solve(name, tol):
+    g = np.load(os.path.join(ROOT, "tests", "golden", name + "_ref.npz"))
+    sys_, st = SC.run_scene(os.path.join(ROOT, "scenes", name + ".scene"))
+    x_ref = g["x"]
+    u_ref = x_ref - sys_.rest
+    # same equilibrium up to the Newton tolerance's slack (residual <= tol_N;
+    # patch test: 6.25e-7 N against a soft interface -> ~1e-4 of u; measured
+    # 8.7e-5. Fingertip: measured 1e-13)
+    assert np.max(np.abs(sys_.x - x_ref)) <= tol * np.max(np.abs(u_ref))
+    assert len(st.steps) == int(g["stats"][2])
+    assert abs(st.total_newton_iters - int(g["stats"][0])) <= 3
+    assert st.newton_tol_used == g["stats"][4]
+    assert all(s.min_gap > 0 for s in st.steps)
+    for p in range(len(sys_.contacts)):
+        tot = sys_.contact_force_summary(p)[3]
+        assert np.allclose(tot, g["force"][3 * p:3 * p + 3], rtol=tol, atol=tol * np.max(np.abs(g["force"])))
