@@ -630,4 +630,39 @@ int ref_scene_arrays(const char* path, int64_t* n_dof, double* f_ext, uint8_t* f
   });
 }
 
+// The reference's own writers (vtk_io.hpp) on given arrays, for byte-level
+// format pinning: <dir>/vol.vtk (tets + displacement + stress), <dir>/surf.vtk,
+// <dir>/p.csv (7 columns as write_step_outputs), <dir>/report.txt.
+int ref_write_formats(const char* dir, const double* pts, int64_t np, const int32_t* tets, int64_t nt,
+                      const int32_t* tris, int64_t ntri, const double* disp, const double* stress,
+                      const double* rows, int64_t nrows) {
+  return guarded([&] {
+    const std::string d(dir);
+    std::vector<Vec3> points(np);
+    for (int64_t i = 0; i < np; ++i) points[i] = Vec3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    std::vector<std::array<int, 4>> cells(nt);
+    for (int64_t i = 0; i < nt; ++i)
+      for (int k = 0; k < 4; ++k) cells[i][k] = tets[4 * i + k];
+    std::vector<std::array<int, 3>> tr(ntri);
+    for (int64_t i = 0; i < ntri; ++i)
+      for (int k = 0; k < 3; ++k) tr[i][k] = tris[3 * i + k];
+    GridField dsp{"displacement", 3, std::vector<Real>(disp, disp + 3 * np)};
+    GridField sig{"cauchy_stress", 9, std::vector<Real>(stress, stress + 9 * nt)};
+    save_vtk_tets(d + "/vol.vtk", points, cells, {dsp}, {sig});
+    save_vtk_tris(d + "/surf.vtk", points, tr);
+    std::vector<std::vector<Real>> rw(nrows);
+    for (int64_t i = 0; i < nrows; ++i) rw[i].assign(rows + 7 * i, rows + 7 * i + 7);
+    save_csv(d + "/p.csv", {"pair", "sample", "x", "y", "z", "gap", "pressure"}, rw);
+    Report rep;
+    rep.set("scene.path", std::string("a b.scene"));
+    rep.set("scene.bodies", 3L);
+    rep.set("x", 0.1);
+    rep.set("y", -2.5e-300);
+    rep.set("x", 1.0 / 3.0);
+    rep.set("threads", 1);
+    rep.save(d + "/report.txt");
+    return GMCP_OK;
+  });
+}
+
 }  // extern "C"

@@ -32,3 +32,28 @@ def test_scene_matches_reference_solve(name, tol):
     for p in range(len(sys_.contacts)):
         tot = sys_.contact_force_summary(p)[3]
         assert np.allclose(tot, g["force"][3 * p:3 * p + 3], rtol=tol, atol=tol * np.max(np.abs(g["force"])))
+
+
+@pytest.mark.gpu
+def test_scene_outputs_deterministic(tmp_path):
+    """bench.hpp:374-402 run_scene with per-step files, twice in sequential
+    mode: every file byte-identical (the reference's determinism criterion);
+    pressure tables list each pair's face samples with positive pressures."""
+    from paper_2605_24339_b200 import outputs as O
+    import shutil
+    d = tmp_path / "out"
+    snaps = []
+    for k in range(2):  # same output directory both times (it is echoed in the report)
+        if d.exists():
+            shutil.rmtree(d)
+        cfg = SC.parse_scene(os.path.join(ROOT, "scenes", "patch_test.scene"))
+        rep = O.run_scene(cfg, out_override=str(d), sequential=True)
+        snaps.append({p.name: p.read_bytes() for p in d.iterdir()})
+    names = sorted(snaps[0])
+    assert names == sorted(snaps[1])
+    assert "report.txt" in names and "step_10_pressure.csv" in names and "step_01_volume.vtk" in names
+    for n in names:
+        assert snaps[0][n] == snaps[1][n], n
+    assert rep.find("total_newton_iters") is not None and rep.find("wall_seconds") is None
+    rows = np.loadtxt(d / "step_10_pressure.csv", delimiter=",", skiprows=1)
+    assert rows.shape[1] == 7 and np.all(rows[:, 0] == 0) and np.max(rows[:, 6]) > 0
