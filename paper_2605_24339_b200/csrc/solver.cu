@@ -117,16 +117,32 @@ __device__ __forceinline__ d3 row_mv(const Bcsr& A, int v, const double* __restr
 constexpr int kRowLanes = 8;  // lanes per BCSR row in the SpMV
 constexpr double kRegularization = 1e-8;  // SolverSettings::regularization (solver.hpp:40)
 
-// y_v = sum_j A_vj (z_j + beta p_j) over one row by kRowLanes lanes (fixed butterfly: deterministic)
+// A_vj x with the block read through the read-only path
+__device__ __forceinline__ d3 bmv_ro(const double* __restrict__ b, d3 p) {
+  const double b0 = __ldg(b), b1 = __ldg(b + 1), b2 = __ldg(b + 2), b3 = __ldg(b + 3), b4 = __ldg(b + 4);
+  const double b5 = __ldg(b + 5), b6 = __ldg(b + 6), b7 = __ldg(b + 7), b8 = __ldg(b + 8);
+  return d3{b0 * p.x + b1 * p.y + b2 * p.z, b3 * p.x + b4 * p.y + b5 * p.z, b6 * p.x + b7 * p.y + b8 * p.z};
+}
+
+// y_v = sum_j A_vj (z_j + beta p_j) over one row by kRowLanes lanes, two
+// blocks in flight per lane (fixed order: deterministic)
 __device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __restrict__ z,
                                       const double* __restrict__ p, double beta, int sub) {
-  d3 acc = mk3(0, 0, 0);
-  const int a = A.rowptr[v], b = A.rowptr[v + 1];
-  for (int k = a + sub; k < b; k += kRowLanes) {
-    const int j = A.cols[k];
-    acc = acc + bmv(A.vals + 9 * (int64_t)k, ld3(z, j) + beta * ld3(p, j));
+  d3 acc0 = mk3(0, 0, 0), acc1 = mk3(0, 0, 0);
+  const int a = __ldg(A.rowptr + v), b = __ldg(A.rowptr + v + 1);
+  int k = a + sub;
+  for (; k + kRowLanes < b; k += 2 * kRowLanes) {
+    const int j0 = __ldg(A.cols + k), j1 = __ldg(A.cols + k + kRowLanes);
+    const d3 x0 = ld3(z, j0) + beta * ld3(p, j0);
+    const d3 x1 = ld3(z, j1) + beta * ld3(p, j1);
+    acc0 = acc0 + bmv_ro(A.vals + 9 * (int64_t)k, x0);
+    acc1 = acc1 + bmv_ro(A.vals + 9 * (int64_t)(k + kRowLanes), x1);
   }
-  return acc;
+  if (k < b) {
+    const int j = __ldg(A.cols + k);
+    acc0 = acc0 + bmv_ro(A.vals + 9 * (int64_t)k, ld3(z, j) + beta * ld3(p, j));
+  }
+  return acc0 + acc1;
 }
 
 // K9a: p_new = z + beta p_old (own rows), q = mask .* (H p_new), pq -> alpha (last block).
@@ -670,6 +686,7 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   const double target = tol * tol * bb;
   const int chunk = 16;
   const int gsp = std::min(grid_for((int64_t)nv * kRowLanes, kThreads), kBlocks);
+  const int gup = std::min(grid_for((int64_t)nv, kThreads), kBlocks);  // one vertex per thread
   // one chunk of iterations as a CUDA graph (pointers fixed for this solve)
   cudaGraph_t graph;
   cudaGraphExec_t exec;
@@ -678,7 +695,7 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
     double* p_old = (k & 1) ? S.w.p : S.p.p;
     double* p_new = (k & 1) ? S.p.p : S.w.p;
     k_spmv_cg<<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p, S.slot(1));
-    k_update_cg<<<kBlocks, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
+    k_update_cg<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
                                                     S.slot(2));
   }
   GMCP_CUDA(cudaStreamEndCapture(S.stream, &graph));
