@@ -234,6 +234,8 @@ void build_assembly_plan(Ctx& c) {
   P.nnzb = (int64_t)cols.size();
   P.rowptr.upload(rowptr, s);
   P.cols.upload(cols, s);
+  P.h_rowptr = rowptr;
+  P.h_cols = cols;
   P.vals.resize(std::max<int64_t>(9 * P.nnzb, 1));
   P.row_ent_off.upload(eoff, s);
   P.row_ent.upload(ents, s);

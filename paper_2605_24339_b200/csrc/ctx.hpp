@@ -33,6 +33,7 @@ struct AssemblyPlan {
   int64_t nnzb = 0;
   DBuf<int32_t> rowptr;      // [N+1]
   DBuf<int32_t> cols;        // [nnzb]
+  std::vector<int32_t> h_rowptr, h_cols;  // host mirror of the pattern (System's merged matrix)
   DBuf<double> vals;         // [nnzb][9]
   DBuf<int32_t> row_ent_off; // [N+1]
   DBuf<int32_t> blk_off;     // [nnzb+1] contribution list of each BCSR block

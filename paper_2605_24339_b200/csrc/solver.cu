@@ -417,6 +417,28 @@ __global__ void k_motion(int64_t n, const int32_t* __restrict__ verts, const dou
   if ((threadIdx.x & 31) == 0) atomicMax(red, best);
 }
 
+// Merged values: H_k = K_el[src0] + sum_p K_c,p[src1+p] (fixed order).
+struct ValPtrs {
+  const double* v[1 + kMaxPairs];
+};
+__global__ void k_merge(int64_t nnzb, int ns, const int32_t* __restrict__ src, ValPtrs V, double* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnzb; k += (int64_t)gridDim.x * blockDim.x) {
+    double acc[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+    for (int s = 0; s < ns; ++s) {
+      const int32_t i = src[(int64_t)ns * k + s];
+      if (i >= 0) {
+        const double* b = V.v[s] + 9 * (int64_t)i;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q] += b[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) out[9 * k + q] = acc[q];
+  }
+}
+
 int grid_for(int64_t n, int threads) {
   const int64_t b = (n + threads - 1) / threads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
@@ -457,6 +479,14 @@ struct SystemImpl {
   DBuf<unsigned long long> redu;
   DBuf<int32_t> k_rowptr, k_cols;
   DBuf<double> k_vals;
+  std::vector<int32_t> h_krowptr, h_kcols;
+  // merged Newton matrix H = K_el + sum_pairs K_c on the union pattern (PCG operand);
+  // u_src[(1 + np) * k + s]: block index of union block k in the elastic (s = 0) /
+  // pair s-1 matrix, or -1. Pattern rebuilt when a pair is re-sampled.
+  DBuf<int32_t> u_rowptr, u_cols, u_src;
+  DBuf<double> u_vals;
+  int64_t u_nnzb = 0;
+  bool u_valid = false;
   DBuf<const double*> gc_ptrs;
   bool el_built = false;
   int64_t el_nnzb = 0;
@@ -563,21 +593,64 @@ void build_elastic(SystemImpl& S) {
     rowptr[v + 1] = (int32_t)cols.size();
   }
   S.k_rowptr.upload(rowptr, S.stream);
+  S.h_krowptr = rowptr;
+  S.h_kcols = cols;
   S.k_cols.upload(cols, S.stream);
   S.k_vals.upload(vals, S.stream);
   S.el_nnzb = (int64_t)cols.size();
   S.el_built = true;
 }
 
+// The PCG operand: the merged matrix (one BCSR) when pairs exist.
 MatSet mats(SystemImpl& S) {
   MatSet M;
-  M.el = Bcsr{S.k_rowptr.p, S.k_cols.p, S.k_vals.p};
-  M.np = (int)S.pairs.size();
-  for (int k = 0; k < M.np; ++k) {
-    const AssemblyPlan& P = S.pairs[k]->c->plan;
-    M.c[k] = Bcsr{P.rowptr.p, P.cols.p, P.vals.p};
+  if (S.pairs.empty() || !S.u_valid) {
+    M.el = Bcsr{S.k_rowptr.p, S.k_cols.p, S.k_vals.p};
+    M.np = (int)S.pairs.size();
+    for (int k = 0; k < M.np; ++k) {
+      const AssemblyPlan& P = S.pairs[k]->c->plan;
+      M.c[k] = Bcsr{P.rowptr.p, P.cols.p, P.vals.p};
+    }
+    return M;
   }
+  M.el = Bcsr{S.u_rowptr.p, S.u_cols.p, S.u_vals.p};
+  M.np = 0;
   return M;
+}
+
+// Union pattern of the elastic and every pair's contact BCSR (host, per rebuild).
+void build_union(SystemImpl& S) {
+  const int nv = S.nv(), np = (int)S.pairs.size();
+  std::vector<int32_t> rowptr(nv + 1, 0), cols, src;
+  struct E {
+    int32_t col, source, idx;
+  };
+  std::vector<E> row;
+  for (int v = 0; v < nv; ++v) {
+    row.clear();
+    for (int k = S.h_krowptr[v]; k < S.h_krowptr[v + 1]; ++k) row.push_back({S.h_kcols[k], 0, k});
+    for (int p = 0; p < np; ++p) {
+      const AssemblyPlan& P = S.pairs[p]->c->plan;
+      for (int k = P.h_rowptr[v]; k < P.h_rowptr[v + 1]; ++k) row.push_back({P.h_cols[k], 1 + p, k});
+    }
+    std::sort(row.begin(), row.end(), [](const E& a, const E& b) {
+      return a.col != b.col ? a.col < b.col : a.source < b.source;
+    });
+    for (size_t q = 0; q < row.size(); ++q) {
+      if (q == 0 || row[q].col != row[q - 1].col) {
+        cols.push_back(row[q].col);
+        src.insert(src.end(), 1 + np, -1);
+      }
+      src[src.size() - (1 + np) + row[q].source] = row[q].idx;
+    }
+    rowptr[v + 1] = (int32_t)cols.size();
+  }
+  S.u_rowptr.upload(rowptr, S.stream);
+  S.u_cols.upload(cols, S.stream);
+  S.u_src.upload(src, S.stream);
+  S.u_nnzb = (int64_t)cols.size();
+  S.u_vals.resize(std::max<int64_t>(9 * S.u_nnzb, 1));
+  S.u_valid = true;
 }
 
 // solver.hpp:256-269
@@ -598,6 +671,7 @@ double derived_newton_tol(const SystemImpl& S) {
 
 void rebuild_pair(SystemImpl& S, PairRt& pr, const double* eps_ref_dev) {
   Ctx& c = *pr.c;
+  S.u_valid = false;
   int64_t counts[3];
   run_broadphase(c, pr.params.detection_radius, counts);
   run_sampler(c, eps_ref_dev);
@@ -650,6 +724,15 @@ double assemble(SystemImpl& S, double lambda) {
     int64_t bad = -1;
     run_assembly(*pr->c, 1, &bad);
     gp.push_back(pr->c->grad.p);
+  }
+  if (!S.pairs.empty()) {  // merged PCG operand
+    if (!S.u_valid) build_union(S);
+    ValPtrs V{};
+    V.v[0] = S.k_vals.p;
+    for (size_t p = 0; p < S.pairs.size(); ++p) V.v[1 + p] = S.pairs[p]->c->plan.vals.p;
+    k_merge<<<grid_for(S.u_nnzb, 256), 256, 0, S.stream>>>(S.u_nnzb, 1 + (int)S.pairs.size(), S.u_src.p, V,
+                                                            S.u_vals.p);
+    ++S.launches;
   }
   S.gc_ptrs.resize(std::max<size_t>(gp.size(), 1));
   if (!gp.empty())
