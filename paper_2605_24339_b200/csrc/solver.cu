@@ -84,6 +84,8 @@ struct Bcsr {
   const int32_t* rowptr = nullptr;
   const int32_t* cols = nullptr;
   const double* vals = nullptr;
+  int bs = 9;       // value (block k, entry q) at vals[k * bs + q * cs]:
+  int64_t cs = 1;   // AoS (9, 1) or component-major (1, nnzb)
 };
 struct MatSet {
   Bcsr el;
@@ -114,13 +116,15 @@ __device__ __forceinline__ d3 row_mv(const Bcsr& A, int v, const double* __restr
 //   z = Minv r, beta = rz_new / rz.
 // scal: [0] rz [1] pq [2] alpha [3] beta [4] rr [5] bb
 
-constexpr int kRowLanes = 8;  // lanes per BCSR row in the SpMV
+constexpr int kRowLanes = 4;  // lanes per BCSR row in the SpMV (4 beats 2, 8, 16 on C3)
 constexpr double kRegularization = 1e-8;  // SolverSettings::regularization (solver.hpp:40)
 
-// A_vj x with the block read through the read-only path
-__device__ __forceinline__ d3 bmv_ro(const double* __restrict__ b, d3 p) {
-  const double b0 = __ldg(b), b1 = __ldg(b + 1), b2 = __ldg(b + 2), b3 = __ldg(b + 3), b4 = __ldg(b + 4);
-  const double b5 = __ldg(b + 5), b6 = __ldg(b + 6), b7 = __ldg(b + 7), b8 = __ldg(b + 8);
+// A_vj x for block k, read through the read-only path (either layout)
+__device__ __forceinline__ d3 bmv_ro(const Bcsr& A, int64_t k, d3 p) {
+  const double* b = A.vals + k * A.bs;
+  const int64_t c = A.cs;
+  const double b0 = __ldg(b), b1 = __ldg(b + c), b2 = __ldg(b + 2 * c), b3 = __ldg(b + 3 * c), b4 = __ldg(b + 4 * c);
+  const double b5 = __ldg(b + 5 * c), b6 = __ldg(b + 6 * c), b7 = __ldg(b + 7 * c), b8 = __ldg(b + 8 * c);
   return d3{b0 * p.x + b1 * p.y + b2 * p.z, b3 * p.x + b4 * p.y + b5 * p.z, b6 * p.x + b7 * p.y + b8 * p.z};
 }
 
@@ -135,12 +139,12 @@ __device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __rest
     const int j0 = __ldg(A.cols + k), j1 = __ldg(A.cols + k + kRowLanes);
     const d3 x0 = ld3(z, j0) + beta * ld3(p, j0);
     const d3 x1 = ld3(z, j1) + beta * ld3(p, j1);
-    acc0 = acc0 + bmv_ro(A.vals + 9 * (int64_t)k, x0);
-    acc1 = acc1 + bmv_ro(A.vals + 9 * (int64_t)(k + kRowLanes), x1);
+    acc0 = acc0 + bmv_ro(A, k, x0);
+    acc1 = acc1 + bmv_ro(A, k + kRowLanes, x1);
   }
   if (k < b) {
     const int j = __ldg(A.cols + k);
-    acc0 = acc0 + bmv_ro(A.vals + 9 * (int64_t)k, ld3(z, j) + beta * ld3(p, j));
+    acc0 = acc0 + bmv_ro(A, k, ld3(z, j) + beta * ld3(p, j));
   }
   return acc0 + acc1;
 }
@@ -251,24 +255,26 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(int nv, const double* __r
 }
 
 // Block-Jacobi: Minv_v = inverse of the masked 3x3 diagonal block.
-__device__ __forceinline__ const double* find_diag(const Bcsr& A, int v) {
+// diagonal block of row v copied to d[9] (either layout); false if absent
+__device__ __forceinline__ bool get_diag(const Bcsr& A, int v, double* d) {
   int lo = A.rowptr[v], hi = A.rowptr[v + 1];
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (A.cols[mid] < v) lo = mid + 1; else hi = mid;
   }
-  return (lo < A.rowptr[v + 1] && A.cols[lo] == v) ? A.vals + 9 * (int64_t)lo : nullptr;
+  if (!(lo < A.rowptr[v + 1] && A.cols[lo] == v)) return false;
+  const double* b = A.vals + (int64_t)lo * A.bs;
+  for (int q = 0; q < 9; ++q) d[q] = b[q * A.cs];
+  return true;
 }
 
 __global__ void k_block_jacobi(int nv, MatSet M, const double* __restrict__ mask, double* __restrict__ minv) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
     double D[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const double* e = find_diag(M.el, v);
-    if (e)
-      for (int q = 0; q < 9; ++q) D[q] = e[q];
+    get_diag(M.el, v, D);
     for (int k = 0; k < M.np; ++k) {
-      const double* c = find_diag(M.c[k], v);
-      if (c)
+      double c[9];
+      if (get_diag(M.c[k], v, c))
         for (int q = 0; q < 9; ++q) D[q] += c[q];
     }
     D[0] += M.shift;
@@ -303,12 +309,12 @@ __global__ void __launch_bounds__(kThreads) k_diag_sum(int nv, MatSet M, const d
   double acc[1] = {0};
   for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
     double d[3] = {0, 0, 0};
-    const double* e = find_diag(M.el, v);
-    if (e)
+    double e[9];
+    if (get_diag(M.el, v, e))
       for (int a = 0; a < 3; ++a) d[a] = e[4 * a];
     for (int k = 0; k < M.np; ++k) {
-      const double* c = find_diag(M.c[k], v);
-      if (c)
+      double c[9];
+      if (get_diag(M.c[k], v, c))
         for (int a = 0; a < 3; ++a) d[a] += c[4 * a];
     }
     for (int a = 0; a < 3; ++a)
@@ -435,7 +441,7 @@ __global__ void k_merge(int64_t nnzb, int ns, const int32_t* __restrict__ src, V
       }
     }
 #pragma unroll
-    for (int q = 0; q < 9; ++q) out[9 * k + q] = acc[q];
+    for (int q = 0; q < 9; ++q) out[q * nnzb + k] = acc[q];  // component-major (coalesced SpMV loads)
   }
 }
 
@@ -613,7 +619,7 @@ MatSet mats(SystemImpl& S) {
     }
     return M;
   }
-  M.el = Bcsr{S.u_rowptr.p, S.u_cols.p, S.u_vals.p};
+  M.el = Bcsr{S.u_rowptr.p, S.u_cols.p, S.u_vals.p, 1, S.u_nnzb};
   M.np = 0;
   return M;
 }
