@@ -307,9 +307,9 @@ static int grad_common(gmcp_ctx* ctx, int mode, double* grad, double* energy, in
       if (bad) *bad = se.bad;
       throw;
     }
-    if (grad) {
-      std::vector<double> g(c.n_dof);
-      c.grad.download(g.data(), c.n_dof, c.stream);
+    if (grad) {  // accumulated into the caller's buffer (contact_energy.hpp:126-142)
+      double* g = c.stage((size_t)c.n_dof);
+      c.grad.download(g, c.n_dof, c.stream);
       c.sync();
       for (int64_t i = 0; i < c.n_dof; ++i) grad[i] += g[i];
     }

@@ -80,6 +80,25 @@ struct Ctx {
   DBuf<double> red_d;
   DBuf<unsigned long long> red_u;
 
+  // pinned host staging for downloads that are accumulated into caller buffers
+  double* h_stage = nullptr;
+  size_t h_stage_n = 0;
+  double* stage(size_t n) {
+    if (n > h_stage_n) {
+      if (h_stage) cudaFreeHost(h_stage);
+      h_stage = nullptr;
+      GMCP_CUDA(cudaMallocHost(&h_stage, std::max<size_t>(n, 1) * sizeof(double)));
+      h_stage_n = n;
+    }
+    return h_stage;
+  }
+  Ctx() = default;
+  Ctx(const Ctx&) = delete;
+  Ctx& operator=(const Ctx&) = delete;
+  ~Ctx() {
+    if (h_stage) cudaFreeHost(h_stage);
+  }
+
   DevSamples samples() const {
     DevSamples d;
     d.n = ns;
