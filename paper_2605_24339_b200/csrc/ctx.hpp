@@ -22,8 +22,6 @@ struct AssemblyPlan {
   DBuf<int32_t> run_slave;   // [R][3]
   DBuf<int32_t> lm_off;      // [R+1] local master vertex table offsets
   DBuf<int32_t> lm_ids;      // global ids, ascending within a run
-  DBuf<int32_t> lp_off;      // [R+1] local master pair table offsets
-  DBuf<int32_t> lp;          // packed (a << 16 | b), local indices, a <= b
   DBuf<int64_t> pbase;       // [R] partial base offset (doubles)
   DBuf<uint32_t> li4;        // per sample: local master index of each slot (u8 x 3, 0xff = none)
   int64_t partial_len = 0;
@@ -34,6 +32,12 @@ struct AssemblyPlan {
   DBuf<int32_t> rowptr;      // [N+1]
   DBuf<int32_t> cols;        // [nnzb]
   std::vector<int32_t> h_rowptr, h_cols;  // host mirror of the pattern (System's merged matrix)
+  // device planner scratch (plan.cu), reused across rebuilds
+  struct Tmp {
+    DBuf<int32_t> head, hscan, run_cnt, run_first, run_M, rowcnt, ucnt, nuniq;
+    DBuf<int64_t> seg_start, psize, ccount, coff, ecount, eoff, cval, cval2, eval, eval2;
+    DBuf<unsigned long long> pmask, ckey, ckey2, ekey, ekey2, ukey;
+  } tmp;
   DBuf<double> vals;         // [nnzb][9]
   DBuf<int32_t> row_ent_off; // [N+1]
   DBuf<int32_t> blk_off;     // [nnzb+1] contribution list of each BCSR block

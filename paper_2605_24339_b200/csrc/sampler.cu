@@ -22,48 +22,13 @@
 
 #include "ctx.hpp"
 #include "kin.cuh"
+#include "cubutil.cuh"
 
 namespace gmcp_b200 {
 
 namespace {
 
 constexpr double kDblMax = 1.7976931348623157e308;
-
-// ---------------------------------------------------------------------------
-// scan / sort helpers (CUB, temp storage owned here)
-
-struct Scratch {
-  DBuf<unsigned char> tmp;
-  void* get(size_t bytes) {
-    tmp.resize(std::max<size_t>(bytes, 1));
-    return tmp.p;
-  }
-};
-Scratch g_scratch;
-
-template <class T>
-void exclusive_scan(const T* in, T* out, int64_t n, cudaStream_t s) {
-  size_t bytes = 0;
-  GMCP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
-  void* t = g_scratch.get(bytes);
-  GMCP_CUDA(cub::DeviceScan::ExclusiveSum(t, bytes, in, out, n, s));
-}
-
-template <class K, class V>
-void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, int64_t n, cudaStream_t s, int end_bit) {
-  size_t bytes = 0;
-  GMCP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, n, 0, end_bit, s));
-  void* t = g_scratch.get(bytes);
-  GMCP_CUDA(cub::DeviceRadixSort::SortPairs(t, bytes, kin, kout, vin, vout, n, 0, end_bit, s));
-}
-
-template <class K>
-void sort_keys(const K* kin, K* kout, int64_t n, cudaStream_t s, int end_bit) {
-  size_t bytes = 0;
-  GMCP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kin, kout, n, 0, end_bit, s));
-  void* t = g_scratch.get(bytes);
-  GMCP_CUDA(cub::DeviceRadixSort::SortKeys(t, bytes, kin, kout, n, 0, end_bit, s));
-}
 
 int grid_for(int64_t n, int threads) {
   const int64_t b = (n + threads - 1) / threads;
