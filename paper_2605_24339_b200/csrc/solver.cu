@@ -116,7 +116,9 @@ __device__ __forceinline__ d3 row_mv(const Bcsr& A, int v, const double* __restr
 //   z = Minv r, beta = rz_new / rz.
 // scal: [0] rz [1] pq [2] alpha [3] beta [4] rr [5] bb
 
-constexpr int kRowLanes = 4;  // lanes per BCSR row in the SpMV (4 beats 2, 8, 16 on C3)
+// lanes per BCSR row in the SpMV: 4 for large systems (beats 2, 8, 16 on C3),
+// 8 below kSmallRows rows, where the iteration is latency-bound
+constexpr int kSmallRows = 32768;
 constexpr double kRegularization = 1e-8;  // SolverSettings::regularization (solver.hpp:40)
 
 // A_vj x for block k, read through the read-only path (either layout)
@@ -130,6 +132,7 @@ __device__ __forceinline__ d3 bmv_ro(const Bcsr& A, int64_t k, d3 p) {
 
 // y_v = sum_j A_vj (z_j + beta p_j) over one row by kRowLanes lanes, two
 // blocks in flight per lane (fixed order: deterministic)
+template <int kRowLanes>
 __device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __restrict__ z,
                                       const double* __restrict__ p, double beta, int sub) {
   d3 acc0 = mk3(0, 0, 0), acc1 = mk3(0, 0, 0);
@@ -150,6 +153,7 @@ __device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __rest
 }
 
 // K9a: p_new = z + beta p_old (own rows), q = mask .* (H p_new), pq -> alpha (last block).
+template <int kRowLanes>
 __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const double* __restrict__ mask,
                                                       const double* __restrict__ z, const double* __restrict__ p_old,
                                                       double* __restrict__ p_new, double* __restrict__ q,
@@ -164,8 +168,8 @@ __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const do
     const int v = v0 + (lane / kRowLanes);
     d3 acc = mk3(0, 0, 0);
     if (v < nv) {
-      acc = row_mv8(M.el, v, z, p_old, beta, sub);
-      for (int k = 0; k < M.np; ++k) acc = acc + row_mv8(M.c[k], v, z, p_old, beta, sub);
+      acc = row_mv8<kRowLanes>(M.el, v, z, p_old, beta, sub);
+      for (int k = 0; k < M.np; ++k) acc = acc + row_mv8<kRowLanes>(M.c[k], v, z, p_old, beta, sub);
     }
 #pragma unroll
     for (int o = kRowLanes / 2; o > 0; o >>= 1) {
@@ -774,7 +778,8 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   }
   const double target = tol * tol * bb;
   const int chunk = 16;
-  const int gsp = std::min(grid_for((int64_t)nv * kRowLanes, kThreads), kBlocks);
+  const int lanes = nv < kSmallRows ? 8 : 4;
+  const int gsp = std::min(grid_for((int64_t)nv * lanes, kThreads), kBlocks);
   const int gup = std::min(grid_for((int64_t)nv, kThreads), kBlocks);  // one vertex per thread
   // one chunk of iterations as a CUDA graph (pointers fixed for this solve)
   cudaGraph_t graph;
@@ -783,7 +788,10 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   for (int k = 0; k < chunk; ++k) {  // p ping-pongs between S.p and S.w (chunk is even)
     double* p_old = (k & 1) ? S.w.p : S.p.p;
     double* p_new = (k & 1) ? S.p.p : S.w.p;
-    k_spmv_cg<<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p, S.slot(1));
+    if (lanes == 8)
+      k_spmv_cg<8><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p, S.slot(1));
+    else
+      k_spmv_cg<4><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p, S.slot(1));
     k_update_cg<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
                                                     S.slot(2));
   }
