@@ -1,6 +1,8 @@
 // Device context behind gmcp_ctx (include/gmcp_b200.h).
 #pragma once
 
+#include <memory>
+
 #include "common.cuh"
 
 namespace gmcp_b200 {
@@ -31,7 +33,6 @@ struct AssemblyPlan {
   int64_t nnzb = 0;
   DBuf<int32_t> rowptr;      // [N+1]
   DBuf<int32_t> cols;        // [nnzb]
-  std::vector<int32_t> h_rowptr, h_cols;  // host mirror of the pattern (System's merged matrix)
   // device planner scratch (plan.cu), reused across rebuilds
   struct Tmp {
     DBuf<int32_t> head, hscan, run_cnt, run_first, run_M, rowcnt, ucnt, nuniq;
@@ -46,8 +47,14 @@ struct AssemblyPlan {
   bool valid = false;
 };
 
+// Base of per-context scratch defined next to the code that uses it.
+struct TmpBase {
+  virtual ~TmpBase() = default;
+};
+
 struct Ctx {
   int device = 0;
+  std::unique_ptr<TmpBase> rebuild_tmp;  // broadphase + sampler scratch (sampler.cu)
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   int64_t n_dof = 0;

@@ -354,11 +354,6 @@ void build_assembly_plan(Ctx& c) {
   if (nc > 0) GMCP_CUDA(cudaMemcpyAsync(P.contrib.p, T.cval2.p, nc * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   if (ne > 0) GMCP_CUDA(cudaMemcpyAsync(P.row_ent.p, T.eval2.p, ne * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   P.vals.resize(std::max<int64_t>(9 * nnzb, 1));
-  // host mirror of the pattern (the System's merged Newton matrix is built from it)
-  P.h_rowptr.resize(N + 1);
-  P.h_cols.resize(nnzb);
-  P.rowptr.download(P.h_rowptr.data(), N + 1, s);
-  P.cols.download(P.h_cols.data(), nnzb, s);
   c.sync();
   GMCP_CUDA(cudaGetLastError());
   P.valid = true;

@@ -810,11 +810,36 @@ int64_t last_of(const DBuf<int64_t>& a, int64_t idx, cudaStream_t s) {
   return v;
 }
 
+// Broadphase + sampler scratch kept per context across rebuilds (grow-only:
+// no cudaMalloc / cudaFree on the rebuild path after the first one).
+struct RebuildTmp : TmpBase {
+  DBuf<Box> tboxes, nodes;
+  DBuf<unsigned long long> bounds, keys, keys_sorted;
+  DBuf<int32_t> idx, idx_sorted, left, right, parent, flags;
+  DBuf<int2> srange;
+  DBuf<int64_t> cnt;
+  DBuf<int> ovf;
+  DBuf<int32_t> tmp_e, tmp_v;
+  DBuf<int64_t> ecnt, vcnt;
+  DBuf<unsigned long long> err;
+  DBuf<unsigned long long> k1, k2;
+  DBuf<int64_t> by_off, pcnt, poff, pt_off;
+  DBuf<int32_t> by_st, pt_ids;
+  DBuf<int32_t> task_st, task_feat;
+  DBuf<int8_t> task_kind;
+  DBuf<int64_t> tcnt, toff;
+};
+RebuildTmp& rebuild_tmp(Ctx& c) {
+  if (!c.rebuild_tmp) c.rebuild_tmp = std::make_unique<RebuildTmp>();
+  return *static_cast<RebuildTmp*>(c.rebuild_tmp.get());
+}
+
 }  // namespace
 
 // ===========================================================================
 
 void run_broadphase(Ctx& c, double r, int64_t* counts) {
+  RebuildTmp& RT = rebuild_tmp(c);
   cudaStream_t s = c.stream;
   // self-contact check (contact_sampling.hpp:286-294), host mirrors are sorted
   {
@@ -841,9 +866,17 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
     return;
   }
   // K1: boxes, Morton keys, sort, hierarchy, refit
-  DBuf<Box> tboxes, nodes;
-  DBuf<unsigned long long> bounds, keys, keys_sorted;
-  DBuf<int32_t> idx, idx_sorted, left, right, parent, flags;
+  auto& tboxes = RT.tboxes;
+  auto& nodes = RT.nodes;
+  auto& bounds = RT.bounds;
+  auto& keys = RT.keys;
+  auto& keys_sorted = RT.keys_sorted;
+  auto& idx = RT.idx;
+  auto& idx_sorted = RT.idx_sorted;
+  auto& left = RT.left;
+  auto& right = RT.right;
+  auto& parent = RT.parent;
+  auto& flags = RT.flags;
   tboxes.resize(nmt);
   bounds.resize(6);
   const unsigned long long binit[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
@@ -875,14 +908,14 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   flags.zero(s);
   GMCP_CUDA(cudaMemsetAsync(parent.p, 0xff, nnodes * sizeof(int32_t), s));
   if (nmt > 1) k_karras<<<grid_for(nmt - 1, 256), 256, 0, s>>>(nmt, keys_sorted.p, left.p, right.p, parent.p);
-  DBuf<int2> srange;
+  auto& srange = RT.srange;
   if (vsc) srange.resize(nnodes);
   k_refit<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, idx_sorted.p, tboxes.p, left.p, right.p, parent.p, nodes.p, flags.p,
                                              c.master.tris.p, vsc, srange.p);
   c.launches += 3 + (nmt > 1 ? 1 : 0) + 2;
   // K2: count, scan, emit+sort
-  DBuf<int64_t> cnt;
-  DBuf<int> ovf;
+  auto& cnt = RT.cnt;
+  auto& ovf = RT.ovf;
   cnt.resize(nst + 1);
   cnt.zero(s);
   ovf.resize(1);
@@ -897,8 +930,10 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
                                                  srange.p);
   c.pair_ids[0].n = ntri;
   // K3: candidate edges / verts
-  DBuf<int32_t> tmp_e, tmp_v;
-  DBuf<int64_t> ecnt, vcnt;
+  auto& tmp_e = RT.tmp_e;
+  auto& tmp_v = RT.tmp_v;
+  auto& ecnt = RT.ecnt;
+  auto& vcnt = RT.vcnt;
   tmp_e.resize(std::max<int64_t>(3 * ntri, 1));
   tmp_v.resize(std::max<int64_t>(3 * ntri, 1));
   ecnt.resize(nst + 1);
@@ -930,6 +965,7 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
 }
 
 int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
+  RebuildTmp& RT = rebuild_tmp(c);
   cudaStream_t s = c.stream;
   const int32_t nst = c.slave.n_tris, nmv = c.master.n_verts;
   SamplerArgs A;
@@ -941,15 +977,20 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
   A.medges = c.master.edges.p;
   A.mverts = c.master.verts.p;
   A.P = c.params;
-  DBuf<unsigned long long> err;
+  auto& err = RT.err;
   err.resize(1);
   GMCP_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
 
   // K4: inverse lists mv -> slave tris (ascending st), ownership, regroup by st
   const int64_t nvc = (int64_t)c.pair_ids[2].n;
-  DBuf<unsigned long long> k1, k2;
-  DBuf<int64_t> by_off, pcnt, poff, pt_off;
-  DBuf<int32_t> by_st, pt_ids;
+  auto& k1 = RT.k1;
+  auto& k2 = RT.k2;
+  auto& by_off = RT.by_off;
+  auto& pcnt = RT.pcnt;
+  auto& poff = RT.poff;
+  auto& pt_off = RT.pt_off;
+  auto& by_st = RT.by_st;
+  auto& pt_ids = RT.pt_ids;
   by_off.resize(nmv + 1);
   by_st.resize(std::max<int64_t>(nvc, 1));
   if (nvc) {
@@ -987,9 +1028,11 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
   }
   // K5: tasks in reference order, count -> scan -> emit
   const int64_t ntask = (int64_t)c.pair_ids[0].n + (int64_t)c.pair_ids[1].n + npts;
-  DBuf<int32_t> task_st, task_feat;
-  DBuf<int8_t> task_kind;
-  DBuf<int64_t> tcnt, toff;
+  auto& task_st = RT.task_st;
+  auto& task_feat = RT.task_feat;
+  auto& task_kind = RT.task_kind;
+  auto& tcnt = RT.tcnt;
+  auto& toff = RT.toff;
   task_st.resize(std::max<int64_t>(ntask, 1));
   task_feat.resize(std::max<int64_t>(ntask, 1));
   task_kind.resize(std::max<int64_t>(ntask, 1));

@@ -15,6 +15,7 @@
 #include "../../include/gmcp_solver.h"
 #include "ctx.hpp"
 #include "kin.cuh"
+#include "cubutil.cuh"
 
 namespace gmcp_b200 {
 
@@ -489,7 +490,6 @@ struct SystemImpl {
   DBuf<unsigned long long> redu;
   DBuf<int32_t> k_rowptr, k_cols;
   DBuf<double> k_vals;
-  std::vector<int32_t> h_krowptr, h_kcols;
   // merged Newton matrix H = K_el + sum_pairs K_c on the union pattern (PCG operand);
   // u_src[(1 + np) * k + s]: block index of union block k in the elastic (s = 0) /
   // pair s-1 matrix, or -1. Pattern rebuilt when a pair is re-sampled.
@@ -497,6 +497,11 @@ struct SystemImpl {
   DBuf<double> u_vals;
   int64_t u_nnzb = 0;
   bool u_valid = false;
+  struct UnionTmp {  // build_union scratch, reused across rebuilds
+    DBuf<unsigned long long> keys, keys2, ukeys;
+    DBuf<int64_t> vals, vals2;
+    DBuf<int32_t> ucnt, uoff, nuniq, rowcnt;
+  } utmp;
   DBuf<const double*> gc_ptrs;
   bool el_built = false;
   int64_t el_nnzb = 0;
@@ -603,8 +608,6 @@ void build_elastic(SystemImpl& S) {
     rowptr[v + 1] = (int32_t)cols.size();
   }
   S.k_rowptr.upload(rowptr, S.stream);
-  S.h_krowptr = rowptr;
-  S.h_kcols = cols;
   S.k_cols.upload(cols, S.stream);
   S.k_vals.upload(vals, S.stream);
   S.el_nnzb = (int64_t)cols.size();
@@ -628,38 +631,90 @@ MatSet mats(SystemImpl& S) {
   return M;
 }
 
-// Union pattern of the elastic and every pair's contact BCSR (host, per rebuild).
-void build_union(SystemImpl& S) {
-  const int nv = S.nv(), np = (int)S.pairs.size();
-  std::vector<int32_t> rowptr(nv + 1, 0), cols, src;
-  struct E {
-    int32_t col, source, idx;
-  };
-  std::vector<E> row;
-  for (int v = 0; v < nv; ++v) {
-    row.clear();
-    for (int k = S.h_krowptr[v]; k < S.h_krowptr[v + 1]; ++k) row.push_back({S.h_kcols[k], 0, k});
-    for (int p = 0; p < np; ++p) {
-      const AssemblyPlan& P = S.pairs[p]->c->plan;
-      for (int k = P.h_rowptr[v]; k < P.h_rowptr[v + 1]; ++k) row.push_back({P.h_cols[k], 1 + p, k});
+// Union pattern of the elastic and every pair's contact BCSR, on the device
+// (per rebuild): every block of every source is emitted as ((row, col) key,
+// source << 32 | block) in source order, stably radix-sorted by key and
+// run-length encoded; u_src then lists each union block's source blocks.
+__global__ void k_union_emit(int nv, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                             int64_t source, int64_t base, unsigned long long* __restrict__ keys,
+                             int64_t* __restrict__ vals) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x)
+    for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
+      keys[base + k] = ((unsigned long long)(uint32_t)v << 32) | (unsigned long long)(uint32_t)cols[k];
+      vals[base + k] = (source << 32) | k;
     }
-    std::sort(row.begin(), row.end(), [](const E& a, const E& b) {
-      return a.col != b.col ? a.col < b.col : a.source < b.source;
-    });
-    for (size_t q = 0; q < row.size(); ++q) {
-      if (q == 0 || row[q].col != row[q - 1].col) {
-        cols.push_back(row[q].col);
-        src.insert(src.end(), 1 + np, -1);
-      }
-      src[src.size() - (1 + np) + row[q].source] = row[q].idx;
-    }
-    rowptr[v + 1] = (int32_t)cols.size();
+}
+__global__ void k_union_fill(int64_t nu, int ns, const unsigned long long* __restrict__ ukeys,
+                             const int32_t* __restrict__ uoff, const int32_t* __restrict__ ucnt,
+                             const int64_t* __restrict__ vals, int32_t* __restrict__ ucols, int32_t* __restrict__ src,
+                             int32_t* __restrict__ rowcnt) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nu; k += (int64_t)gridDim.x * blockDim.x) {
+    ucols[k] = (int32_t)(ukeys[k] & 0xffffffffull);
+    atomicAdd(&rowcnt[(int64_t)(ukeys[k] >> 32)], 1);  // integer counts: order-free
+    for (int e = uoff[k]; e < uoff[k] + ucnt[k]; ++e)
+      src[(int64_t)ns * k + (vals[e] >> 32)] = (int32_t)(vals[e] & 0xffffffffll);
   }
-  S.u_rowptr.upload(rowptr, S.stream);
-  S.u_cols.upload(cols, S.stream);
-  S.u_src.upload(src, S.stream);
-  S.u_nnzb = (int64_t)cols.size();
+}
+
+void build_union(SystemImpl& S) {
+  const int nv = S.nv(), np = (int)S.pairs.size(), ns = 1 + np;
+  std::vector<const int32_t*> rp{S.k_rowptr.p}, cl{S.k_cols.p};
+  std::vector<int64_t> nb{S.el_nnzb};
+  for (auto& pr : S.pairs) {
+    rp.push_back(pr->c->plan.rowptr.p);
+    cl.push_back(pr->c->plan.cols.p);
+    nb.push_back(pr->c->plan.nnzb);
+  }
+  int64_t total = 0;
+  for (int64_t v : nb) total += v;
+  auto& T = S.utmp;
+  auto& keys = T.keys;
+  auto& keys2 = T.keys2;
+  auto& ukeys = T.ukeys;
+  auto& vals = T.vals;
+  auto& vals2 = T.vals2;
+  auto& ucnt = T.ucnt;
+  auto& uoff = T.uoff;
+  auto& nuniq = T.nuniq;
+  auto& rowcnt = T.rowcnt;
+  keys.resize(std::max<int64_t>(total, 1));
+  keys2.resize(std::max<int64_t>(total, 1));
+  ukeys.resize(std::max<int64_t>(total, 1));
+  vals.resize(std::max<int64_t>(total, 1));
+  vals2.resize(std::max<int64_t>(total, 1));
+  ucnt.resize(total + 1);
+  uoff.resize(total + 1);
+  nuniq.resize(1);
+  int64_t base = 0;
+  for (int q = 0; q < ns; ++q) {
+    if (nb[q]) {
+      k_union_emit<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, rp[q], cl[q], q, base, keys.p, vals.p);
+      ++S.launches;
+    }
+    base += nb[q];
+  }
+  int rb = 1;
+  while ((1ll << rb) < nv) ++rb;
+  sort_pairs(keys.p, keys2.p, vals.p, vals2.p, total, S.stream, 32 + rb);
+  run_length_encode(keys2.p, ukeys.p, ucnt.p, nuniq.p, total, S.stream);
+  int32_t nu = 0;
+  GMCP_CUDA(cudaMemcpyAsync(&nu, nuniq.p, sizeof nu, cudaMemcpyDeviceToHost, S.stream));
+  S.sync();
+  GMCP_CUDA(cudaMemsetAsync(ucnt.p + nu, 0, sizeof(int32_t), S.stream));
+  exclusive_scan(ucnt.p, uoff.p, (int64_t)nu + 1, S.stream);
+  S.u_nnzb = nu;
+  S.u_cols.resize(std::max<int64_t>(nu, 1));
+  S.u_src.resize(std::max<int64_t>((int64_t)ns * nu, 1));
+  GMCP_CUDA(cudaMemsetAsync(S.u_src.p, 0xff, std::max<int64_t>((int64_t)ns * nu, 1) * sizeof(int32_t), S.stream));
+  rowcnt.resize(nv + 1);
+  rowcnt.zero(S.stream);
+  k_union_fill<<<grid_for(nu, 256), 256, 0, S.stream>>>(nu, ns, ukeys.p, uoff.p, ucnt.p, vals2.p, S.u_cols.p, S.u_src.p,
+                                                        rowcnt.p);
+  ++S.launches;
+  S.u_rowptr.resize(nv + 1);
+  exclusive_scan(rowcnt.p, S.u_rowptr.p, (int64_t)nv + 1, S.stream);
   S.u_vals.resize(std::max<int64_t>(9 * S.u_nnzb, 1));
+  S.sync();
   S.u_valid = true;
 }
 
