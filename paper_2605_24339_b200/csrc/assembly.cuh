@@ -78,6 +78,7 @@ __global__ void k_derive(int64_t n, const int8_t* __restrict__ type, const doubl
 // bitwise reproducible.
 
 constexpr int kUC = 16;               // U' / V columns
+
 constexpr int kRunWarps = 4;          // warps (= runs in flight) per K7 block
 #ifndef K7_MINB
 #define K7_MINB 4
@@ -202,7 +203,11 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
       }
     }
     __syncwarp();
-    double d00 = 0, d01 = 0, d10 = 0, d11 = 0, d20 = 0, d21 = 0, d30 = 0, d31 = 0;
+    // C quadrants [rows 0-7 | 8-15] x [cols 0-7 | 8-15]; the lower-left one
+    // (W_m>=2 / ones rows x b, r, W_0, W_1 columns) is never read -- its entries
+    // are read from the transposed upper-right quadrant -- so 3 DMMAs per step.
+    double d00 = 0, d01 = 0, d10 = 0, d11 = 0, d30 = 0, d31 = 0;
+
     for (int64_t base = s0; base < s1; base += 32) {
       const int64_t i = base + lane;
       const int rows = s1 - base < 32 ? (int)(s1 - base) : 32;
@@ -275,7 +280,6 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
           const double va = W.v[g][k], vb = W.v[8 + g][k];
           dmma(d00, d01, ua, va);
           dmma(d10, d11, ua, vb);
-          dmma(d20, d21, ub8, va);
           dmma(d30, d31, ub8, vb);
         }
       }
@@ -286,8 +290,6 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     C[g][2 * t4 + 1] = d01;
     C[g][8 + 2 * t4] = d10;
     C[g][9 + 2 * t4] = d11;
-    C[8 + g][2 * t4] = d20;
-    C[8 + g][2 * t4 + 1] = d21;
     C[8 + g][8 + 2 * t4] = d30;
     C[8 + g][9 + 2 * t4] = d31;
     __syncwarp();
@@ -353,7 +355,8 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
         } else {
           const int i = (q - 1) / 3, a = (q - 1) % 3;
           const double* Aia = A + 9 * i + 3 * a;
-          val = (-Cm[i]) * nn[a] + ((Aia[0] * Cm[3] + Aia[1] * Cm[4]) + Aia[2] * Cm[5]);
+          const int cm = 6 + m;  // Hwb / Hwr from the upper entries C[b_i][W_m], C[r_c][W_m]
+          val = (-C[i][cm]) * nn[a] + ((Aia[0] * C[3][cm] + Aia[1] * C[4][cm]) + Aia[2] * C[5][cm]);
         }
         P[m_base(M) + t] = val;
       }
