@@ -300,18 +300,28 @@ static int grad_common(gmcp_ctx* ctx, int mode, double* grad, double* energy, in
     Ctx& c = ctx->c;
     int64_t b = -1;
     if (bad) *bad = -1;
+    if (grad) {  // the caller's gradient travels up while the assembly runs
+      if (!c.aux) {
+        GMCP_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
+        GMCP_CUDA(cudaEventCreateWithFlags(&c.aux_done, cudaEventDisableTiming));
+      }
+      c.grad_in.resize(std::max<int64_t>(c.n_dof, 1));
+      GMCP_CUDA(cudaMemcpyAsync(c.grad_in.p, grad, c.n_dof * sizeof(double), cudaMemcpyHostToDevice, c.aux));
+      GMCP_CUDA(cudaEventRecord(c.aux_done, c.aux));
+    }
     try {
       const double e = run_assembly(c, mode, &b);
       if (energy) *energy = e;
     } catch (const StatusError& se) {
+      if (grad) GMCP_CUDA(cudaStreamSynchronize(c.aux));
       if (bad) *bad = se.bad;
       throw;
     }
-    if (grad) {  // accumulated into the caller's buffer (contact_energy.hpp:126-142)
-      double* g = c.stage((size_t)c.n_dof);
-      c.grad.download(g, c.n_dof, c.stream);
+    if (grad) {  // accumulated into the caller's buffer (contact_energy.hpp:126-142): grad += g_c
+      GMCP_CUDA(cudaStreamWaitEvent(c.stream, c.aux_done, 0));
+      add_into(c, c.grad_in.p, c.grad.p, c.n_dof);
+      c.grad_in.download(grad, c.n_dof, c.stream);
       c.sync();
-      for (int64_t i = 0; i < c.n_dof; ++i) grad[i] += g[i];
     }
     return GMCP_OK;
   });

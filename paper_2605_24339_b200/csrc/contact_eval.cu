@@ -100,6 +100,17 @@ void derive_sample_fields(Ctx& c) {
   c.plan.valid = false;
 }
 
+__global__ void k_add_into(int64_t n, double* __restrict__ dst, const double* __restrict__ src) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = dst[i] + src[i];
+}
+
+void add_into(Ctx& c, double* dst, const double* src, int64_t n) {
+  if (n <= 0) return;
+  k_add_into<<<grid_for(n, 256), 256, 0, c.stream>>>(n, dst, src);
+  ++c.launches;
+}
+
 double run_assembly(Ctx& c, int mode, int64_t* bad) {
   init_kernels();
   if (!c.plan.valid) build_assembly_plan(c);

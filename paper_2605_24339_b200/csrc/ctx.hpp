@@ -91,23 +91,17 @@ struct Ctx {
   DBuf<double> red_d;
   DBuf<unsigned long long> red_u;
 
-  // pinned host staging for downloads that are accumulated into caller buffers
-  double* h_stage = nullptr;
-  size_t h_stage_n = 0;
-  double* stage(size_t n) {
-    if (n > h_stage_n) {
-      if (h_stage) cudaFreeHost(h_stage);
-      h_stage = nullptr;
-      GMCP_CUDA(cudaMallocHost(&h_stage, std::max<size_t>(n, 1) * sizeof(double)));
-      h_stage_n = n;
-    }
-    return h_stage;
-  }
+  // accumulate-into-caller gradients: the caller's buffer is uploaded on an
+  // auxiliary stream while the assembly runs, summed on the device, downloaded once
+  cudaStream_t aux = nullptr;
+  cudaEvent_t aux_done = nullptr;
+  DBuf<double> grad_in;
   Ctx() = default;
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;
   ~Ctx() {
-    if (h_stage) cudaFreeHost(h_stage);
+    if (aux_done) cudaEventDestroy(aux_done);
+    if (aux) cudaStreamDestroy(aux);
   }
 
   DevSamples samples() const {
@@ -135,6 +129,7 @@ struct EnergyOut {
   int64_t first_bad, first_degenerate;
 };
 EnergyOut run_energy(Ctx& c, bool need_prefix_min);
+void add_into(Ctx& c, double* dst, const double* src, int64_t n);  // dst += src on c.stream
 void build_assembly_plan(Ctx& c);  // host-side plan from the device samples
 // mode 0: gradient only, 1: gradient + Hessian. Returns energy; throws on infeasible.
 double run_assembly(Ctx& c, int mode, int64_t* bad);
