@@ -111,6 +111,23 @@ int gmcp_kinematics(gmcp_ctx* ctx, double* g, int32_t* nv, int32_t* ids, double*
  * pass of the whole pass and of its dominant kernel. */
 int gmcp_time_assembly(gmcp_ctx* ctx, int reps, int flush_l2, double* ms_pass, double* ms_kernel);
 
+/* ---- dual-mesh embedding (embedding.hpp:26-106) ------------ */
+/* embed_in_surface: each point binds to the host triangle with the smallest
+ * point-triangle distance (lowest index on ties; LBVH branch and bound, equal
+ * to the reference's tree and brute-force results) and stores unclamped plane
+ * barycentrics (3 per point) and the signed offset along the triangle normal.
+ * host: n_host_vertices xyz, n_host_tris local-id triangles. A zero-area host
+ * triangle returns GMCP_ERR_DEGENERATE with *bad = its index. */
+int gmcp_embed_in_surface(gmcp_ctx* ctx, const double* points, int64_t n_points, const double* host_vertices,
+                          int64_t n_host_vertices, const int32_t* host_tris, int64_t n_host_tris, int32_t* tri,
+                          double* bary, double* offset, int64_t* bad);
+/* apply_embedding: reconstruct the embedded points from deformed host
+ * positions. A host triangle that degenerated returns GMCP_ERR_DEGENERATE
+ * with *bad = that triangle (of the first embedded point using it). */
+int gmcp_apply_embedding(gmcp_ctx* ctx, const int32_t* tri, const double* bary, const double* offset, int64_t n,
+                         const int32_t* host_tris, int64_t n_host_tris, const double* host_positions,
+                         int64_t n_host_vertices, double* out, int64_t* bad);
+
 #ifdef __cplusplus
 }
 #endif

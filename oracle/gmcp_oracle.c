@@ -1186,3 +1186,120 @@ int orc_time_assembly(const orc_state* S, const gmcp_barrier_params* P, const do
   *best_seconds = best;
   return GMCP_OK;
 }
+
+
+/* ------------------------------------------------------------------------ */
+/* embedding.hpp                                                             */
+
+/* geometry.hpp:26-34 */
+static int solve_barycentric_gram(v3 d, v3 e1, v3 e2, double* v, double* w) {
+  const double a11 = dot3(e1, e1), a12 = dot3(e1, e2), a22 = dot3(e2, e2);
+  const double b1 = dot3(d, e1), b2 = dot3(d, e2);
+  const double det = a11 * a22 - a12 * a12;
+  const double gram_eps = 1e-14 * a11 * a22;
+  if (!(det > gram_eps)) return set_err(GMCP_ERR_DEGENERATE, "solve_barycentric_gram: near-degenerate edge basis");
+  *v = (a22 * b1 - a12 * b2) / det;
+  *w = (a11 * b2 - a12 * b1) / det;
+  return GMCP_OK;
+}
+
+/* geometry.hpp:45-103: closest point on the closed triangle (Voronoi regions) */
+static v3 closest_point_on_triangle(v3 p, v3 a, v3 b, v3 c) {
+  const v3 ab = sub3(b, a), ac = sub3(c, a), ap = sub3(p, a);
+  const double d1 = dot3(ab, ap), d2 = dot3(ac, ap);
+  if (d1 <= 0 && d2 <= 0) return a;
+  const v3 bp = sub3(p, b);
+  const double d3 = dot3(ab, bp), d4 = dot3(ac, bp);
+  if (d3 >= 0 && d4 <= d3) return b;
+  const double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0 && d1 >= 0 && d3 <= 0) {
+    const double v = d1 / (d1 - d3);
+    return add3(a, scl3(v, ab));
+  }
+  const v3 cp = sub3(p, c);
+  const double d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+  if (d6 >= 0 && d5 <= d6) return c;
+  const double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) {
+    const double w = d2 / (d2 - d6);
+    return add3(a, scl3(w, ac));
+  }
+  const double va = d3 * d6 - d5 * d4;
+  if (va <= 0 && (d4 - d3) >= 0 && (d5 - d6) >= 0) {
+    const double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+    return add3(b, scl3(w, sub3(c, b)));
+  }
+  const double denom = 1.0 / ((va + vb) + vc);
+  const double v = vb * denom, w = vc * denom;
+  return add3(add3(a, scl3(v, ab)), scl3(w, ac));
+}
+
+/* embedding.hpp:26-84 (brute-force scan == the tree's result: min squared
+ * distance, lowest triangle index on exact ties) */
+int orc_embed_in_surface(const double* points, int64_t n_points, const double* host_v, int64_t n_hv,
+                         const int32_t* host_t, int64_t n_ht, int32_t use_tree, int32_t* tri, double* bary,
+                         double* offset, int64_t* bad) {
+  (void)n_hv;
+  (void)use_tree;
+  *bad = -1;
+  if (n_ht <= 0) return set_err(GMCP_ERR_CONFIG, "embedding host has no triangles");
+  for (int64_t t = 0; t < n_ht; ++t) {
+    const v3 a = ld3(host_v, host_t[3 * t]), b = ld3(host_v, host_t[3 * t + 1]), c = ld3(host_v, host_t[3 * t + 2]);
+    if (!(nrm3(crs3(sub3(b, a), sub3(c, a))) > 0)) {
+      *bad = t;
+      return set_err(GMCP_ERR_DEGENERATE, "embedding host triangle is degenerate");
+    }
+  }
+  for (int64_t i = 0; i < n_points; ++i) {
+    const v3 p = ld3(points, i);
+    int64_t best = -1;
+    double best_d2 = DBL_MAX;
+    for (int64_t t = 0; t < n_ht; ++t) {
+      const v3 a = ld3(host_v, host_t[3 * t]), b = ld3(host_v, host_t[3 * t + 1]), c = ld3(host_v, host_t[3 * t + 2]);
+      v3 n;
+      if (triangle_normal(a, b, c, &n) != GMCP_OK) return GMCP_ERR_DEGENERATE;  /* closest_point_on_triangle */
+      const v3 q = sub3(closest_point_on_triangle(p, a, b, c), p);
+      const double d2 = dot3(q, q);
+      if (d2 < best_d2) {
+        best_d2 = d2;
+        best = t;
+      }
+    }
+    const v3 a = ld3(host_v, host_t[3 * best]), b = ld3(host_v, host_t[3 * best + 1]), c = ld3(host_v, host_t[3 * best + 2]);
+    v3 n;
+    if (triangle_normal(a, b, c, &n) != GMCP_OK) return GMCP_ERR_DEGENERATE;
+    const v3 d = sub3(p, a);
+    double v, w;
+    if (solve_barycentric_gram(d, sub3(b, a), sub3(c, a), &v, &w) != GMCP_OK) return GMCP_ERR_DEGENERATE;
+    tri[i] = (int32_t)best;
+    bary[3 * i] = (1.0 - v) - w;
+    bary[3 * i + 1] = v;
+    bary[3 * i + 2] = w;
+    offset[i] = dot3(n, d);
+  }
+  return GMCP_OK;
+}
+
+/* embedding.hpp:87-106 */
+int orc_apply_embedding(const int32_t* tri, const double* bary, const double* offset, int64_t n,
+                        const int32_t* host_t, int64_t n_ht, const double* host_x, int64_t n_hv, double* out,
+                        int64_t* bad) {
+  (void)n_ht;
+  (void)n_hv;
+  *bad = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t* t = host_t + 3 * (int64_t)tri[i];
+    const v3 v0 = ld3(host_x, t[0]), v1 = ld3(host_x, t[1]), v2 = ld3(host_x, t[2]);
+    v3 nn;
+    if (triangle_normal(v0, v1, v2, &nn) != GMCP_OK) {
+      *bad = tri[i];
+      return set_err(GMCP_ERR_DEGENERATE, "host triangle is degenerate in the deformed configuration");
+    }
+    const v3 r = add3(add3(add3(scl3(bary[3 * i], v0), scl3(bary[3 * i + 1], v1)), scl3(bary[3 * i + 2], v2)),
+                      scl3(offset[i], nn));
+    out[3 * i] = r.v[0];
+    out[3 * i + 1] = r.v[1];
+    out[3 * i + 2] = r.v[2];
+  }
+  return GMCP_OK;
+}

@@ -99,6 +99,21 @@ int orc_force_summary(const orc_state* st, const gmcp_barrier_params* p, const d
 int orc_time_assembly(const orc_state* st, const gmcp_barrier_params* p, const double* x, int32_t reps,
                       double* best_seconds, int64_t* n_triplets);
 
+/* ---- dual-mesh embedding (embedding.hpp) -------------------------------- */
+/* embedding.hpp:26-84: nearest host triangle per point (lowest index on ties),
+ * plane barycentrics and signed normal offset. host: n_hv vertices (3 doubles
+ * each), n_ht triangles (local ids). use_tree selects the reference's AABB
+ * tree (reference library only; the restatement always scans). On a
+ * degenerate host triangle returns GMCP_ERR_DEGENERATE with *bad = index. */
+int orc_embed_in_surface(const double* points, int64_t n_points, const double* host_v, int64_t n_hv,
+                         const int32_t* host_t, int64_t n_ht, int32_t use_tree, int32_t* tri, double* bary,
+                         double* offset, int64_t* bad);
+/* embedding.hpp:87-106: reconstruct; GMCP_ERR_DEGENERATE with *bad = host
+ * triangle of the first embedded vertex whose triangle degenerated. */
+int orc_apply_embedding(const int32_t* tri, const double* bary, const double* offset, int64_t n,
+                        const int32_t* host_t, int64_t n_ht, const double* host_x, int64_t n_hv, double* out,
+                        int64_t* bad);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,6 +123,35 @@ class Oracle:
         self._check(self.lib.orc_barrier(C.c_double(g), C.c_double(eps), out.ctypes.data_as(C.c_void_p)))
         return out
 
+    # -- dual-mesh embedding (embedding.hpp) -----------------------------
+    def embed_in_surface(self, points, host_v, host_t, use_tree=True):
+        P = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        V = np.ascontiguousarray(host_v, np.float64).reshape(-1, 3)
+        T = np.ascontiguousarray(host_t, np.int32).reshape(-1, 3)
+        n = P.shape[0]
+        tri, bary, off = np.zeros(n, np.int32), np.zeros((n, 3)), np.zeros(n)
+        bad = C.c_int64(-1)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        rc = self.lib.orc_embed_in_surface(p(P), C.c_int64(n), p(V), C.c_int64(V.shape[0]), p(T),
+                                           C.c_int64(T.shape[0]), C.c_int32(int(use_tree)), p(tri), p(bary),
+                                           p(off), C.byref(bad))
+        self._check(rc, bad.value)
+        return tri, bary, off
+
+    def apply_embedding(self, tri, bary, off, host_t, host_x):
+        tri = np.ascontiguousarray(tri, np.int32)
+        bary = np.ascontiguousarray(bary, np.float64).reshape(-1, 3)
+        off = np.ascontiguousarray(off, np.float64)
+        T = np.ascontiguousarray(host_t, np.int32).reshape(-1, 3)
+        X = np.ascontiguousarray(host_x, np.float64).reshape(-1, 3)
+        out = np.zeros((tri.size, 3))
+        bad = C.c_int64(-1)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        rc = self.lib.orc_apply_embedding(p(tri), p(bary), p(off), C.c_int64(tri.size), p(T), C.c_int64(T.shape[0]),
+                                          p(X), C.c_int64(X.shape[0]), p(out), C.byref(bad))
+        self._check(rc, bad.value)
+        return out
+
     # -- broadphase ------------------------------------------------------
     def candidate_pairs(self, slave, master, x, r: float, use_tree: bool = True):
         s, ka = surface_struct(slave)

@@ -5,6 +5,7 @@
 // verbatim, plus ref_* helpers (meshes, scene solves) used to pin the Python
 // scene generators and to time the reference CPU path.
 #include "gmcp/bench.hpp"
+#include "gmcp/embedding.hpp"
 
 #include <chrono>
 #include <cstring>
@@ -661,6 +662,73 @@ int ref_write_formats(const char* dir, const double* pts, int64_t np, const int3
     rep.set("x", 1.0 / 3.0);
     rep.set("threads", 1);
     rep.save(d + "/report.txt");
+    return GMCP_OK;
+  });
+}
+
+// embedding.hpp:26-106 (the reference's own functions)
+static SurfaceMesh host_mesh(const double* host_v, int64_t n_hv, const int32_t* host_t, int64_t n_ht) {
+  SurfaceMesh h;
+  h.vertices.resize(n_hv);
+  for (int64_t v = 0; v < n_hv; ++v) h.vertices[v] = Vec3(host_v[3 * v], host_v[3 * v + 1], host_v[3 * v + 2]);
+  h.triangles.resize(n_ht);
+  for (int64_t t = 0; t < n_ht; ++t)
+    for (int k = 0; k < 3; ++k) h.triangles[t][k] = host_t[3 * t + k];
+  return h;
+}
+
+int orc_embed_in_surface(const double* points, int64_t n_points, const double* host_v, int64_t n_hv,
+                         const int32_t* host_t, int64_t n_ht, int32_t use_tree, int32_t* tri, double* bary,
+                         double* offset, int64_t* bad) {
+  *bad = -1;
+  const SurfaceMesh h = host_mesh(host_v, n_hv, host_t, n_ht);
+  for (int64_t t = 0; t < n_ht; ++t) {  // the index the reference's message names
+    const auto& tr = h.triangles[t];
+    if (!((h.vertices[tr[1]] - h.vertices[tr[0]]).cross(h.vertices[tr[2]] - h.vertices[tr[0]]).norm() > 0)) {
+      *bad = t;
+      break;
+    }
+  }
+  return guarded([&] {
+    std::vector<Vec3> pts(n_points);
+    for (int64_t i = 0; i < n_points; ++i) pts[i] = Vec3(points[3 * i], points[3 * i + 1], points[3 * i + 2]);
+    const SurfaceEmbedding e = embed_in_surface(pts, h, use_tree != 0);
+    for (int64_t i = 0; i < n_points; ++i) {
+      tri[i] = e[i].tri;
+      for (int k = 0; k < 3; ++k) bary[3 * i + k] = e[i].bary[k];
+      offset[i] = e[i].offset;
+    }
+    return GMCP_OK;
+  });
+}
+
+int orc_apply_embedding(const int32_t* tri, const double* bary, const double* offset, int64_t n,
+                        const int32_t* host_t, int64_t n_ht, const double* host_x, int64_t n_hv, double* out,
+                        int64_t* bad) {
+  *bad = -1;
+  SurfaceEmbedding e(n);
+  for (int64_t i = 0; i < n; ++i) {
+    e[i].tri = tri[i];
+    e[i].bary = Vec3(bary[3 * i], bary[3 * i + 1], bary[3 * i + 2]);
+    e[i].offset = offset[i];
+  }
+  std::vector<std::array<int, 3>> ht(n_ht);
+  for (int64_t t = 0; t < n_ht; ++t)
+    for (int k = 0; k < 3; ++k) ht[t][k] = host_t[3 * t + k];
+  std::vector<Vec3> hx(n_hv);
+  for (int64_t v = 0; v < n_hv; ++v) hx[v] = Vec3(host_x[3 * v], host_x[3 * v + 1], host_x[3 * v + 2]);
+  return guarded([&] {
+    std::vector<Vec3> r;
+    try {
+      r = apply_embedding(e, ht, hx);
+    } catch (const MeshError& me) {
+      const std::string m = me.what();  // "host triangle <t> is degenerate ..."
+      const auto p = m.find("host triangle ");
+      if (p != std::string::npos) *bad = std::atoll(m.c_str() + p + 14);
+      throw;
+    }
+    for (int64_t i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k) out[3 * i + k] = r[i][k];
     return GMCP_OK;
   });
 }

@@ -455,4 +455,52 @@ int gmcp_time_assembly(gmcp_ctx* ctx, int reps, int flush_l2, double* ms_pass, d
   });
 }
 
+
+int gmcp_embed_in_surface(gmcp_ctx* ctx, const double* points, int64_t n_points, const double* host_vertices,
+                          int64_t n_host_vertices, const int32_t* host_tris, int64_t n_host_tris, int32_t* tri,
+                          double* bary, double* offset, int64_t* bad) {
+  return guarded([&] {
+    check_ctx(ctx);
+    need(n_points >= 0 && n_host_vertices >= 0 && n_host_tris >= 0, "embedding: negative sizes");
+    need((points || !n_points) && host_vertices && host_tris && (tri || !n_points) && (bary || !n_points) &&
+             (offset || !n_points),
+         "embedding: null buffer");
+    for (int64_t k = 0; k < 3 * n_host_tris; ++k)
+      need(host_tris[k] >= 0 && host_tris[k] < n_host_vertices, "embedding: host triangle vertex out of range");
+    int64_t b = -1;
+    try {
+      run_embed(ctx->c, points, n_points, host_vertices, n_host_vertices, host_tris, n_host_tris, tri, bary, offset,
+                &b);
+    } catch (const StatusError&) {
+      if (bad) *bad = b;
+      throw;
+    }
+    if (bad) *bad = -1;
+    return GMCP_OK;
+  });
+}
+
+int gmcp_apply_embedding(gmcp_ctx* ctx, const int32_t* tri, const double* bary, const double* offset, int64_t n,
+                         const int32_t* host_tris, int64_t n_host_tris, const double* host_positions,
+                         int64_t n_host_vertices, double* out, int64_t* bad) {
+  return guarded([&] {
+    check_ctx(ctx);
+    need(n >= 0 && (tri || !n) && (bary || !n) && (offset || !n) && (out || !n) && host_tris && host_positions,
+         "apply_embedding: null buffer");
+    for (int64_t i = 0; i < n; ++i) need(tri[i] >= 0 && tri[i] < n_host_tris, "apply_embedding: triangle out of range");
+    for (int64_t k = 0; k < 3 * n_host_tris; ++k)
+      need(host_tris[k] >= 0 && host_tris[k] < n_host_vertices, "apply_embedding: host vertex out of range");
+    int64_t b = -1;
+    try {
+      run_apply_embedding(ctx->c, tri, bary, offset, n, host_tris, n_host_tris, host_positions, n_host_vertices,
+                          out, &b);
+    } catch (const StatusError&) {
+      if (bad) *bad = b;
+      throw;
+    }
+    if (bad) *bad = -1;
+    return GMCP_OK;
+  });
+}
+
 }  // extern "C"

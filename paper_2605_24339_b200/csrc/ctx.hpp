@@ -55,6 +55,7 @@ struct TmpBase {
 struct Ctx {
   int device = 0;
   std::unique_ptr<TmpBase> rebuild_tmp;  // broadphase + sampler scratch (sampler.cu)
+  std::unique_ptr<TmpBase> embed_tmp;    // dual-mesh embedding scratch (sampler.cu)
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   int64_t n_dof = 0;
@@ -142,5 +143,10 @@ double run_step_filter(Ctx& c);
 double run_displacement_cap(Ctx& c);
 void run_broadphase(Ctx& c, double r, int64_t* counts);
 int64_t run_sampler(Ctx& c, const double* eps_ref_dev);
+void run_embed(Ctx& c, const double* points, int64_t np, const double* host_v, int64_t nhv, const int32_t* host_t,
+               int64_t nht, int32_t* tri, double* bary, double* offset, int64_t* bad);
+void run_apply_embedding(Ctx& c, const int32_t* tri, const double* bary, const double* offset, int64_t n,
+                         const int32_t* host_t, int64_t nht, const double* host_x, int64_t nhv, double* out,
+                         int64_t* bad);
 
 }  // namespace gmcp_b200

@@ -810,13 +810,177 @@ int64_t last_of(const DBuf<int64_t>& a, int64_t idx, cudaStream_t s) {
   return v;
 }
 
-// Broadphase + sampler scratch kept per context across rebuilds (grow-only:
-// no cudaMalloc / cudaFree on the rebuild path after the first one).
-struct RebuildTmp : TmpBase {
+// ---------------------------------------------------------------------------
+// Dual-mesh embedding (embedding.hpp:26-106)
+
+// geometry.hpp:45-103: closest point on the closed triangle (Voronoi regions)
+__device__ __forceinline__ d3 closest_point_on_triangle(d3 p, d3 a, d3 b, d3 c) {
+  const d3 ab = b - a, ac = c - a, ap = p - a;
+  const double d1 = dot(ab, ap), d2 = dot(ac, ap);
+  if (d1 <= 0 && d2 <= 0) return a;
+  const d3 bp = p - b;
+  const double d3v = dot(ab, bp), d4 = dot(ac, bp);
+  if (d3v >= 0 && d4 <= d3v) return b;
+  const double vc = d1 * d4 - d3v * d2;
+  if (vc <= 0 && d1 >= 0 && d3v <= 0) return a + (d1 / (d1 - d3v)) * ab;
+  const d3 cp = p - c;
+  const double d5 = dot(ab, cp), d6 = dot(ac, cp);
+  if (d6 >= 0 && d5 <= d6) return c;
+  const double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) return a + (d2 / (d2 - d6)) * ac;
+  const double va = d3v * d6 - d5 * d4;
+  if (va <= 0 && (d4 - d3v) >= 0 && (d5 - d6) >= 0) return b + ((d4 - d3v) / ((d4 - d3v) + (d5 - d6))) * (c - b);
+  const double denom = 1.0 / ((va + vb) + vc);
+  const double v = vb * denom, w = vc * denom;
+  return (a + v * ab) + w * ac;
+}
+
+__device__ __forceinline__ double box_sq_dist(const Box& b, d3 p) {  // core.hpp:86-89
+  const double pv[3] = {p.x, p.y, p.z};
+  double s = 0;
+  for (int k = 0; k < 3; ++k) {
+    const double d = dmax(dmax(b.lo[k] - pv[k], 0.0), pv[k] - b.hi[k]);
+    s = k == 0 ? d * d : s + d * d;
+  }
+  return s;
+}
+
+// host triangle checks: exact-zero area (embedding.hpp:30-35, by index) and
+// triangle_normal's area cutoff (closest_point_on_triangle would throw)
+__global__ void k_embed_check(int32_t nt, const int32_t* __restrict__ tris, const double* __restrict__ x,
+                              unsigned long long* bad) {
+  GRID_LOOP(t, nt) {
+    const d3 a = ld3(x, tris[3 * t]), b = ld3(x, tris[3 * t + 1]), c = ld3(x, tris[3 * t + 2]);
+    if (!(norm(cross(b - a, c - a)) > 0)) atomicMin(&bad[0], (unsigned long long)t);
+    d3 n;
+    if (!triangle_normal(a, b, c, n)) atomicMin(&bad[1], (unsigned long long)t);
+  }
+}
+
+// nearest host triangle (min squared distance, lowest index on ties) by LBVH
+// branch and bound, then plane barycentrics and the normal offset
+__global__ void k_embed(int64_t np, const double* __restrict__ pts, int32_t nt, const int32_t* __restrict__ tris,
+                        const double* __restrict__ x, const Box* __restrict__ nodes, const int32_t* __restrict__ left,
+                        const int32_t* __restrict__ right, const int32_t* __restrict__ sorted_idx,
+                        int32_t* __restrict__ tri_out, double* __restrict__ bary, double* __restrict__ offset,
+                        unsigned long long* bad) {
+  GRID_LOOP(i, np) {
+    const d3 p = ld3(pts, i);
+    int best = -1;
+    double best_d2 = kDblMax;
+    int stack[64];
+    int top = 0;
+    stack[top++] = 0;
+    while (top > 0) {
+      const int node = stack[--top];
+      // conservative prune: equal (or rounding-close) lower bounds are still
+      // visited so index ties break exactly as a full scan would
+      if (best >= 0 && box_sq_dist(nodes[node], p) > best_d2 * (1.0 + 1e-12) + 1e-300) continue;
+      if (node >= nt - 1) {
+        const int t = sorted_idx[node - (nt - 1)];
+        const d3 a = ld3(x, tris[3 * t]), b = ld3(x, tris[3 * t + 1]), c = ld3(x, tris[3 * t + 2]);
+        const d3 q = closest_point_on_triangle(p, a, b, c) - p;
+        const double d2 = dot(q, q);
+        if (d2 < best_d2 || (d2 == best_d2 && t < best)) {
+          best_d2 = d2;
+          best = t;
+        }
+      } else {
+        if (top + 2 > 64) {
+          atomicExch(&bad[2], 1ull);
+          break;
+        }
+        stack[top++] = right[node];
+        stack[top++] = left[node];
+      }
+    }
+    const d3 a = ld3(x, tris[3 * best]), b = ld3(x, tris[3 * best + 1]), c = ld3(x, tris[3 * best + 2]);
+    d3 n;
+    triangle_normal(a, b, c, n);
+    const d3 d = p - a, e1 = b - a, e2 = c - a;
+    // geometry.hpp:26-34 solve_barycentric_gram
+    const double a11 = dot(e1, e1), a12 = dot(e1, e2), a22 = dot(e2, e2);
+    const double b1 = dot(d, e1), b2 = dot(d, e2);
+    const double det = a11 * a22 - a12 * a12;
+    if (!(det > 1e-14 * a11 * a22)) atomicMin(&bad[1], (unsigned long long)best);
+    const double v = (a22 * b1 - a12 * b2) / det, w = (a11 * b2 - a12 * b1) / det;
+    tri_out[i] = best;
+    bary[3 * i] = (1.0 - v) - w;
+    bary[3 * i + 1] = v;
+    bary[3 * i + 2] = w;
+    offset[i] = dot(n, d);
+  }
+}
+
+// embedding.hpp:87-106; bad = first embedded vertex whose host triangle degenerated
+__global__ void k_apply_embedding(int64_t n, const int32_t* __restrict__ tri, const double* __restrict__ bary,
+                                  const double* __restrict__ offset, const int32_t* __restrict__ tris,
+                                  const double* __restrict__ x, double* __restrict__ out, unsigned long long* bad) {
+  GRID_LOOP(i, n) {
+    const int32_t* t = tris + 3 * (int64_t)tri[i];
+    const d3 v0 = ld3(x, t[0]), v1 = ld3(x, t[1]), v2 = ld3(x, t[2]);
+    d3 nn;
+    if (!triangle_normal(v0, v1, v2, nn)) {
+      atomicMin(bad, (unsigned long long)i);
+      continue;
+    }
+    const d3 r = ((bary[3 * i] * v0 + bary[3 * i + 1] * v1) + bary[3 * i + 2] * v2) + offset[i] * nn;
+    out[3 * i] = r.x;
+    out[3 * i + 1] = r.y;
+    out[3 * i + 2] = r.z;
+  }
+}
+
+// LBVH over triangles (K1): boxes, Morton keys (+ scene id for batches),
+// radix sort, Karras hierarchy, bottom-up refit. Internal nodes 0..n-2,
+// leaves n-1..2n-2 (leaf k -> triangle idx_sorted[k]).
+struct Lbvh {
   DBuf<Box> tboxes, nodes;
   DBuf<unsigned long long> bounds, keys, keys_sorted;
   DBuf<int32_t> idx, idx_sorted, left, right, parent, flags;
-  DBuf<int2> srange;
+  DBuf<int2> srange;  // per-node [min, max] scene (batched scenes only)
+};
+
+int lbvh_build(Lbvh& B, int32_t n, const int32_t* tris, const double* x, const int32_t* vsc, int n_scenes,
+               cudaStream_t s) {
+  B.tboxes.resize(n);
+  B.bounds.resize(6);
+  const unsigned long long binit[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+  GMCP_CUDA(cudaMemcpyAsync(B.bounds.p, binit, sizeof binit, cudaMemcpyHostToDevice, s));
+  k_master_boxes<<<grid_for(n, 256), 256, 0, s>>>(n, tris, x, B.tboxes.p, B.bounds.p);
+  B.keys.resize(n);
+  B.keys_sorted.resize(n);
+  B.idx.resize(n);
+  B.idx_sorted.resize(n);
+  int ib = 32;  // index bits of the key; fewer when a scene id must fit above the Morton code
+  if (vsc) {
+    ib = 1;
+    while ((1ll << ib) < n) ++ib;
+    int sb = 1;
+    while ((1 << sb) < n_scenes) ++sb;
+    if (sb + 30 + ib > 64) throw StatusError(GMCP_ERR_CONFIG, "batched broadphase: too many scenes x triangles");
+  }
+  k_morton<<<grid_for(n, 256), 256, 0, s>>>(n, B.tboxes.p, B.bounds.p, tris, vsc, ib, B.keys.p, B.idx.p);
+  sort_pairs(B.keys.p, B.keys_sorted.p, B.idx.p, B.idx_sorted.p, n, s, 64);
+  const int nnodes = 2 * n - 1;
+  B.nodes.resize(nnodes);
+  B.left.resize(std::max(n - 1, 1));
+  B.right.resize(std::max(n - 1, 1));
+  B.parent.resize(nnodes);
+  B.flags.resize(std::max(n - 1, 1));
+  B.flags.zero(s);
+  GMCP_CUDA(cudaMemsetAsync(B.parent.p, 0xff, nnodes * sizeof(int32_t), s));
+  if (n > 1) k_karras<<<grid_for(n - 1, 256), 256, 0, s>>>(n, B.keys_sorted.p, B.left.p, B.right.p, B.parent.p);
+  if (vsc) B.srange.resize(nnodes);
+  k_refit<<<grid_for(n, 256), 256, 0, s>>>(n, B.idx_sorted.p, B.tboxes.p, B.left.p, B.right.p, B.parent.p, B.nodes.p,
+                                           B.flags.p, tris, vsc, B.srange.p);
+  return 3 + (n > 1 ? 1 : 0) + 2;
+}
+
+// Broadphase + sampler scratch kept per context across rebuilds (grow-only:
+// no cudaMalloc / cudaFree on the rebuild path after the first one).
+struct RebuildTmp : TmpBase {
+  Lbvh bvh;
   DBuf<int64_t> cnt;
   DBuf<int> ovf;
   DBuf<int32_t> tmp_e, tmp_v;
@@ -866,53 +1030,16 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
     return;
   }
   // K1: boxes, Morton keys, sort, hierarchy, refit
-  auto& tboxes = RT.tboxes;
-  auto& nodes = RT.nodes;
-  auto& bounds = RT.bounds;
-  auto& keys = RT.keys;
-  auto& keys_sorted = RT.keys_sorted;
-  auto& idx = RT.idx;
-  auto& idx_sorted = RT.idx_sorted;
-  auto& left = RT.left;
-  auto& right = RT.right;
-  auto& parent = RT.parent;
-  auto& flags = RT.flags;
-  tboxes.resize(nmt);
-  bounds.resize(6);
-  const unsigned long long binit[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
-  GMCP_CUDA(cudaMemcpyAsync(bounds.p, binit, sizeof binit, cudaMemcpyHostToDevice, s));
-  k_master_boxes<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, c.master.tris.p, c.X(), tboxes.p, bounds.p);
-  keys.resize(nmt);
-  keys_sorted.resize(nmt);
-  idx.resize(nmt);
-  idx_sorted.resize(nmt);
   const int32_t* vsc = c.vscene.n ? c.vscene.p : nullptr;
   if (vsc && (int64_t)c.vscene.n != c.n_vertices())
     throw StatusError(GMCP_ERR_CONFIG, "batched broadphase: vertex scene ids do not cover the positions");
-  int ib = 32;  // index bits of the key; fewer when a scene id must fit above the Morton code
-  if (vsc) {
-    ib = 1;
-    while ((1ll << ib) < nmt) ++ib;
-    int sb = 1;
-    while ((1 << sb) < c.n_scenes) ++sb;
-    if (sb + 30 + ib > 64) throw StatusError(GMCP_ERR_CONFIG, "batched broadphase: too many scenes x triangles");
-  }
-  k_morton<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, tboxes.p, bounds.p, c.master.tris.p, vsc, ib, keys.p, idx.p);
-  sort_pairs(keys.p, keys_sorted.p, idx.p, idx_sorted.p, nmt, s, 64);
-  const int nnodes = 2 * nmt - 1;
-  nodes.resize(nnodes);
-  left.resize(std::max(nmt - 1, 1));
-  right.resize(std::max(nmt - 1, 1));
-  parent.resize(nnodes);
-  flags.resize(std::max(nmt - 1, 1));
-  flags.zero(s);
-  GMCP_CUDA(cudaMemsetAsync(parent.p, 0xff, nnodes * sizeof(int32_t), s));
-  if (nmt > 1) k_karras<<<grid_for(nmt - 1, 256), 256, 0, s>>>(nmt, keys_sorted.p, left.p, right.p, parent.p);
-  auto& srange = RT.srange;
-  if (vsc) srange.resize(nnodes);
-  k_refit<<<grid_for(nmt, 256), 256, 0, s>>>(nmt, idx_sorted.p, tboxes.p, left.p, right.p, parent.p, nodes.p, flags.p,
-                                             c.master.tris.p, vsc, srange.p);
-  c.launches += 3 + (nmt > 1 ? 1 : 0) + 2;
+  Lbvh& B = RT.bvh;
+  c.launches += lbvh_build(B, nmt, c.master.tris.p, c.X(), vsc, c.n_scenes, s);
+  auto& nodes = B.nodes;
+  auto& left = B.left;
+  auto& right = B.right;
+  auto& idx_sorted = B.idx_sorted;
+  auto& srange = B.srange;
   // K2: count, scan, emit+sort
   auto& cnt = RT.cnt;
   auto& ovf = RT.ovf;
@@ -1076,6 +1203,95 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
   derive_sample_fields(c);
   c.sync();
   return n;
+}
+
+// ===========================================================================
+// embedding host entry points (embedding.hpp:26-106)
+
+struct EmbedTmp : TmpBase {
+  Lbvh bvh;
+  DBuf<double> pts, x, bary, off, out;
+  DBuf<int32_t> tris, tri;
+  DBuf<unsigned long long> bad;
+};
+static EmbedTmp& embed_tmp(Ctx& c) {
+  if (!c.embed_tmp) c.embed_tmp = std::make_unique<EmbedTmp>();
+  return *static_cast<EmbedTmp*>(c.embed_tmp.get());
+}
+
+void run_embed(Ctx& c, const double* points, int64_t np, const double* host_v, int64_t nhv, const int32_t* host_t,
+               int64_t nht, int32_t* tri, double* bary, double* offset, int64_t* bad) {
+  cudaStream_t s = c.stream;
+  *bad = -1;
+  if (nht <= 0) throw StatusError(GMCP_ERR_CONFIG, "embedding host has no triangles");
+  if (nht >= (int64_t)INT32_MAX / 2) throw StatusError(GMCP_ERR_CONFIG, "embedding host too large");
+  EmbedTmp& E = embed_tmp(c);
+  E.x.upload(host_v, 3 * nhv, s);
+  E.tris.upload(host_t, 3 * nht, s);
+  E.bad.resize(3);
+  const unsigned long long binit[3] = {~0ull, ~0ull, 0};
+  GMCP_CUDA(cudaMemcpyAsync(E.bad.p, binit, sizeof binit, cudaMemcpyHostToDevice, s));
+  const int32_t nt = (int32_t)nht;
+  k_embed_check<<<grid_for(nt, 256), 256, 0, s>>>(nt, E.tris.p, E.x.p, E.bad.p);
+  ++c.launches;
+  unsigned long long h[3];
+  GMCP_CUDA(cudaMemcpyAsync(h, E.bad.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  c.sync();
+  if (h[0] != ~0ull) {
+    *bad = (int64_t)h[0];
+    throw StatusError(GMCP_ERR_DEGENERATE, "embedding host triangle " + std::to_string(h[0]) + " is degenerate",
+                      (int64_t)h[0]);
+  }
+  if (h[1] != ~0ull)
+    throw StatusError(GMCP_ERR_DEGENERATE, "triangle_normal: degenerate triangle (area below cutoff)");
+  if (np == 0) return;
+  c.launches += lbvh_build(E.bvh, nt, E.tris.p, E.x.p, nullptr, 1, s);
+  E.pts.upload(points, 3 * np, s);
+  E.tri.resize(np);
+  E.bary.resize(3 * np);
+  E.off.resize(np);
+  k_embed<<<grid_for(np, 128), 128, 0, s>>>(np, E.pts.p, nt, E.tris.p, E.x.p, E.bvh.nodes.p, E.bvh.left.p,
+                                             E.bvh.right.p, E.bvh.idx_sorted.p, E.tri.p, E.bary.p, E.off.p, E.bad.p);
+  ++c.launches;
+  GMCP_CUDA(cudaGetLastError());
+  GMCP_CUDA(cudaMemcpyAsync(h, E.bad.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  E.tri.download(tri, np, s);
+  E.bary.download(bary, 3 * np, s);
+  E.off.download(offset, np, s);
+  c.sync();
+  if (h[2]) throw StatusError(GMCP_ERR_CONFIG, "embedding: BVH traversal stack overflow");
+  if (h[1] != ~0ull) throw StatusError(GMCP_ERR_DEGENERATE, "solve_barycentric_gram: near-degenerate edge basis");
+}
+
+void run_apply_embedding(Ctx& c, const int32_t* tri, const double* bary, const double* offset, int64_t n,
+                         const int32_t* host_t, int64_t nht, const double* host_x, int64_t nhv, double* out,
+                         int64_t* bad) {
+  cudaStream_t s = c.stream;
+  *bad = -1;
+  if (n == 0) return;
+  EmbedTmp& E = embed_tmp(c);
+  E.tris.upload(host_t, 3 * nht, s);
+  E.x.upload(host_x, 3 * nhv, s);
+  E.tri.upload(tri, n, s);
+  E.bary.upload(bary, 3 * n, s);
+  E.off.upload(offset, n, s);
+  E.out.resize(3 * n);
+  E.bad.resize(3);
+  GMCP_CUDA(cudaMemsetAsync(E.bad.p, 0xff, sizeof(unsigned long long), s));
+  k_apply_embedding<<<grid_for(n, 256), 256, 0, s>>>(n, E.tri.p, E.bary.p, E.off.p, E.tris.p, E.x.p, E.out.p,
+                                                      E.bad.p);
+  ++c.launches;
+  GMCP_CUDA(cudaGetLastError());
+  unsigned long long h = 0;
+  GMCP_CUDA(cudaMemcpyAsync(&h, E.bad.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  E.out.download(out, 3 * n, s);
+  c.sync();
+  if (h != ~0ull) {
+    *bad = tri[h];
+    throw StatusError(GMCP_ERR_DEGENERATE,
+                      "host triangle " + std::to_string(tri[h]) + " is degenerate in the deformed configuration",
+                      (int64_t)tri[h]);
+  }
 }
 
 }  // namespace gmcp_b200
