@@ -78,6 +78,17 @@ int gmcp_system_pair_force_summary(gmcp_system* sys, int32_t pair, double* out12
 int gmcp_system_pair_pressure(gmcp_system* sys, int32_t pair, int64_t* n, gmcp_pressure_record* out);
 int64_t gmcp_system_launch_count(const gmcp_system* sys);
 
+/* Batched independent scenes. scene[v] numbers the scenes
+ * 0, 1, ... over contiguous vertex ranges (no body spans two scenes); NULL
+ * clears. gmcp_system_solve then runs every scene with its own residual
+ * tolerance (derived from that scene's loads and bodies), step filter, cap,
+ * line search and convergence; the linear solve is one PCG over the active
+ * scenes. gmcp_run_stats.total_newton_iters then counts scene-Newton-
+ * iterations (sum over scenes); per-step newton_iters counts loop passes. */
+int gmcp_system_set_vertex_scenes(gmcp_system* sys, const int32_t* scene, int64_t n_vertices);
+/* Newton iterations per scene of the last batched solve (out[n_scenes]). */
+int gmcp_system_scene_newton_iters(const gmcp_system* sys, int64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

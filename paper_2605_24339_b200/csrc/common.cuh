@@ -74,6 +74,11 @@ struct DBuf {
   void zero(cudaStream_t s) {
     if (n) GMCP_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
   }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(cap, o.cap);
+  }
 };
 
 // ---------------------------------------------------------------------------

@@ -100,6 +100,46 @@ void derive_sample_fields(Ctx& c) {
   c.plan.valid = false;
 }
 
+struct SampleRefs {
+  int8_t* type;
+  int32_t *slave, *master;
+  double *beta_s, *beta_m, *eta, *weight, *gamma, *eps, *gref;
+};
+__device__ __forceinline__ void copy_sample(const SampleRefs& a, int64_t i, const SampleRefs& b, int64_t j) {
+  a.type[i] = b.type[j];
+  for (int k = 0; k < 3; ++k) {
+    a.slave[3 * i + k] = b.slave[3 * j + k];
+    a.master[3 * i + k] = b.master[3 * j + k];
+    a.beta_s[3 * i + k] = b.beta_s[3 * j + k];
+    a.beta_m[3 * i + k] = b.beta_m[3 * j + k];
+  }
+  a.eta[i] = b.eta[j];
+  a.weight[i] = b.weight[j];
+  a.gamma[i] = b.gamma[j];
+  a.eps[i] = b.eps[j];
+  a.gref[i] = b.gref[j];
+}
+__global__ void k_snapshot(int64_t n, SampleRefs dst, SampleRefs src) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    copy_sample(dst, i, src, i);
+}
+// out sample i of scene s (merged offsets moff) comes from the new arrays at
+// soff_new[s] + k or the snapshot at soff_old[s] + k
+__global__ void k_splice(int64_t n, int ns, const int64_t* __restrict__ moff, const int64_t* __restrict__ soff_old,
+                         const int64_t* __restrict__ soff_new, const uint8_t* __restrict__ take, SampleRefs out,
+                         SampleRefs fresh, SampleRefs old) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = ns;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (moff[mid] <= i) lo = mid; else hi = mid;
+    }
+    const int64_t k = i - moff[lo];
+    if (take[lo]) copy_sample(out, i, fresh, soff_new[lo] + k);
+    else copy_sample(out, i, old, soff_old[lo] + k);
+  }
+}
+
 __global__ void k_add_into(int64_t n, double* __restrict__ dst, const double* __restrict__ src) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = dst[i] + src[i];
@@ -109,6 +149,69 @@ void add_into(Ctx& c, double* dst, const double* src, int64_t n) {
   if (n <= 0) return;
   k_add_into<<<grid_for(n, 256), 256, 0, c.stream>>>(n, dst, src);
   ++c.launches;
+}
+
+static SampleRefs refs_of(Ctx& c) {
+  return SampleRefs{c.s_type.p, c.s_slave.p, c.s_master.p, c.s_beta_s.p, c.s_beta_m.p, c.s_eta.p,
+                    c.s_weight.p, c.s_gamma.p, c.s_eps.p, c.s_gref.p};
+}
+static SampleRefs refs_of(Ctx::Snapshot& a) {
+  return SampleRefs{a.type.p, a.slave.p, a.master.p, a.beta_s.p, a.beta_m.p, a.eta.p,
+                    a.weight.p, a.gamma.p, a.eps.p, a.gref.p};
+}
+static void size_snapshot(Ctx::Snapshot& a, int64_t n) {
+  const int64_t m = std::max<int64_t>(n, 1);
+  a.type.resize(m);
+  a.slave.resize(3 * m);
+  a.master.resize(3 * m);
+  a.beta_s.resize(3 * m);
+  a.beta_m.resize(3 * m);
+  for (auto* b : {&a.eta, &a.weight, &a.gamma, &a.eps, &a.gref}) b->resize(m);
+}
+
+void snapshot_samples(Ctx& c) {
+  size_snapshot(c.snap, c.ns);
+  c.snap.ns = c.ns;
+  if (c.ns) {
+    k_snapshot<<<grid_for(c.ns, 256), 256, 0, c.stream>>>(c.ns, refs_of(c.snap), refs_of(c));
+    ++c.launches;
+  }
+}
+
+void splice_samples(Ctx& c, const std::vector<int64_t>& soff_old, const std::vector<int64_t>& soff_new,
+                    const std::vector<uint8_t>& take_new, std::vector<int64_t>& soff_out) {
+  const int ns = (int)take_new.size();
+  soff_out.assign(ns + 1, 0);
+  for (int s = 0; s < ns; ++s)
+    soff_out[s + 1] = soff_out[s] + (take_new[s] ? soff_new[s + 1] - soff_new[s] : soff_old[s + 1] - soff_old[s]);
+  const int64_t n = soff_out[ns];
+  Ctx::Snapshot merged;
+  size_snapshot(merged, n);
+  DBuf<int64_t> moff, so, sn;
+  DBuf<uint8_t> take;
+  moff.upload(soff_out, c.stream);
+  so.upload(soff_old, c.stream);
+  sn.upload(soff_new, c.stream);
+  take.upload(take_new, c.stream);
+  if (n) {
+    k_splice<<<grid_for(n, 256), 256, 0, c.stream>>>(n, ns, moff.p, so.p, sn.p, take.p, refs_of(merged), refs_of(c),
+                                                      refs_of(c.snap));
+    ++c.launches;
+  }
+  // merged -> c's arrays
+  c.s_type.swap(merged.type);
+  c.s_slave.swap(merged.slave);
+  c.s_master.swap(merged.master);
+  c.s_beta_s.swap(merged.beta_s);
+  c.s_beta_m.swap(merged.beta_m);
+  c.s_eta.swap(merged.eta);
+  c.s_weight.swap(merged.weight);
+  c.s_gamma.swap(merged.gamma);
+  c.s_eps.swap(merged.eps);
+  c.s_gref.swap(merged.gref);
+  c.ns = n;
+  c.sync();  // merged (now the old buffers) is freed at scope exit
+  derive_sample_fields(c);
 }
 
 double run_assembly(Ctx& c, int mode, int64_t* bad) {

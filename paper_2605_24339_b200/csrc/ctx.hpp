@@ -56,6 +56,7 @@ struct Ctx {
   int device = 0;
   std::unique_ptr<TmpBase> rebuild_tmp;  // broadphase + sampler scratch (sampler.cu)
   std::unique_ptr<TmpBase> embed_tmp;    // dual-mesh embedding scratch (sampler.cu)
+  std::unique_ptr<TmpBase> scene_tmp;    // scene-segmented reductions scratch (exact.cu)
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   int64_t n_dof = 0;
@@ -87,6 +88,15 @@ struct Ctx {
   DBuf<int64_t> face_idx;  // indices of face samples (pressure field order)
 
   AssemblyPlan plan;
+
+  // snapshot of the raw sample fields (batched per-scene rebuilds splice old
+  // and new per-scene segments)
+  struct Snapshot {
+    int64_t ns = 0;
+    DBuf<int8_t> type;
+    DBuf<int32_t> slave, master;
+    DBuf<double> beta_s, beta_m, eta, weight, gamma, eps, gref;
+  } snap;
 
   // reduction scratch
   DBuf<double> red_d;
@@ -125,6 +135,11 @@ struct Ctx {
 // --- entry points implemented in the .cu files (all enqueue on ctx.stream) ---
 // contact_eval.cu
 void derive_sample_fields(Ctx& c);  // coef, wm, face_idx from the raw fields
+void snapshot_samples(Ctx& c);      // raw sample fields -> c.snap
+// per scene s: keep the snapshot's segment [soff_old[s], soff_old[s+1]) or take
+// the current (new) segment [soff_new[s], soff_new[s+1]); result in c's arrays
+void splice_samples(Ctx& c, const std::vector<int64_t>& soff_old, const std::vector<int64_t>& soff_new,
+                    const std::vector<uint8_t>& take_new, std::vector<int64_t>& soff_out);
 struct EnergyOut {
   double energy, min_gap, min_gap_prefix;
   int64_t first_bad, first_degenerate;
@@ -141,6 +156,14 @@ void time_assembly(Ctx& c, int reps, int flush_l2, double* ms_pass, double* ms_k
 // exact.cu (-fmad=false)
 double run_step_filter(Ctx& c);
 double run_displacement_cap(Ctx& c);
+// batched scenes (contiguous per scene): sample offsets per scene, per-scene
+// energy / feasibility, per-scene step size min(1, filter, cap)
+void scene_sample_offsets(Ctx& c, const int32_t* vscene_dev, int n_scenes, std::vector<int64_t>& soff_host,
+                          DBuf<int64_t>& soff_dev);
+void run_scene_energy(Ctx& c, const double* xp, int n_scenes, const int64_t* soff_dev, double* e,
+                      int64_t* first_bad, int64_t* first_deg, double* min_gap);
+void run_scene_alpha(Ctx& c, int n_scenes, const int64_t* soff_dev, const int64_t* voff_dev, double* alpha,
+                     int64_t* first_deg);
 void run_broadphase(Ctx& c, double r, int64_t* counts);
 int64_t run_sampler(Ctx& c, const double* eps_ref_dev);
 void run_embed(Ctx& c, const double* points, int64_t np, const double* host_v, int64_t nhv, const int32_t* host_t,

@@ -188,6 +188,115 @@ __global__ void k_max_move(int64_t nv, const double* __restrict__ dx, unsigned l
   if ((threadIdx.x & 31) == 0) atomicMax(&red[3], best);
 }
 
+// ---------------------------------------------------------------------------
+// Scene-segmented variants (batched scenes): one block per scene
+// over its contiguous sample range, per-sample arithmetic identical to K6 /
+// K10 / the cap, block reductions in a fixed order (sums) or order-free
+// (mins / maxes): deterministic.
+
+constexpr int kSceneThreads = 256;
+
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, unsigned long long* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned long long r = sh[0];
+  for (int i = 1; i < kSceneThreads / 32; ++i) r = min(r, sh[i]);
+  return r;
+}
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v, unsigned long long* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned long long r = sh[0];
+  for (int i = 1; i < kSceneThreads / 32; ++i) r = max(r, sh[i]);
+  return r;
+}
+
+// u[4 s + 0] first non-positive gap, [1] first degenerate, [2] ord_bits(min gap)
+__global__ void __launch_bounds__(kSceneThreads) k_scene_energy(DevSamples S, const double* __restrict__ x,
+                                                                const int64_t* __restrict__ soff,
+                                                                double* __restrict__ e, unsigned long long* u) {
+  __shared__ double shd[kSceneThreads / 32];
+  __shared__ unsigned long long shu[kSceneThreads / 32];
+  const int sc = blockIdx.x;
+  double acc = 0;
+  double mg = 1.7976931348623157e308;
+  unsigned long long bad = ~0ull, deg = ~0ull;
+  for (int64_t i = soff[sc] + threadIdx.x; i < soff[sc + 1]; i += kSceneThreads) {
+    double g;
+    if (!sample_gap(S, i, x, g)) {
+      deg = min(deg, (unsigned long long)i);
+      continue;
+    }
+    mg = dmin(mg, g);
+    if (!(g > 0)) {
+      bad = min(bad, (unsigned long long)i);
+      continue;
+    }
+    double B, dB, ddB;
+    barrier_eval(g, S.eps[i], B, dB, ddB);
+    acc += S.coef[i] * B;
+  }
+  const double r = block_sum<kSceneThreads>(acc, shd);
+  const unsigned long long b = block_min_u64(bad, shu), d = block_min_u64(deg, shu), m = block_min_u64(ord_bits(mg), shu);
+  if (threadIdx.x == 0) {
+    e[sc] = r;
+    u[4 * sc] = b;
+    u[4 * sc + 1] = d;
+    u[4 * sc + 2] = m;
+  }
+}
+
+// per scene: u[4 s] ord_bits(filter alpha), [1] first degenerate, [2] first
+// sample with g < eps (cap active), [3] ord_bits(max |dx_v| over the scene)
+__global__ void __launch_bounds__(kSceneThreads) k_scene_alpha(DevSamples S, const double* __restrict__ x,
+                                                               const double* __restrict__ dx,
+                                                               const int64_t* __restrict__ soff,
+                                                               const int64_t* __restrict__ voff,
+                                                               unsigned long long* u) {
+  __shared__ unsigned long long shu[kSceneThreads / 32];
+  const int sc = blockIdx.x;
+  unsigned long long best = ord_bits(1.0), deg = ~0ull, act = ~0ull, mv = ord_bits(0.0);
+  for (int64_t i = soff[sc] + threadIdx.x; i < soff[sc + 1]; i += kSceneThreads) {
+    Kin k;
+    if (!kinematics<true>(S, i, x, k)) {
+      deg = min(deg, (unsigned long long)i);
+      continue;
+    }
+    if (k.g < S.eps[i]) act = min(act, (unsigned long long)i);
+    double dgdx = 0;
+    for (int v = 0; v < k.nv; ++v) {
+      const int id = v < 3 ? S.slave[3 * i + v] : S.master[3 * i + v - 3];
+      dgdx += dot(k.dg[v], ld3(dx, id));
+    }
+    if (dgdx < 0) {
+      const unsigned long long b = ord_bits(0.9 * k.g / (-dgdx));
+      best = b < best ? b : best;
+    }
+  }
+  for (int64_t v = voff[sc] + threadIdx.x; v < voff[sc + 1]; v += kSceneThreads) {
+    const unsigned long long b = ord_bits(norm(ld3(dx, (int)v)));
+    mv = b > mv ? b : mv;
+  }
+  const unsigned long long a = block_min_u64(best, shu), d = block_min_u64(deg, shu), c = block_min_u64(act, shu),
+                           m = block_max_u64(mv, shu);
+  if (threadIdx.x == 0) {
+    u[4 * sc] = a;
+    u[4 * sc + 1] = d;
+    u[4 * sc + 2] = c;
+    u[4 * sc + 3] = m;
+  }
+}
+
+// samples per scene (scene of a sample = scene of its first slave vertex)
+__global__ void k_scene_count(DevSamples S, const int32_t* __restrict__ vscene, int32_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S.n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[vscene[S.slave[3 * i]]], 1);  // integer counts: order-free
+}
+
 int grid_for(int64_t n, int threads) {
   const int64_t b = (n + threads - 1) / threads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
@@ -336,6 +445,75 @@ double run_displacement_cap(Ctx& c) {
   const double max_move = from_ord_bits(u[3]);
   if (max_move <= 0.5 * c.params.eps_max) return 1.0;
   return 0.5 * c.params.eps_max / max_move;
+}
+
+// ===========================================================================
+// scene-segmented host entry points (batched System solve)
+
+struct SceneTmp : TmpBase {
+  DBuf<double> e;
+  DBuf<unsigned long long> u;
+  DBuf<int32_t> cnt;
+};
+static SceneTmp& scene_tmp(Ctx& c) {
+  if (!c.scene_tmp) c.scene_tmp = std::make_unique<SceneTmp>();
+  return *static_cast<SceneTmp*>(c.scene_tmp.get());
+}
+
+void scene_sample_offsets(Ctx& c, const int32_t* vscene_dev, int n_scenes, std::vector<int64_t>& soff_host,
+                          DBuf<int64_t>& soff_dev) {
+  SceneTmp& T = scene_tmp(c);
+  T.cnt.resize(n_scenes);
+  T.cnt.zero(c.stream);
+  if (c.ns) {
+    k_scene_count<<<grid_for(c.ns, 256), 256, 0, c.stream>>>(c.samples(), vscene_dev, T.cnt.p);
+    ++c.launches;
+  }
+  std::vector<int32_t> cnt = T.cnt.to_host(c.stream);
+  soff_host.assign(n_scenes + 1, 0);
+  for (int s = 0; s < n_scenes; ++s) soff_host[s + 1] = soff_host[s] + cnt[s];
+  soff_dev.upload(soff_host, c.stream);
+}
+
+void run_scene_energy(Ctx& c, const double* xp, int n_scenes, const int64_t* soff_dev, double* e,
+                      int64_t* first_bad, int64_t* first_deg, double* min_gap) {
+  SceneTmp& T = scene_tmp(c);
+  T.e.resize(n_scenes);
+  T.u.resize(4 * n_scenes);
+  k_scene_energy<<<n_scenes, kSceneThreads, 0, c.stream>>>(c.samples(), xp, soff_dev, T.e.p, T.u.p);
+  ++c.launches;
+  GMCP_CUDA(cudaGetLastError());
+  std::vector<unsigned long long> u(4 * n_scenes);
+  T.e.download(e, n_scenes, c.stream);
+  T.u.download(u.data(), 4 * n_scenes, c.stream);
+  c.sync();
+  for (int s = 0; s < n_scenes; ++s) {
+    first_bad[s] = u[4 * s] == ~0ull ? -1 : (int64_t)u[4 * s];
+    first_deg[s] = u[4 * s + 1] == ~0ull ? -1 : (int64_t)u[4 * s + 1];
+    min_gap[s] = from_ord_bits(u[4 * s + 2]);
+  }
+}
+
+// alpha_s = min(1, step_filter_s, displacement_cap_s) (contact_energy.hpp:184-213 per scene)
+void run_scene_alpha(Ctx& c, int n_scenes, const int64_t* soff_dev, const int64_t* voff_dev, double* alpha,
+                     int64_t* first_deg) {
+  SceneTmp& T = scene_tmp(c);
+  T.u.resize(4 * n_scenes);
+  k_scene_alpha<<<n_scenes, kSceneThreads, 0, c.stream>>>(c.samples(), c.X(), c.DX(), soff_dev, voff_dev, T.u.p);
+  ++c.launches;
+  GMCP_CUDA(cudaGetLastError());
+  std::vector<unsigned long long> u(4 * n_scenes);
+  T.u.download(u.data(), 4 * n_scenes, c.stream);
+  c.sync();
+  for (int s = 0; s < n_scenes; ++s) {
+    double a = from_ord_bits(u[4 * s]);
+    first_deg[s] = u[4 * s + 1] == ~0ull ? -1 : (int64_t)u[4 * s + 1];
+    if (u[4 * s + 2] != ~0ull) {  // cap active in this scene
+      const double max_move = from_ord_bits(u[4 * s + 3]);
+      if (max_move > 0.5 * c.params.eps_max) a = std::min(a, 0.5 * c.params.eps_max / max_move);
+    }
+    alpha[s] = std::min(1.0, a);
+  }
 }
 
 }  // namespace gmcp_b200

@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -478,6 +480,11 @@ struct PairRt {
 struct SystemImpl {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // batched independent scenes: contiguous vertex ranges per scene
+  int32_t n_scenes = 1;
+  std::vector<int32_t> vscene;       // scene of each vertex (empty: one scene)
+  std::vector<int64_t> scene_voff;   // [S+1] vertex offsets
+  std::vector<int64_t> scene_iters;  // Newton iterations per scene (last solve)
   int64_t n_dof = 0;
   int64_t launches = 0;
   std::vector<Body> bodies;
@@ -878,15 +885,10 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
 // ---------------------------------------------------------------------------
 // solve loop (solver.hpp:125-228)
 
-void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callback cb, void* user,
-                  gmcp_run_stats* out) {
-  if (S.bodies.empty()) throw StatusError(GMCP_ERR_CONFIG, "solve: no bodies");
-  if (st.load_steps < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: load_steps must be >= 1");
-  if (st.max_newton_iters < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: max_newton_iters must be >= 1");
-  if (st.max_line_search < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: max_line_search must be >= 1");
-  const auto t_start = std::chrono::steady_clock::now();
-  const double tol = st.newton_tol > 0 ? st.newton_tol : derived_newton_tol(S);
-  int64_t n_free = 0;
+// Shared solve set-up: elastic BCSR, Dirichlet targets, device vectors, the
+// fixed-dof mask, run-start anchor positions, pair contexts bound to S.x/S.dx.
+void setup_solve(SystemImpl& S, int64_t& n_free, DBuf<double>& eps_ref) {
+  n_free = 0;
   for (uint8_t f : S.fixed) n_free += f == 0;
   if (n_free == 0) throw StatusError(GMCP_ERR_CONFIG, "solve: no free degrees of freedom");
   if (!S.el_built) build_elastic(S);
@@ -910,7 +912,6 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
   std::vector<double> mask(n);
   for (int64_t d = 0; d < n; ++d) mask[d] = S.fixed[d] ? 0.0 : 1.0;
   S.mask_d.upload(mask, S.stream);
-  DBuf<double> eps_ref;  // run-start positions anchor every support radius (solver.hpp:146)
   eps_ref.resize(n);
   GMCP_CUDA(cudaMemcpyAsync(eps_ref.p, S.x.p, n * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
   for (auto& pr : S.pairs) {
@@ -919,6 +920,713 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
     pr->c->n_dof = n;
     pr->c->stream = S.stream;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Batched independent scenes: one System holds S scenes in
+// contiguous vertex ranges; every reduction that steers the Newton loop is
+// segmented by scene (residual, step filter + cap, line-search energies and
+// coefficients), each scene converges and backtracks on its own, and the
+// linear solve is one PCG over the active scenes (the Hessian is block
+// diagonal per scene; converged scenes are masked like fixed dofs).
+namespace {
+
+constexpr int kSceneBlk = 256;
+
+// per scene: out[5 s + 0..4] = g_el.dx, dx.K dx, f.dx, 0.5 gel.u, f.u  (u = x - rest)
+__global__ void __launch_bounds__(kSceneBlk) k_sys_scene_el(const int64_t* __restrict__ voff, Bcsr K,
+                                                           const double* __restrict__ dx,
+                                                           const double* __restrict__ gel,
+                                                           const double* __restrict__ fext,
+                                                           const double* __restrict__ x,
+                                                           const double* __restrict__ rest, double* __restrict__ out) {
+  __shared__ double sh[5][kSceneBlk / 32];
+  const int sc = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double d[5] = {0, 0, 0, 0, 0};
+  for (int64_t v = voff[sc] + wid; v < voff[sc + 1]; v += kSceneBlk / 32) {
+    d3 acc = row_mv(K, (int)v, dx, lane);
+    acc.x = warp_sum(acc.x);
+    acc.y = warp_sum(acc.y);
+    acc.z = warp_sum(acc.z);
+    if (lane == 0) {
+      const d3 dv = ld3(dx, (int)v), u = ld3(x, (int)v) - ld3(rest, (int)v);
+      d[0] += dot(ld3(gel, (int)v), dv);
+      d[1] += dot(dv, acc);
+      d[2] += dot(ld3(fext, (int)v), dv);
+      d[3] += dot(ld3(gel, (int)v), u);
+      d[4] += dot(ld3(fext, (int)v), u);
+    }
+  }
+  if (lane == 0)
+    for (int q = 0; q < 5; ++q) sh[q][wid] = d[q];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 5; ++q) {
+      double t = 0;
+      for (int i = 0; i < kSceneBlk / 32; ++i) t += sh[q][i];
+      out[5 * sc + q] = q == 3 ? 0.5 * t : t;
+    }
+}
+
+// per scene: ord_bits(max |grad_d|) over free dofs
+__global__ void __launch_bounds__(kSceneBlk) k_sys_scene_resid(const int64_t* __restrict__ voff,
+                                                              const double* __restrict__ grad,
+                                                              const double* __restrict__ mask,
+                                                              unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long sh[kSceneBlk / 32];
+  const int sc = blockIdx.x;
+  unsigned long long best = 0;
+  for (int64_t d = 3 * voff[sc] + threadIdx.x; d < 3 * voff[sc + 1]; d += kSceneBlk)
+    if (mask[d] != 0) {
+      const unsigned long long b = ord_bits(fabs(grad[d]));
+      best = b > best ? b : best;
+    }
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long r = 0;
+    for (int i = 0; i < kSceneBlk / 32; ++i) r = max(r, sh[i]);
+    out[sc] = r;
+  }
+}
+
+// xtry = x + alpha_s dx per scene; x = xtry where taken_s
+__global__ void k_sys_scene_axpy(int64_t n, const int32_t* __restrict__ vscene, const double* __restrict__ alpha,
+                                 const double* __restrict__ x, const double* __restrict__ dx, double* __restrict__ xt) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x)
+    xt[d] = x[d] + alpha[vscene[d / 3]] * dx[d];
+}
+__global__ void k_sys_scene_take(int64_t n, const int32_t* __restrict__ vscene, const int32_t* __restrict__ take,
+                                 const double* __restrict__ xt, double* __restrict__ x) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x)
+    if (take[vscene[d / 3]]) x[d] = xt[d];
+}
+
+// per-scene max |x_v - ref_v| over a pair's vertices (pair_motion per scene)
+__global__ void k_sys_scene_motion(int64_t m, const int32_t* __restrict__ verts, const int32_t* __restrict__ vscene,
+                                   const double* __restrict__ x, const double* __restrict__ ref,
+                                   unsigned long long* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = verts[i];
+    atomicMax(&out[vscene[v]], ord_bits(norm(ld3(x, v) - ld3(ref, v))));  // order-free max
+  }
+}
+// ref = x on the vertices of the re-sampled scenes
+__global__ void k_sys_scene_refpos(int64_t n, const int32_t* __restrict__ vscene, const uint8_t* __restrict__ take,
+                                   const double* __restrict__ x, double* __restrict__ ref) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x)
+    if (take[vscene[d / 3]]) ref[d] = x[d];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Scene-segmented PCG (batched scenes): the same arithmetic as K9 per scene --
+// every dot product, alpha, beta and the convergence test are per scene
+// (contiguous vertex ranges, block-per-scene fixed-order sums), so each scene
+// iterates exactly as its own PCG would, and stops on its own tolerance.
+namespace {
+
+// SpMV: p_new = z + beta_s p_old, q = mask .* ((H + shift_s I) p_new); dv[v] = p_new.q
+template <int kRowLanes>
+__global__ void __launch_bounds__(kThreads) k_spmv_seg(int nv, MatSet M, const double* __restrict__ mask,
+                                                       const int32_t* __restrict__ vscene,
+                                                       const int32_t* __restrict__ act,
+                                                       const double* __restrict__ st,
+                                                       const double* __restrict__ shift_s,
+                                                       const double* __restrict__ z, const double* __restrict__ p_old,
+                                                       double* __restrict__ p_new, double* __restrict__ q,
+                                                       double* __restrict__ dv) {
+  const int lane = threadIdx.x & 31, sub = lane & (kRowLanes - 1);
+  const int rows_per_block = kThreads / kRowLanes;
+  for (int v0 = blockIdx.x * rows_per_block + (threadIdx.x >> 5) * (32 / kRowLanes); v0 < nv;
+       v0 += gridDim.x * rows_per_block) {
+    const int v = v0 + (lane / kRowLanes);
+    // neighbours share the row's scene (the matrix is block diagonal per scene);
+    // scenes that stopped are skipped (their x, r stay as they converged)
+    const bool live = v < nv && act[vscene[v]];
+    const double beta = live ? st[8 * vscene[v] + 3] : 0.0;
+    d3 acc = mk3(0, 0, 0);
+    if (live) {
+      acc = row_mv8<kRowLanes>(M.el, v, z, p_old, beta, sub);
+      for (int k = 0; k < M.np; ++k) acc = acc + row_mv8<kRowLanes>(M.c[k], v, z, p_old, beta, sub);
+    }
+#pragma unroll
+    for (int o = kRowLanes / 2; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    }
+    if (sub == 0 && v < nv && !live) dv[v] = 0;
+    if (sub == 0 && live) {
+      const d3 m = ld3(mask, v);
+      const d3 pv = ld3(z, v) + beta * ld3(p_old, v);
+      const double sh = shift_s[vscene[v]];
+      if (sh != 0) acc = acc + sh * pv;
+      const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
+      q[3 * v] = y.x;
+      q[3 * v + 1] = y.y;
+      q[3 * v + 2] = y.z;
+      p_new[3 * v] = pv.x;
+      p_new[3 * v + 1] = pv.y;
+      p_new[3 * v + 2] = pv.z;
+      dv[v] = dot(pv, y);
+    }
+  }
+}
+
+// per scene: sum of dv over its vertices (fixed order). mode 0: pq -> alpha;
+// mode 1: (rz_new, rr) -> beta, rz, rr, active flag; mode 2: init (rz, rr, bb)
+template <int Mode>
+__global__ void __launch_bounds__(kSceneBlk) k_seg_sums(const int64_t* __restrict__ voff,
+                                                        const double* __restrict__ dv, int nv, double tol2,
+                                                        double* __restrict__ st, int32_t* __restrict__ act) {
+  // st[8 s + 0] rz, [1] pq, [2] alpha, [3] beta, [4] rr, [5] bb
+  __shared__ double sh[2][kSceneBlk / 32];
+  const int sc = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int W = Mode == 0 ? 1 : 2;
+  double a[2] = {0, 0};
+  for (int64_t v = voff[sc] + threadIdx.x; v < voff[sc + 1]; v += kSceneBlk)
+    for (int q = 0; q < W; ++q) a[q] += dv[(int64_t)q * nv + v];
+  for (int q = 0; q < W; ++q) {
+    const double t = warp_sum(a[q]);
+    if (lane == 0) sh[q][wid] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double r[2] = {0, 0};
+  for (int q = 0; q < W; ++q)
+    for (int i = 0; i < kSceneBlk / 32; ++i) r[q] += sh[q][i];
+  double* s = st + 8 * sc;
+  if (Mode == 0) {
+    s[1] = r[0];
+    s[2] = act[sc] && r[0] != 0 ? s[0] / r[0] : 0.0;
+  } else if (Mode == 1) {
+    if (act[sc]) {
+      s[3] = s[0] != 0 ? r[0] / s[0] : 0.0;
+      s[0] = r[0];
+      s[4] = r[1];
+      act[sc] = r[1] > tol2 * s[5] ? 1 : 0;  // converged (or non-finite) -> stop
+    }
+  } else {
+    s[0] = r[0];
+    s[3] = 0.0;
+    s[4] = r[1];
+    s[5] = r[1];
+    act[sc] = act[sc] && r[1] > 0 ? 1 : 0;
+  }
+}
+
+// x += alpha_s p, r -= alpha_s q, z = Minv r; dv = (r.z, r.r) per vertex
+__global__ void __launch_bounds__(kThreads) k_update_seg(int nv, const int32_t* __restrict__ vscene,
+                                                         const int32_t* __restrict__ act,
+                                                         const double* __restrict__ st, const double* __restrict__ p,
+                                                         const double* __restrict__ q, double* __restrict__ x,
+                                                         double* __restrict__ r, double* __restrict__ z,
+                                                         const double* __restrict__ minv, double* __restrict__ dv) {
+  for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
+    if (!act[vscene[v]]) {
+      dv[v] = 0;
+      dv[nv + v] = 0;
+      continue;
+    }
+    const double a = st[8 * vscene[v] + 2];
+    const d3 xv = ld3nc(x, v) + a * ld3nc(p, v);
+    const d3 rv = ld3nc(r, v) - a * ld3nc(q, v);
+    const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
+    const double xa[3] = {xv.x, xv.y, xv.z}, ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      x[3 * v + c] = xa[c];
+      r[3 * v + c] = ra[c];
+      z[3 * v + c] = za[c];
+    }
+    dv[v] = dot(rv, zv);
+    dv[nv + v] = dot(rv, rv);
+  }
+}
+
+// init: x = p = 0, r = -mask .* grad, z = Minv r; dv = (r.z, r.r)
+__global__ void k_init_seg(int nv, const int32_t* __restrict__ vscene, const int32_t* __restrict__ act,
+                           const double* __restrict__ grad, const double* __restrict__ mask,
+                           const double* __restrict__ minv, double* __restrict__ x, double* __restrict__ r,
+                           double* __restrict__ z, double* __restrict__ p, double* __restrict__ dv) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    if (!act[vscene[v]]) {  // scenes not being solved keep their x (dx)
+      dv[v] = 0;
+      dv[nv + v] = 0;
+      continue;
+    }
+    const d3 m = ld3(mask, v), g = ld3(grad, v);
+    const d3 rv = mk3(-m.x * g.x, -m.y * g.y, -m.z * g.z);
+    const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
+    const double ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
+    for (int k = 0; k < 3; ++k) {
+      x[3 * v + k] = 0;
+      p[3 * v + k] = 0;
+      r[3 * v + k] = ra[k];
+      z[3 * v + k] = za[k];
+    }
+    dv[v] = dot(rv, zv);
+    dv[nv + v] = dot(rv, rv);
+  }
+}
+
+// block-Jacobi with a per-scene diagonal shift
+__global__ void k_block_jacobi_seg(int nv, MatSet M, const double* __restrict__ mask,
+                                   const int32_t* __restrict__ vscene, const double* __restrict__ shift_s,
+                                   double* __restrict__ minv) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    double D[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    get_diag(M.el, v, D);
+    const double sh = shift_s[vscene[v]];
+    D[0] += sh;
+    D[4] += sh;
+    D[8] += sh;
+    const double m[3] = {mask[3 * v], mask[3 * v + 1], mask[3 * v + 2]};
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        if (m[a] == 0 || m[b] == 0) D[3 * a + b] = (a == b) ? 1.0 : 0.0;
+    const double c00 = D[4] * D[8] - D[5] * D[7], c01 = D[2] * D[7] - D[1] * D[8], c02 = D[1] * D[5] - D[2] * D[4];
+    const double c10 = D[5] * D[6] - D[3] * D[8], c11 = D[0] * D[8] - D[2] * D[6], c12 = D[2] * D[3] - D[0] * D[5];
+    const double c20 = D[3] * D[7] - D[4] * D[6], c21 = D[1] * D[6] - D[0] * D[7], c22 = D[0] * D[4] - D[1] * D[3];
+    const double det = D[0] * c00 + D[1] * c10 + D[2] * c20;
+    double* o = minv + 9 * (int64_t)v;
+    if (det != 0 && isfinite(det)) {
+      const double id = 1.0 / det;
+      o[0] = c00 * id; o[1] = c01 * id; o[2] = c02 * id;
+      o[3] = c10 * id; o[4] = c11 * id; o[5] = c12 * id;
+      o[6] = c20 * id; o[7] = c21 * id; o[8] = c22 * id;
+    } else {
+      for (int q = 0; q < 9; ++q) o[q] = 0;
+      for (int a = 0; a < 3; ++a) o[4 * a] = D[4 * a] != 0 ? 1.0 / D[4 * a] : 1.0;
+    }
+  }
+}
+
+// per scene: sum of the free diagonal entries of H (the regularization scale)
+__global__ void __launch_bounds__(kSceneBlk) k_seg_diag(int nv, MatSet M, const double* __restrict__ mask,
+                                                        const int64_t* __restrict__ voff, double* __restrict__ out) {
+  __shared__ double sh[kSceneBlk / 32];
+  const int sc = blockIdx.x;
+  double acc = 0;
+  for (int64_t v = voff[sc] + threadIdx.x; v < voff[sc + 1]; v += kSceneBlk) {
+    double e[9];
+    if (get_diag(M.el, (int)v, e))
+      for (int a = 0; a < 3; ++a)
+        if (mask[3 * v + a] != 0) acc += e[4 * a];
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int i = 0; i < kSceneBlk / 32; ++i) t += sh[i];
+    out[sc] = t;
+  }
+}
+
+}  // namespace
+
+struct SegPcgTmp {
+  DBuf<double> dv, st, shift;
+  DBuf<int32_t> act, vscene;
+  DBuf<int64_t> voff;
+};
+
+// Runs the segmented PCG for the scenes with active[s]; returns iterations of
+// the slowest scene; rel[s] = sqrt(rr_s / bb_s) at exit (0 when bb_s = 0).
+int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::vector<int32_t>& active,
+                const std::vector<double>& shift, std::vector<double>& rel) {
+  const int nv = S.nv(), NS = S.n_scenes;
+  cudaStream_t s = S.stream;
+  MatSet M = mats(S);
+  T.dv.resize(2 * (int64_t)nv);
+  T.st.resize(8 * NS);
+  T.st.zero(s);
+  T.act.upload(active, s);
+  T.shift.upload(shift, s);
+  k_block_jacobi_seg<<<grid_for(nv, 256), 256, 0, s>>>(nv, M, S.mask_d.p, T.vscene.p, T.shift.p, S.minv.p);
+  k_init_seg<<<grid_for(nv, 256), 256, 0, s>>>(nv, T.vscene.p, T.act.p, S.grad.p, S.mask_d.p, S.minv.p, S.dx.p,
+                                              S.r.p, S.z.p, S.p.p, T.dv.p);
+  k_seg_sums<2><<<NS, kSceneBlk, 0, s>>>(T.voff.p, T.dv.p, nv, 0.0, T.st.p, T.act.p);
+  S.launches += 3;
+  const double tol2 = tol * tol;
+  const int chunk = 16;
+  const int lanes = nv / std::max(NS, 1) < kSmallRows ? 8 : 4;
+  const int gsp = std::min(grid_for((int64_t)nv * lanes, kThreads), kBlocks);
+  const int gup = std::min(grid_for((int64_t)nv, kThreads), kBlocks);
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  GMCP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int k = 0; k < chunk; ++k) {
+    double* p_old = (k & 1) ? S.w.p : S.p.p;
+    double* p_new = (k & 1) ? S.p.p : S.w.p;
+    if (lanes == 8)
+      k_spmv_seg<8><<<gsp, kThreads, 0, s>>>(nv, M, S.mask_d.p, T.vscene.p, T.act.p, T.st.p, T.shift.p, S.z.p, p_old, p_new,
+                                             S.q.p, T.dv.p);
+    else
+      k_spmv_seg<4><<<gsp, kThreads, 0, s>>>(nv, M, S.mask_d.p, T.vscene.p, T.act.p, T.st.p, T.shift.p, S.z.p, p_old, p_new,
+                                             S.q.p, T.dv.p);
+    k_seg_sums<0><<<NS, kSceneBlk, 0, s>>>(T.voff.p, T.dv.p, nv, tol2, T.st.p, T.act.p);
+    k_update_seg<<<gup, kThreads, 0, s>>>(nv, T.vscene.p, T.act.p, T.st.p, p_new, S.q.p, S.dx.p, S.r.p, S.z.p,
+                                          S.minv.p, T.dv.p);
+    k_seg_sums<1><<<NS, kSceneBlk, 0, s>>>(T.voff.p, T.dv.p, nv, tol2, T.st.p, T.act.p);
+  }
+  GMCP_CUDA(cudaStreamEndCapture(s, &graph));
+  GMCP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  int it = 0;
+  std::vector<int32_t> act(NS);
+  while (it < maxit) {
+    GMCP_CUDA(cudaGraphLaunch(exec, s));
+    S.launches += 4 * chunk;
+    it += chunk;
+    T.act.download(act.data(), NS, s);
+    S.sync();
+    bool any = false;
+    for (int v : act) any |= v != 0;
+    if (!any) break;
+  }
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  std::vector<double> st = T.st.to_host(s);
+  rel.resize(NS, 0.0);
+  for (int sc = 0; sc < NS; ++sc) {
+    if (!active[sc]) continue;  // not solved by this call
+    if (!std::isfinite(st[8 * sc + 4])) throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
+    rel[sc] = st[8 * sc + 5] > 0 ? std::sqrt(st[8 * sc + 4] / st[8 * sc + 5]) : 0.0;
+  }
+  GMCP_CUDA(cudaGetLastError());
+  return it;
+}
+
+// solver.hpp:256-269 per scene (loads and bodies of that scene)
+std::vector<double> derived_newton_tol_scenes(const SystemImpl& S) {
+  const int NS = S.n_scenes;
+  std::vector<double> scale(NS, 0.0), vol(NS, 0.0), emax(NS, 0.0);
+  std::vector<long> nel(NS, 0);
+  for (int64_t d = 0; d < S.n_dof; ++d) {
+    const int sc = S.vscene[d / 3];
+    scale[sc] = std::max(scale[sc], std::abs(S.f_ext[d]));
+  }
+  for (const Body& b : S.bodies) {
+    const int sc = S.vscene[b.offset];
+    for (double v : b.vol) vol[sc] += v;
+    nel[sc] += (long)b.vol.size();
+    emax[sc] = std::max(emax[sc], b.E);
+  }
+  std::vector<double> tol(NS);
+  for (int sc = 0; sc < NS; ++sc) {
+    const double h = std::cbrt(6.0 * vol[sc] / std::max<long>(nel[sc], 1));
+    const double sv = std::max(scale[sc], 1e-6 * emax[sc] * h * h);
+    tol[sc] = 1e-6 * std::max(sv, 1e-6);
+  }
+  return tol;
+}
+
+void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callback cb, void* user,
+                          gmcp_run_stats* out, std::chrono::steady_clock::time_point t_start) {
+  const int NS = S.n_scenes;
+  const std::vector<double> tol =
+      st.newton_tol > 0 ? std::vector<double>(NS, st.newton_tol) : derived_newton_tol_scenes(S);
+  int64_t n_free = 0;
+  DBuf<double> eps_ref;
+  setup_solve(S, n_free, eps_ref);
+  const int64_t n = S.n_dof;
+  cudaStream_t s = S.stream;
+  DBuf<int32_t> vscene_d, active_d, take_d;
+  DBuf<int64_t> voff_d;
+  DBuf<double> alpha_d, el_d, mask_fixed;
+  DBuf<unsigned long long> resid_d;
+  vscene_d.upload(S.vscene, s);
+  voff_d.upload(S.scene_voff, s);
+  SegPcgTmp segT;
+  segT.vscene.upload(S.vscene, s);
+  segT.voff.upload(S.scene_voff, s);
+  std::vector<int64_t> n_free_s(NS, 0);
+  for (int64_t d = 0; d < n; ++d) n_free_s[S.vscene[d / 3]] += S.fixed[d] == 0;
+  active_d.resize(NS);
+  take_d.resize(NS);
+  alpha_d.resize(NS);
+  el_d.resize(5 * NS);
+  resid_d.resize(NS);
+  mask_fixed.resize(n);
+  GMCP_CUDA(cudaMemcpyAsync(mask_fixed.p, S.mask_d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  for (auto& pr : S.pairs) {  // the pairs' broadphase is scene-aware
+    pr->c->vscene.upload(S.vscene, s);
+    pr->c->n_scenes = NS;
+  }
+  const int np = (int)S.pairs.size();
+  std::vector<std::vector<int64_t>> soff_h(np);
+  std::vector<DBuf<int64_t>> soff_d(np);
+  auto rebuild_all = [&]() {
+    for (int p = 0; p < np; ++p) {
+      rebuild_pair(S, *S.pairs[p], eps_ref.p);
+      scene_sample_offsets(*S.pairs[p]->c, vscene_d.p, NS, soff_h[p], soff_d[p]);
+    }
+  };
+  // re-sample only the flagged scenes of pair p (as separate Systems would):
+  // sample everything, then keep the old per-scene segments elsewhere
+  DBuf<uint8_t> flag_d;
+  DBuf<unsigned long long> motion_d;
+  std::vector<int64_t> soff_new;
+  auto rebuild_scenes = [&](int p, const std::vector<uint8_t>& flag) {
+    PairRt& pr = *S.pairs[p];
+    Ctx& c = *pr.c;
+    S.u_valid = false;
+    snapshot_samples(c);
+    int64_t counts[3];
+    run_broadphase(c, pr.params.detection_radius, counts);
+    run_sampler(c, eps_ref.p);
+    DBuf<int64_t> tmp;
+    scene_sample_offsets(c, vscene_d.p, NS, soff_new, tmp);
+    std::vector<int64_t> merged;
+    splice_samples(c, soff_h[p], soff_new, flag, merged);
+    soff_h[p] = merged;
+    soff_d[p].upload(merged, s);
+    c.plan.valid = false;
+    build_assembly_plan(c);
+    flag_d.upload(flag, s);
+    k_sys_scene_refpos<<<grid_for(n, 256), 256, 0, s>>>(n, vscene_d.p, flag_d.p, S.x.p, pr.ref_pos.p);
+    ++S.launches;
+  };
+  // contact energies per scene at xp (all pairs): feasible_s, energy_s, min gap
+  std::vector<double> ce(NS), ce_try(NS), tmp_e(NS), tmp_mg(NS), mg(NS);
+  std::vector<int64_t> tmp_bad(NS), tmp_deg(NS);
+  std::vector<uint8_t> feas(NS);
+  auto scene_contact = [&](double* xp, std::vector<double>& e) {
+    std::fill(e.begin(), e.end(), 0.0);
+    std::fill(feas.begin(), feas.end(), 1);
+    std::fill(mg.begin(), mg.end(), 1.7976931348623157e308);
+    for (int p = 0; p < np; ++p) {
+      Ctx& c = *S.pairs[p]->c;
+      double* saved = c.x_ext;
+      c.x_ext = xp;
+      run_scene_energy(c, xp, NS, soff_d[p].p, tmp_e.data(), tmp_bad.data(), tmp_deg.data(), tmp_mg.data());
+      c.x_ext = saved;
+      for (int sc = 0; sc < NS; ++sc) {
+        if (tmp_deg[sc] >= 0 && (tmp_bad[sc] < 0 || tmp_deg[sc] < tmp_bad[sc]))
+          throw StatusError(GMCP_ERR_DEGENERATE, "contact sample on a degenerate slave triangle");
+        if (tmp_bad[sc] >= 0) feas[sc] = 0;
+        e[sc] += tmp_e[sc];
+        mg[sc] = std::min(mg[sc], tmp_mg[sc]);
+      }
+    }
+  };
+  std::vector<double> el(5 * NS);
+  auto scene_el = [&]() {
+    k_sys_scene_el<<<NS, kSceneBlk, 0, s>>>(voff_d.p, Bcsr{S.k_rowptr.p, S.k_cols.p, S.k_vals.p}, S.dx.p, S.gel.p,
+                                            S.fext_d.p, S.x.p, S.rest_d.p, el_d.p);
+    ++S.launches;
+    el_d.download(el.data(), 5 * NS, s);
+    S.sync();
+  };
+  std::vector<unsigned long long> resid_u(NS);
+  std::vector<double> resid(NS);
+  auto scene_resid = [&]() {
+    k_sys_scene_resid<<<NS, kSceneBlk, 0, s>>>(voff_d.p, S.grad.p, mask_fixed.p, resid_d.p);
+    ++S.launches;
+    resid_d.download(resid_u.data(), NS, s);
+    S.sync();
+    for (int sc = 0; sc < NS; ++sc) resid[sc] = from_ord_bits(resid_u[sc]);
+  };
+  const int gn = grid_for(n, 256);
+  S.scene_iters.assign(NS, 0);
+  out->total_newton_iters = 0;
+  out->total_rebuilds = 0;
+  out->total_pcg_iters = 0;
+  out->newton_tol_used = *std::min_element(tol.begin(), tol.end());
+  std::vector<int32_t> active(NS), take(NS);
+  std::vector<double> alpha(NS), a_pair(NS);
+  std::vector<int64_t> deg(NS);
+  std::vector<uint8_t> accepted(NS);
+  std::vector<double> energy(NS);
+  for (int step = 1; step <= st.load_steps; ++step) {
+    const double lambda = (double)step / st.load_steps;
+    gmcp_step_stats ss{};
+    ss.step = step;
+    ss.min_gap = 1.7976931348623157e308;
+    ss.energy_monotone = 1;
+    rebuild_all();
+    assemble(S, lambda);
+    scene_el();
+    scene_contact(S.x.p, ce);
+    for (int sc = 0; sc < NS; ++sc) {
+      if (!feas[sc]) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
+      energy[sc] = el[5 * sc + 3] + ce[sc] - lambda * el[5 * sc + 4];
+      ss.min_gap = std::min(ss.min_gap, mg[sc]);
+    }
+    bool converged = false;
+    for (int it = 0; it < st.max_newton_iters; ++it) {
+      if (it > 0) assemble(S, lambda);
+      scene_resid();
+      int n_active = 0;
+      for (int sc = 0; sc < NS; ++sc) {
+        active[sc] = resid[sc] > tol[sc];
+        n_active += active[sc];
+      }
+      if (n_active == 0) {
+        converged = true;
+        break;
+      }
+      // scene-segmented PCG over the active scenes; scenes that do not reach
+      // the tolerance retry with their own diagonal shift (solver.hpp:352-361)
+      S.dx.zero(s);
+      std::vector<double> rel, shift(NS, 0.0);
+      int pit = pcg_batched(S, segT, st.pcg_tol, st.pcg_max_iters, active, shift, rel);
+      std::vector<int32_t> retry(NS, 0);
+      bool any_retry = false;
+      for (int sc = 0; sc < NS; ++sc)
+        if (active[sc] && !(rel[sc] <= st.pcg_tol)) {
+          retry[sc] = 1;
+          any_retry = true;
+        }
+      if (any_retry) {
+        DBuf<double> dsum_d;
+        dsum_d.resize(NS);
+        k_seg_diag<<<NS, kSceneBlk, 0, s>>>(S.nv(), mats(S), S.mask_d.p, voff_d.p, dsum_d.p);
+        ++S.launches;
+        std::vector<double> dsum = dsum_d.to_host(s);
+        for (int sc = 0; sc < NS; ++sc)
+          if (retry[sc]) shift[sc] = kRegularization * dsum[sc] / (double)std::max<int64_t>(n_free_s[sc], 1);
+        pit += pcg_batched(S, segT, st.pcg_tol, st.pcg_max_iters, retry, shift, rel);
+        for (int sc = 0; sc < NS; ++sc)
+          if (retry[sc] && !(rel[sc] <= st.pcg_tol))
+            throw StatusError(GMCP_ERR_SOLVER, "scene " + std::to_string(sc) +
+                                                   ": linear solve failed even with regularization; the system is "
+                                                   "insufficiently constrained (unfixed rigid body modes?)");
+      }
+      ss.pcg_iters += pit;
+      ss.newton_iters += 1;
+      for (int sc = 0; sc < NS; ++sc) S.scene_iters[sc] += active[sc];
+
+      // per-scene step size: min over pairs of min(1, filter, cap)
+      for (int sc = 0; sc < NS; ++sc) alpha[sc] = active[sc] ? 1.0 : 0.0;
+      for (int p = 0; p < np; ++p) {
+        run_scene_alpha(*S.pairs[p]->c, NS, soff_d[p].p, voff_d.p, a_pair.data(), deg.data());
+        for (int sc = 0; sc < NS; ++sc) {
+          if (deg[sc] >= 0) throw StatusError(GMCP_ERR_DEGENERATE, "triangle_normal: degenerate triangle", deg[sc]);
+          if (active[sc]) alpha[sc] = std::min(alpha[sc], a_pair[sc]);
+        }
+      }
+      scene_el();  // g_el.dx, dx.K dx, f.dx per scene
+      for (int sc = 0; sc < NS; ++sc) accepted[sc] = !active[sc];
+      for (int ls = 0; ls < st.max_line_search; ++ls) {
+        alpha_d.upload(alpha, s);
+        k_sys_scene_axpy<<<gn, 256, 0, s>>>(n, vscene_d.p, alpha_d.p, S.x.p, S.dx.p, S.xtry.p);
+        ++S.launches;
+        scene_contact(S.xtry.p, ce_try);
+        bool all = true;
+        for (int sc = 0; sc < NS; ++sc) {
+          take[sc] = 0;
+          if (accepted[sc]) continue;
+          const double a = alpha[sc];
+          const double dE =
+              a * el[5 * sc] + 0.5 * a * a * el[5 * sc + 1] - lambda * a * el[5 * sc + 2] + (ce_try[sc] - ce[sc]);
+          if (feas[sc] && dE < 0) {
+            take[sc] = 1;
+            accepted[sc] = 1;
+            energy[sc] += dE;
+            ce[sc] = ce_try[sc];
+            ss.min_gap = std::min(ss.min_gap, mg[sc]);
+          } else {
+            ss.backtracks += 1;
+            alpha[sc] = 0.5 * a;
+            all = false;
+          }
+        }
+        take_d.upload(take, s);
+        k_sys_scene_take<<<gn, 256, 0, s>>>(n, vscene_d.p, take_d.p, S.xtry.p, S.x.p);
+        ++S.launches;
+        if (all) break;
+      }
+      for (int sc = 0; sc < NS; ++sc)
+        if (!accepted[sc])
+          throw StatusError(GMCP_ERR_SOLVER, "load step " + std::to_string(step) + ", scene " + std::to_string(sc) +
+                                                 ": line search failed to find a feasible decrease");
+      // re-sample the scenes whose vertices outran their frozen sampling
+      // (solver.hpp:201-209, per scene)
+      bool rebuild = false;
+      for (int p = 0; p < np; ++p) {
+        PairRt& pr = *S.pairs[p];
+        const int64_t m = (int64_t)pr.motion_verts.n;
+        motion_d.resize(NS);
+        motion_d.zero(s);
+        if (m) {
+          k_sys_scene_motion<<<grid_for(m, 256), 256, 0, s>>>(m, pr.motion_verts.p, vscene_d.p, S.x.p, pr.ref_pos.p,
+                                                              motion_d.p);
+          ++S.launches;
+        }
+        std::vector<unsigned long long> mu = motion_d.to_host(s);
+        std::vector<uint8_t> flag(NS, 0);
+        int nflag = 0;
+        for (int sc = 0; sc < NS; ++sc) {
+          flag[sc] = from_ord_bits(mu[sc]) > 0.5 * pr.params.eps_max;
+          nflag += flag[sc];
+        }
+        if (nflag) {
+          rebuild_scenes(p, flag);
+          rebuild = true;
+        }
+      }
+      if (rebuild) {
+        ss.rebuilds += 1;
+        assemble(S, lambda);
+        scene_el();
+        scene_contact(S.x.p, ce);
+        for (int sc = 0; sc < NS; ++sc) {
+          if (!feas[sc]) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
+          energy[sc] = el[5 * sc + 3] + ce[sc] - lambda * el[5 * sc + 4];
+        }
+      }
+    }
+    if (!converged) {
+      int worst = 0;
+      for (int sc = 0; sc < NS; ++sc)
+        if (resid[sc] / tol[sc] > resid[worst] / tol[worst]) worst = sc;
+      out->residual = resid[worst];
+      throw StatusError(GMCP_ERR_SOLVER, "load step " + std::to_string(step) + ", scene " + std::to_string(worst) +
+                                             ": Newton exceeded " + std::to_string(st.max_newton_iters) +
+                                             " iterations (residual " + std::to_string(resid[worst]) + ", tolerance " +
+                                             std::to_string(tol[worst]) + ")");
+    }
+    scene_el();
+    double e_tot = 0, r_max = 0;
+    for (int sc = 0; sc < NS; ++sc) {
+      e_tot += el[5 * sc + 3] + ce[sc] - lambda * el[5 * sc + 4];
+      r_max = std::max(r_max, resid[sc]);
+    }
+    ss.residual = r_max;
+    ss.energy = e_tot;
+    out->total_rebuilds += ss.rebuilds;
+    out->total_pcg_iters += ss.pcg_iters;
+    S.x.download(S.x_host.data(), n, s);
+    S.sync();
+    if (cb) cb(&ss, S.x_host.data(), n, user);
+  }
+  for (int64_t v : S.scene_iters) out->total_newton_iters += v;  // scene-Newton-iterations
+  S.x.download(S.x_host.data(), n, s);
+  S.sync();
+  out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callback cb, void* user,
+                  gmcp_run_stats* out) {
+  if (S.bodies.empty()) throw StatusError(GMCP_ERR_CONFIG, "solve: no bodies");
+  if (st.load_steps < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: load_steps must be >= 1");
+  if (st.max_newton_iters < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: max_newton_iters must be >= 1");
+  if (st.max_line_search < 1) throw StatusError(GMCP_ERR_CONFIG, "solve: max_line_search must be >= 1");
+  const auto t_start = std::chrono::steady_clock::now();
+  if (S.n_scenes > 1) {
+    system_solve_batched(S, st, cb, user, out, t_start);
+    return;
+  }
+  const double tol = st.newton_tol > 0 ? st.newton_tol : derived_newton_tol(S);
+  int64_t n_free = 0;
+  DBuf<double> eps_ref;  // run-start positions anchor every support radius (solver.hpp:146)
+  setup_solve(S, n_free, eps_ref);
+  const int64_t n = S.n_dof;
   out->total_newton_iters = 0;
   out->total_rebuilds = 0;
   out->total_pcg_iters = 0;
@@ -1148,6 +1856,41 @@ int gmcp_system_add_body(gmcp_system* sys, const double* verts, int64_t nv, cons
     S.el_built = false;
     return GMCP_OK;
   });
+}
+
+int gmcp_system_set_vertex_scenes(gmcp_system* sys, const int32_t* scene, int64_t n_vertices) {
+  return sguard([&] {
+    if (!sys) throw StatusError(GMCP_ERR_ARG, "null system");
+    SystemImpl& S = sys->s;
+    if (!scene) {
+      S.vscene.clear();
+      S.scene_voff.clear();
+      S.n_scenes = 1;
+      return GMCP_OK;
+    }
+    if (n_vertices != S.n_dof / 3) throw StatusError(GMCP_ERR_ARG, "vertex scenes: one id per system vertex");
+    std::vector<int64_t> voff{0};
+    for (int64_t v = 0; v < n_vertices; ++v) {
+      if (scene[v] < 0 || (v > 0 && scene[v] < scene[v - 1]) || (v == 0 && scene[0] != 0) ||
+          (v > 0 && scene[v] > scene[v - 1] + 1))
+        throw StatusError(GMCP_ERR_ARG, "vertex scenes: ids must be 0, 1, ... in contiguous vertex ranges");
+      if (v > 0 && scene[v] != scene[v - 1]) voff.push_back(v);
+    }
+    voff.push_back(n_vertices);
+    for (const Body& b : S.bodies)
+      if (scene[b.offset] != scene[b.offset + b.nv - 1])
+        throw StatusError(GMCP_ERR_ARG, "vertex scenes: a body spans two scenes");
+    S.vscene.assign(scene, scene + n_vertices);
+    S.scene_voff = voff;
+    S.n_scenes = (int32_t)voff.size() - 1;
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_scene_newton_iters(const gmcp_system* sys, int64_t* out) {
+  if (!sys || !out) return GMCP_ERR_ARG;
+  for (size_t k = 0; k < sys->s.scene_iters.size(); ++k) out[k] = sys->s.scene_iters[k];
+  return GMCP_OK;
 }
 
 int gmcp_system_fix_dofs(gmcp_system* sys, int64_t n, const int64_t* dofs, const double* targets) {

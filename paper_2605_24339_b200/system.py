@@ -125,20 +125,43 @@ class System:
     def num_vertices(self) -> int:
         return self.rest.size // 3
 
-    def add_body(self, mesh: S.TetMesh, youngs: float, poisson: float, name: str = "") -> int:
-        v = np.ascontiguousarray(mesh.vertices, np.float64)
-        t = np.ascontiguousarray(mesh.tets, np.int32)
-        off = C.c_int32()
-        _check(self.L, self.L.gmcp_system_add_body(self.h, _g._p(v), C.c_int64(v.shape[0]), _g._p(t),
-                                                   C.c_int64(t.shape[0]), C.c_double(youngs), C.c_double(poisson),
-                                                   C.byref(off)))
-        self.bodies.append(Body(mesh, youngs, poisson, name, off.value, S.extract_boundary_surface(mesh)))
-        self.rest = np.concatenate([self.rest, v.ravel()])
+    def add_body(self, mesh: S.TetMesh, youngs: float, poisson: float, name: str = "", boundary=None) -> int:
+        return self.add_bodies([(mesh, youngs, poisson, name, boundary)])
+
+    def add_bodies(self, specs) -> int:
+        """Adds (mesh, youngs, poisson, name, boundary or None) bodies in order;
+        returns the index of the last one. Loads and BCs are set afterwards."""
+        parts = [self.rest]
+        for mesh, youngs, poisson, name, boundary in specs:
+            v = np.ascontiguousarray(mesh.vertices, np.float64)
+            t = np.ascontiguousarray(mesh.tets, np.int32)
+            off = C.c_int32()
+            _check(self.L, self.L.gmcp_system_add_body(self.h, _g._p(v), C.c_int64(v.shape[0]), _g._p(t),
+                                                       C.c_int64(t.shape[0]), C.c_double(youngs),
+                                                       C.c_double(poisson), C.byref(off)))
+            self.bodies.append(Body(mesh, youngs, poisson, name, off.value,
+                                    boundary if boundary is not None else S.extract_boundary_surface(mesh)))
+            parts.append(v.ravel())
+        self.rest = np.concatenate(parts)
         self.x = self.rest.copy()
         self.f_ext = np.zeros_like(self.rest)
         self.fixed = np.zeros(self.rest.size, np.uint8)
         self.dirichlet = self.rest.copy()
         return len(self.bodies) - 1
+
+    def set_vertex_scenes(self, scene):
+        """Batched independent scenes (C5): scene id per vertex, 0, 1, ... in
+        contiguous vertex ranges; solve() then converges each scene on its own."""
+        self._scenes = None if scene is None else np.ascontiguousarray(scene, np.int32)
+
+    _scenes = None
+
+    def scene_newton_iters(self) -> np.ndarray:
+        n = 0 if self._scenes is None else int(self._scenes.max()) + 1
+        out = np.zeros(n, np.int64)
+        if n:
+            self.L.gmcp_system_scene_newton_iters(self.h, _g._p(out))
+        return out
 
     def fix_dof(self, gv: int, axis: int, target: float):
         self.fixed[3 * gv + axis] = 1
@@ -157,6 +180,13 @@ class System:
         self.contacts.append((slave, master, p))
         return len(self.contacts) - 1
 
+    def add_contact_surfaces(self, slave: S.ContactSurface, master: S.ContactSurface,
+                             resolved_params: S.BarrierParams) -> int:
+        """A contact pair over prebuilt (global-id) surfaces, e.g. packed scene
+        batches spanning several bodies; params already resolved."""
+        self.contacts.append((slave, master, resolved_params))
+        return len(self.contacts) - 1
+
     def _push(self):
         idx = np.nonzero(self.fixed)[0].astype(np.int64)
         tg = np.ascontiguousarray(self.dirichlet[idx])
@@ -165,6 +195,9 @@ class System:
         _check(self.L, self.L.gmcp_system_set_external_force(self.h, _g._p(f), C.c_int64(f.size)))
         x = np.ascontiguousarray(self.x, np.float64)
         _check(self.L, self.L.gmcp_system_set_positions(self.h, _g._p(x), C.c_int64(x.size)))
+        if self._scenes is not None:
+            _check(self.L, self.L.gmcp_system_set_vertex_scenes(self.h, _g._p(self._scenes),
+                                                                C.c_int64(self._scenes.size)))
         for (slave, master, p) in self.contacts[self._pushed_pairs:]:
             arrs, st = [], []
             for s in (slave, master):
@@ -397,3 +430,49 @@ def run_hertz(cfg: S.HertzConfig | None = None, settings: SolverSettings | None 
     res.peak_rel_err = abs(res.peak - res.oracle.p0) / res.oracle.p0
     res.contact_radius_rel_err = abs(res.contact_radius - res.oracle.alpha_H) / res.oracle.alpha_H
     return res
+
+
+def build_hertz_batch_system(batch: S.SceneBatch, device: int = 0, load_scale: bool = True) -> System:
+    """C5 as one device System: the batch's Hertz scenes (block + shifted ball
+    per scene, quarter-model BCs, pressure Q * q_scale[s] on each ball top),
+    one packed contact pair, per-vertex scene ids. solve() then runs every
+    scene's Newton loop on its own (batched reductions)."""
+    base = batch.base
+    sys_ = System(device)
+    N = base.rest.size // 3
+    nb = base.ball_offset
+    bb, bh = S.extract_boundary_surface(base.block), S.extract_boundary_surface(base.ball)  # same topology per scene
+    specs = []
+    for k in range(batch.scenes.size):
+        specs.append((base.block, base.cfg.E, base.cfg.nu, f"block{k}", bb))
+        bv = batch.rest.reshape(-1, 3)[k * N + nb:(k + 1) * N]
+        specs.append((S.TetMesh(bv.copy(), base.ball.tets), base.cfg.E, base.cfg.nu, f"ball{k}", bh))
+    sys_.add_bodies(specs)
+    cnt = batch.scenes.size
+    dofs = (3 * (base.fixed[:, 0][None, :] + N * np.arange(cnt)[:, None]) + base.fixed[:, 1][None, :]).ravel()
+    sys_.fixed[dofs] = 1
+    sys_.dirichlet[dofs] = sys_.rest[dofs]
+    q = batch.q_scale if load_scale else np.ones(cnt)
+    sys_.f_ext[:] = (base.f_ext.reshape(1, -1) * q[:, None]).ravel()
+    sys_.add_contact_surfaces(batch.slave, batch.master, base.params)
+    sys_.set_vertex_scenes(batch.vscene)
+    return sys_
+
+
+def build_hertz_scene_system(batch: S.SceneBatch, k: int, device: int = 0, load_scale: bool = True) -> System:
+    """Scene k of a batch as its own System (same meshes, BCs and loads)."""
+    base = batch.base
+    sys_ = System(device)
+    N = base.rest.size // 3
+    nb = base.ball_offset
+    ib = sys_.add_body(base.block, base.cfg.E, base.cfg.nu, "block")
+    bv = batch.rest.reshape(-1, 3)[k * N + nb:(k + 1) * N]
+    ih = sys_.add_body(S.TetMesh(bv.copy(), base.ball.tets), base.cfg.E, base.cfg.nu, "ball")
+    dofs = 3 * base.fixed[:, 0] + base.fixed[:, 1]
+    sys_.fixed[dofs] = 1
+    sys_.dirichlet[dofs] = sys_.rest[dofs]
+    sys_.f_ext[:] = base.f_ext * (batch.q_scale[k] if load_scale else 1.0)
+    sl = S.make_contact_surface(sys_.bodies[ib].boundary, 0, base.slave_tris)
+    ms = S.make_contact_surface(sys_.bodies[ih].boundary, nb)
+    sys_.add_contact_surfaces(sl, ms, base.params)
+    return sys_
