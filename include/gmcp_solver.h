@@ -86,6 +86,8 @@ int64_t gmcp_system_launch_count(const gmcp_system* sys);
  * scenes. gmcp_run_stats.total_newton_iters then counts scene-Newton-
  * iterations (sum over scenes); per-step newton_iters counts loop passes. */
 int gmcp_system_set_vertex_scenes(gmcp_system* sys, const int32_t* scene, int64_t n_vertices);
+/* Batched gmcp_system_time_newton: scenes iterated in each timed loop pass. */
+int gmcp_system_timed_active_scenes(const gmcp_system* sys, int64_t* out, int32_t n);
 /* Newton iterations per scene of the last batched solve (out[n_scenes]). */
 int gmcp_system_scene_newton_iters(const gmcp_system* sys, int64_t* out);
 

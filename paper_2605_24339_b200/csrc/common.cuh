@@ -52,7 +52,7 @@ struct DBuf {
     if (m > cap) {
       if (p) GMCP_CUDA(cudaFree(p));
       p = nullptr;
-      cap = m + m / 8 + 16;
+      cap = std::max(m + m / 8 + 16, 2 * cap);  // geometric growth: few reallocations (each one synchronizes)
       GMCP_CUDA(cudaMalloc(&p, cap * sizeof(T)));
     }
     n = m;

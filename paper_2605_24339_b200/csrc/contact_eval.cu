@@ -185,7 +185,7 @@ void splice_samples(Ctx& c, const std::vector<int64_t>& soff_old, const std::vec
   for (int s = 0; s < ns; ++s)
     soff_out[s + 1] = soff_out[s] + (take_new[s] ? soff_new[s + 1] - soff_new[s] : soff_old[s + 1] - soff_old[s]);
   const int64_t n = soff_out[ns];
-  Ctx::Snapshot merged;
+  Ctx::Snapshot& merged = c.spliced;
   size_snapshot(merged, n);
   DBuf<int64_t> moff, so, sn;
   DBuf<uint8_t> take;
@@ -210,8 +210,7 @@ void splice_samples(Ctx& c, const std::vector<int64_t>& soff_old, const std::vec
   c.s_eps.swap(merged.eps);
   c.s_gref.swap(merged.gref);
   c.ns = n;
-  c.sync();  // merged (now the old buffers) is freed at scope exit
-  derive_sample_fields(c);
+  derive_sample_fields(c);  // c.spliced now holds the previous arrays (reused next time)
 }
 
 double run_assembly(Ctx& c, int mode, int64_t* bad) {

@@ -96,7 +96,7 @@ struct Ctx {
     DBuf<int8_t> type;
     DBuf<int32_t> slave, master;
     DBuf<double> beta_s, beta_m, eta, weight, gamma, eps, gref;
-  } snap;
+  } snap, spliced;  // spliced: double buffer for the merged arrays (no per-rebuild allocation)
 
   // reduction scratch
   DBuf<double> red_d;

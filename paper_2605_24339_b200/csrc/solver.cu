@@ -519,6 +519,7 @@ struct SystemImpl {
   int64_t iter_limit = 0;
   std::vector<double> iter_ms;
   std::vector<int64_t> iter_pcg;
+  std::vector<int64_t> iter_active;  // batched: scenes iterated per loop pass
 
   int nv() const { return (int)(n_dof / 3); }
   void sync() { GMCP_CUDA(cudaStreamSynchronize(stream)); }
@@ -1459,6 +1460,8 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
     }
     bool converged = false;
     for (int it = 0; it < st.max_newton_iters; ++it) {
+      const auto t_it = std::chrono::steady_clock::now();
+      const int64_t pcg_before = ss.pcg_iters;
       if (it > 0) assemble(S, lambda);
       scene_resid();
       int n_active = 0;
@@ -1578,6 +1581,17 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
         for (int sc = 0; sc < NS; ++sc) {
           if (!feas[sc]) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
           energy[sc] = el[5 * sc + 3] + ce[sc] - lambda * el[5 * sc + 4];
+        }
+      }
+      if (S.iter_limit > 0) {  // timing mode (gmcp_system_time_newton): loop passes
+        S.sync();
+        S.iter_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_it).count());
+        S.iter_pcg.push_back(ss.pcg_iters - pcg_before);
+        S.iter_active.push_back(n_active);
+        if ((int64_t)S.iter_ms.size() >= S.iter_limit) {
+          S.x.download(S.x_host.data(), n, s);
+          S.sync();
+          return;
         }
       }
     }
@@ -1806,6 +1820,18 @@ extern "C" {
 
 const char* gmcp_system_last_error(void) { return g_serr.c_str(); }
 
+// Grows the per-dof host arrays to n_dof (new entries: positions at rest,
+// no load, free); O(new dofs), so adding many bodies stays linear.
+static void sized_host(SystemImpl& S) {
+  const size_t n = (size_t)S.n_dof, o = S.x_host.size();
+  if (o == n) return;
+  S.x_host.resize(n);
+  S.dirichlet.resize(n);
+  for (size_t d = o; d < n; ++d) S.x_host[d] = S.dirichlet[d] = S.rest[d];
+  S.f_ext.resize(n, 0.0);
+  S.fixed.resize(n, 0);
+}
+
 int gmcp_system_create(int device, gmcp_system** out) {
   return sguard([&] {
     int nd = 0;
@@ -1846,11 +1872,7 @@ int gmcp_system_add_body(gmcp_system* sys, const double* verts, int64_t nv, cons
     b.nv = (int32_t)nv;
     build_operators(b);
     S.rest.insert(S.rest.end(), verts, verts + 3 * nv);
-    S.n_dof = (int64_t)S.rest.size();
-    S.x_host = S.rest;
-    S.f_ext.assign(S.n_dof, 0.0);
-    S.fixed.assign(S.n_dof, 0);
-    S.dirichlet = S.rest;
+    S.n_dof = (int64_t)S.rest.size();  // per-dof host arrays grow lazily (sized_host)
     if (vertex_offset) *vertex_offset = b.offset;
     S.bodies.push_back(std::move(b));
     S.el_built = false;
@@ -1887,6 +1909,12 @@ int gmcp_system_set_vertex_scenes(gmcp_system* sys, const int32_t* scene, int64_
   });
 }
 
+int gmcp_system_timed_active_scenes(const gmcp_system* sys, int64_t* out, int32_t n) {
+  if (!sys || !out) return GMCP_ERR_ARG;
+  for (int32_t k = 0; k < n && k < (int32_t)sys->s.iter_active.size(); ++k) out[k] = sys->s.iter_active[k];
+  return GMCP_OK;
+}
+
 int gmcp_system_scene_newton_iters(const gmcp_system* sys, int64_t* out) {
   if (!sys || !out) return GMCP_ERR_ARG;
   for (size_t k = 0; k < sys->s.scene_iters.size(); ++k) out[k] = sys->s.scene_iters[k];
@@ -1896,6 +1924,7 @@ int gmcp_system_scene_newton_iters(const gmcp_system* sys, int64_t* out) {
 int gmcp_system_fix_dofs(gmcp_system* sys, int64_t n, const int64_t* dofs, const double* targets) {
   return sguard([&] {
     SystemImpl& S = sys->s;
+    sized_host(S);
     for (int64_t i = 0; i < n; ++i) {
       if (dofs[i] < 0 || dofs[i] >= S.n_dof) throw StatusError(GMCP_ERR_ARG, "dof out of range");
       S.fixed[dofs[i]] = 1;
@@ -1908,6 +1937,7 @@ int gmcp_system_fix_dofs(gmcp_system* sys, int64_t n, const int64_t* dofs, const
 int gmcp_system_set_external_force(gmcp_system* sys, const double* f, int64_t n_dof) {
   return sguard([&] {
     SystemImpl& S = sys->s;
+    sized_host(S);
     if (n_dof != S.n_dof) throw StatusError(GMCP_ERR_ARG, "f_ext size mismatch");
     S.f_ext.assign(f, f + n_dof);
     return GMCP_OK;
@@ -1955,6 +1985,7 @@ int gmcp_system_add_contact_pair(gmcp_system* sys, const gmcp_surface* slave, co
 int gmcp_system_solve(gmcp_system* sys, const gmcp_solver_settings* st, gmcp_step_callback cb, void* user,
                       gmcp_run_stats* out) {
   return sguard([&] {
+    sized_host(sys->s);
     system_solve(sys->s, *st, cb, user, out);
     return GMCP_OK;
   });
@@ -1964,10 +1995,12 @@ int gmcp_system_time_newton(gmcp_system* sys, const gmcp_solver_settings* st, in
                             int64_t* pcg_per_iter, int32_t* n_done) {
   return sguard([&] {
     SystemImpl& S = sys->s;
+    sized_host(S);
     if (n_iters < 1) throw StatusError(GMCP_ERR_ARG, "n_iters must be positive");
     S.iter_limit = n_iters;
     S.iter_ms.clear();
     S.iter_pcg.clear();
+    S.iter_active.clear();
     gmcp_run_stats out{};
     try {
       system_solve(S, *st, nullptr, nullptr, &out);
@@ -1988,6 +2021,7 @@ int gmcp_system_time_newton(gmcp_system* sys, const gmcp_solver_settings* st, in
 int gmcp_system_positions(gmcp_system* sys, double* x, int64_t n_dof) {
   return sguard([&] {
     if (n_dof != sys->s.n_dof) throw StatusError(GMCP_ERR_ARG, "size mismatch");
+    sized_host(sys->s);
     std::copy(sys->s.x_host.begin(), sys->s.x_host.end(), x);
     return GMCP_OK;
   });
@@ -1996,6 +2030,7 @@ int gmcp_system_positions(gmcp_system* sys, double* x, int64_t n_dof) {
 int gmcp_system_set_positions(gmcp_system* sys, const double* x, int64_t n_dof) {
   return sguard([&] {
     if (n_dof != sys->s.n_dof) throw StatusError(GMCP_ERR_ARG, "size mismatch");
+    sized_host(sys->s);
     sys->s.x_host.assign(x, x + n_dof);
     return GMCP_OK;
   });

@@ -156,6 +156,12 @@ class System:
 
     _scenes = None
 
+    def timed_active_scenes(self, n: int) -> np.ndarray:
+        """After time_newton on a batched system: scenes iterated per timed pass."""
+        out = np.zeros(n, np.int64)
+        self.L.gmcp_system_timed_active_scenes(self.h, _g._p(out), C.c_int32(n))
+        return out
+
     def scene_newton_iters(self) -> np.ndarray:
         n = 0 if self._scenes is None else int(self._scenes.max()) + 1
         out = np.zeros(n, np.int64)
