@@ -130,6 +130,27 @@ def profiled_traffic():
         return None
 
 
+def pcg_roofline(ps: dict) -> dict:
+    """HBM roofline of one PCG iteration (SpMV + update kernels), device time
+    from CUDA events around the chunk graphs of every PCG solve in the timed
+    Newton run. Algorithmic bytes per iteration:
+      SpMV   76 B per 3x3 block of the merged operand (72 B values + 4 B column)
+             + per row 4 B row pointer and 24 B each of z, p_old, mask read and
+             p_new, q written (124 B);
+      update 24 B each of p, q, x, r read, x, r, z written + 72 B block-Jacobi
+             inverse (240 B per row)."""
+    if not ps["iters"]:
+        return None
+    peak, src = peaks()
+    per_iter = 76 * ps["nnzb"] + (124 + 240) * ps["rows"]
+    ms = ps["ms"] / ps["iters"]
+    achieved = per_iter / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "kernels": "k_spmv_cg + k_update_cg (one PCG iteration)", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "algorithmic_bytes": per_iter,
+            "us_per_iter": 1e3 * ms, "iters_timed": ps["iters"], "operand_blocks": ps["nnzb"], "rows": ps["rows"],
+            "peak_source": src, "clock": "CUDA events around each 16-iteration chunk graph on the solve stream"}
+
+
 def cpu_baseline(scene, samples: dict, x: np.ndarray, seconds_budget: float = 20.0, threads: int | None = None):
     """Reference CPU path (oracle/_ref when built here, else the C restatement)
     timed on this host on a bounded sample of the same workload: whole-slab
@@ -297,23 +318,21 @@ def main():
     value = world * n / (ms_pass / 1e3)
 
     # end-to-end through the public API with host buffers (pinned), per step:
-    # H2D x (3N doubles), assembly, D2H gradient (3N doubles) + energy.
+    # H2D x (3N doubles) and of the caller's gradient (3N doubles, accumulated
+    # into as the reference's add_contact_gradient_hessian does), assembly, D2H
+    # gradient (3N doubles) + energy: one C-ABI call (gmcp_add_gradient_hessian).
     xh = torch.empty(scene.rest.size, dtype=torch.float64, pin_memory=True).numpy()
     gh = torch.empty(scene.rest.size, dtype=torch.float64, pin_memory=True).numpy()
     xh[:] = scene.x_eval
+    gh[:] = 0
     for _ in range(args.warmup):
-        gh[:] = 0
-        gm.add_contact_gradient_hessian  # noqa: B018 (public API name; device path below is the same call)
-        ctx.set_positions(xh)
-        ctx.gradient(gh, hessian=True)
+        ctx.add_gradient(xh, gh, hessian=True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        gh[:] = 0
-        ctx.set_positions(xh)
-        ctx.gradient(gh, hessian=True)
+        ctx.add_gradient(xh, gh, hessian=True)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist:
@@ -341,6 +360,7 @@ def main():
         if dist:
             dist.barrier()
         ms_it, pcg_it = nsys.time_newton(settings, args.newton_iters + 1)
+        ps = nsys.pcg_stats()
         steady = ms_it[1:] if ms_it.size > 1 else ms_it
         t = float(np.mean(steady))
         if dist:
@@ -351,7 +371,8 @@ def main():
                   "pcg_iters": [int(v) for v in pcg_it], "pcg_tol": settings.pcg_tol,
                   "first_iter_includes": "load-step rebuild + one-time elastic BCSR build (excluded from the mean)",
                   "dofs": int(nsys.rest.size), "samples": int(nsys.num_samples(0)),
-                  "clock": "host steady_clock around each iteration (device synchronized)"}
+                  "clock": "host steady_clock around each iteration (device synchronized)",
+                  "pcg_roofline": pcg_roofline(ps)}
         del nsys
 
     # C5: the 1024-scene batched job (C1 Hertz scenes), scenes
@@ -450,10 +471,12 @@ def main():
                          "algorithmic_bytes": ab["k7"], "ms": ms_k7, "peak_source": peak_src},
             "roofline_pass": {"achieved": achieved_pass, "peak": peak, "unit": "GB/s", "frac": achieved_pass / peak,
                               "algorithmic_bytes": ab["pass"], "ms": ms_pass},
-            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(scene.rest.size * 8),
-                    "d2h_bytes_per_step": int(scene.rest.size * 8 + 8),
-                    "path": "gmcp.Context.set_positions + gradient(hessian=True) (C-ABI gmcp_set_positions + "
-                            "gmcp_gradient_hessian), pinned host buffers"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(2 * scene.rest.size * 8),
+                    "d2h_bytes_per_step": int(scene.rest.size * 8 + 40),
+                    "path": "gmcp.Context.add_gradient(x, grad, hessian=True) = one C-ABI call "
+                            "gmcp_add_gradient_hessian (reference add_contact_gradient_hessian(state, params, x, "
+                            "grad, H)): H2D x + caller grad, assembly, D2H grad += g_c + energy/status; pinned "
+                            "host buffers; host wall clock around the loop"},
             "newton": newton,
             "batched": batched,
             "gpu_launches": int(launches),

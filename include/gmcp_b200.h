@@ -20,6 +20,8 @@
  *   gmcp_energy                contact_energy             contact_energy.hpp:110-123
  *   gmcp_gradient              add_contact_gradient       contact_energy.hpp:126-142
  *   gmcp_gradient_hessian      add_contact_gradient_hessian contact_energy.hpp:146-179
+ *   gmcp_add_gradient          add_contact_gradient (x, grad in one call)  :126-142
+ *   gmcp_add_gradient_hessian  add_contact_gradient_hessian (one call)     :146-179
  *   gmcp_step_filter           step_filter                contact_energy.hpp:184-193
  *   gmcp_displacement_cap      displacement_cap           contact_energy.hpp:198-213
  *   gmcp_pressure_field        contact_pressure_field     contact_energy.hpp:225-242
@@ -94,6 +96,17 @@ int gmcp_gradient(gmcp_ctx* ctx, double* grad, double* energy, int64_t* bad);
 /* Gradient plus the Gauss-Newton Hessian assembled into the context's BCSR
  * (3x3 blocks, rows = all N vertices, columns sorted). */
 int gmcp_gradient_hessian(gmcp_ctx* ctx, double* grad, double* energy, int64_t* bad);
+/* One call with the reference signature add_contact_gradient[_hessian](state,
+ * params, x, grad[, H]) (contact_energy.hpp:126-179): positions x (host, 3N)
+ * become the context's positions, grad (host, 3N, may be null) is accumulated
+ * into, the Hessian stays in the context's BCSR. Transfers overlap the
+ * assembly (grad goes up during K7 and comes down while the Hessian blocks are
+ * gathered); one synchronisation. On GMCP_ERR_INFEASIBLE / _DEGENERATE grad is
+ * unchanged. */
+int gmcp_add_gradient(gmcp_ctx* ctx, const double* x, int64_t n_dof, double* grad, double* energy,
+                      int64_t* bad);
+int gmcp_add_gradient_hessian(gmcp_ctx* ctx, const double* x, int64_t n_dof, double* grad,
+                              double* energy, int64_t* bad);
 /* BCSR download: rowptr has N+1 entries; call with null arrays to get nnzb. */
 int gmcp_download_hessian(gmcp_ctx* ctx, int64_t* nnzb, int32_t* rowptr, int32_t* cols,
                           double* vals);

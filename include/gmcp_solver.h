@@ -71,6 +71,12 @@ int gmcp_system_solve(gmcp_system* sys, const gmcp_solver_settings* settings, gm
  * PCG iteration count. */
 int gmcp_system_time_newton(gmcp_system* sys, const gmcp_solver_settings* settings, int32_t n_iters,
                             double* ms_per_iter, int64_t* pcg_per_iter, int32_t* n_done);
+/* PCG measurement (no reference counterpart): device ms and iterations of
+ * the PCG chunk graphs since the last gmcp_system_time_newton started (CUDA
+ * events on the solve stream), and the merged operand's shape (rows, 3x3
+ * blocks). */
+int gmcp_system_pcg_stats(const gmcp_system* sys, double* ev_ms, int64_t* ev_iters, int64_t* n_rows,
+                          int64_t* nnzb);
 int gmcp_system_positions(gmcp_system* sys, double* x, int64_t n_dof);
 int gmcp_system_set_positions(gmcp_system* sys, const double* x, int64_t n_dof);
 int64_t gmcp_system_num_samples(gmcp_system* sys, int32_t pair);

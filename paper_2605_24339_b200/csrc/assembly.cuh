@@ -435,32 +435,63 @@ __device__ __forceinline__ void contrib_block(int role, int b, const double* __r
 constexpr int kGatherThreads = 256;
 
 // Items [0, nnzb) are BCSR blocks (Hess only), then one item per vertex row.
-template <bool Hess>
+// Blocks are visited in the plan's blk_perm order (grouped by kind and
+// contribution count: warp-uniform code path and trip count); the next
+// contribution code is loaded while the current one is summed.
+template <bool Hess, bool Rows = true>
 __global__ void __launch_bounds__(kGatherThreads) k_gather(int64_t nnzb, int32_t n_rows,
                                                            const int32_t* __restrict__ blk_off,
                                                            const int64_t* __restrict__ contrib,
+                                                           const int32_t* __restrict__ blk_perm,
                                                            double* __restrict__ vals,
                                                            const int32_t* __restrict__ ent_off,
                                                            const int64_t* __restrict__ ent,
                                                            const double* __restrict__ partial,
                                                            double* __restrict__ grad) {
   const int64_t nb = Hess ? nnzb : 0;
-  const int64_t items = nb + n_rows;
+  const int64_t items = nb + (Rows ? n_rows : 0);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < items; k += (int64_t)gridDim.x * blockDim.x) {
     if (k < nb) {
+#ifndef K8_PERM
+#define K8_PERM 0
+#endif
+      const int64_t bk = K8_PERM ? blk_perm[k] : k;
       double acc[9];
 #pragma unroll
       for (int q = 0; q < 9; ++q) acc[q] = 0.0;
-      const int c1 = blk_off[k + 1];
-      for (int c = blk_off[k]; c < c1; ++c) {
-        const int64_t code = contrib[c];
+      const int c0 = blk_off[bk], c1 = blk_off[bk + 1];
+#ifndef K8_U2
+#define K8_U2 0
+#endif
+#if K8_U2
+      for (int c = c0; c < c1; c += 2) {  // two contributions' loads in flight, summed in order
+        const bool two = c + 1 < c1;
+        const int64_t code0 = contrib[c], code1 = two ? contrib[c + 1] : code0;
+        double b0[9], b1[9];
+        contrib_block((int)((code0 >> 4) & 0xf), (int)(code0 & 0xf), partial + (code0 >> 12),
+                      (int)((code0 >> 8) & 0xf), b0);
+        contrib_block((int)((code1 >> 4) & 0xf), (int)(code1 & 0xf), partial + (code1 >> 12),
+                      (int)((code1 >> 8) & 0xf), b1);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q] += b0[q];
+        if (two) {
+#pragma unroll
+          for (int q = 0; q < 9; ++q) acc[q] += b1[q];
+        }
+      }
+#else
+      int64_t code = contrib[c0];
+      for (int c = c0; c < c1; ++c) {
+        const int64_t nxt = c + 1 < c1 ? contrib[c + 1] : 0;
         double blk[9];
         contrib_block((int)((code >> 4) & 0xf), (int)(code & 0xf), partial + (code >> 12), (int)((code >> 8) & 0xf),
                       blk);
 #pragma unroll
         for (int q = 0; q < 9; ++q) acc[q] += blk[q];
+        code = nxt;
       }
-      double* out = vals + 9 * k;
+#endif
+      double* out = vals + 9 * bk;
 #pragma unroll
       for (int q = 0; q < 9; ++q) out[q] = acc[q];
     } else {

@@ -301,10 +301,7 @@ static int grad_common(gmcp_ctx* ctx, int mode, double* grad, double* energy, in
     int64_t b = -1;
     if (bad) *bad = -1;
     if (grad) {  // the caller's gradient travels up while the assembly runs
-      if (!c.aux) {
-        GMCP_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
-        GMCP_CUDA(cudaEventCreateWithFlags(&c.aux_done, cudaEventDisableTiming));
-      }
+      c.ensure_aux();
       c.grad_in.resize(std::max<int64_t>(c.n_dof, 1));
       GMCP_CUDA(cudaMemcpyAsync(c.grad_in.p, grad, c.n_dof * sizeof(double), cudaMemcpyHostToDevice, c.aux));
       GMCP_CUDA(cudaEventRecord(c.aux_done, c.aux));
@@ -332,6 +329,41 @@ int gmcp_gradient(gmcp_ctx* ctx, double* grad, double* energy, int64_t* bad) {
 }
 int gmcp_gradient_hessian(gmcp_ctx* ctx, double* grad, double* energy, int64_t* bad) {
   return grad_common(ctx, 1, grad, energy, bad);
+}
+
+static int add_common(gmcp_ctx* ctx, int mode, const double* x, int64_t n_dof, double* grad, double* energy,
+                      int64_t* bad) {
+  return guarded([&] {
+    check_ctx(ctx);
+    need(x != nullptr && n_dof >= 0 && n_dof % 3 == 0, "positions: need 3N doubles");
+    Ctx& c = ctx->c;
+    if (n_dof != c.n_dof) {
+      c.plan.valid = false;
+      c.n_dof = n_dof;
+    }
+    if (c.dx.n != (size_t)n_dof) {
+      c.dx.resize(n_dof);
+      c.dx.zero(c.stream);
+    }
+    int64_t b = -1;
+    if (bad) *bad = -1;
+    try {
+      const double e = run_assembly_host(c, mode, x, grad, &b);
+      if (energy) *energy = e;
+    } catch (const StatusError& se) {
+      if (bad) *bad = se.bad;
+      throw;
+    }
+    return GMCP_OK;
+  });
+}
+
+int gmcp_add_gradient(gmcp_ctx* ctx, const double* x, int64_t n_dof, double* grad, double* energy, int64_t* bad) {
+  return add_common(ctx, 0, x, n_dof, grad, energy, bad);
+}
+int gmcp_add_gradient_hessian(gmcp_ctx* ctx, const double* x, int64_t n_dof, double* grad, double* energy,
+                              int64_t* bad) {
+  return add_common(ctx, 1, x, n_dof, grad, energy, bad);
 }
 
 int gmcp_download_hessian(gmcp_ctx* ctx, int64_t* nnzb, int32_t* rowptr, int32_t* cols, double* vals) {

@@ -56,10 +56,10 @@ void launch_k8(Ctx& c, int mode) {
   const int64_t items = (mode == 1 ? P.nnzb : 0) + P.n_rows;
   const int gb = grid_for(items, kGatherThreads);
   if (mode == 1)
-    k_gather<true><<<gb, kGatherThreads, 0, c.stream>>>(P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.vals.p,
+    k_gather<true><<<gb, kGatherThreads, 0, c.stream>>>(P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p,
                                                         P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   else
-    k_gather<false><<<gb, kGatherThreads, 0, c.stream>>>(P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.vals.p,
+    k_gather<false><<<gb, kGatherThreads, 0, c.stream>>>(P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p,
                                                          P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   ++c.launches;
 }
@@ -234,6 +234,80 @@ double run_assembly(Ctx& c, int mode, int64_t* bad) {
   c.sync();
   const int64_t first_bad = u[0] == ~0ull ? -1 : (int64_t)u[0];
   const int64_t first_deg = u[1] == ~0ull ? -1 : (int64_t)u[1];
+  if (first_deg >= 0 && (first_bad < 0 || first_deg < first_bad))
+    throw StatusError(GMCP_ERR_DEGENERATE, "contact sample on a degenerate slave triangle", first_deg);
+  if (first_bad >= 0) {
+    *bad = first_bad;  // contact_energy.hpp:132-135
+    throw StatusError(GMCP_ERR_INFEASIBLE, "contact sample " + std::to_string(first_bad) + " has non-positive gap",
+                      first_bad);
+  }
+  return e;
+}
+
+__global__ void k_add3(int64_t n, double* __restrict__ dst, const double* __restrict__ a, const double* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = a[i] + b[i];
+}
+
+double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_t* bad) {
+  init_kernels();
+  *bad = -1;
+  const int64_t n = c.n_dof;
+  c.ensure_aux();
+  c.x.upload(x, n, c.stream);
+  if (!c.plan.valid) build_assembly_plan(c);
+  c.grad.resize(std::max<int64_t>(n, 1));
+  c.red_d.resize(kRedBlocks + 8);
+  reset_red(c);
+  if (grad) {  // behind x on the copy engine, overlapping K7
+    c.grad_in.resize(std::max<int64_t>(n, 1));
+    c.grad_sum.resize(std::max<int64_t>(n, 1));
+    GMCP_CUDA(cudaEventRecord(c.x_ready, c.stream));
+    GMCP_CUDA(cudaStreamWaitEvent(c.aux, c.x_ready, 0));
+    GMCP_CUDA(cudaMemcpyAsync(c.grad_in.p, grad, n * sizeof(double), cudaMemcpyHostToDevice, c.aux));
+  }
+  unsigned long long u[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+  double e = 0.0;
+  if (c.ns == 0) {
+    c.grad.zero(c.stream);
+    if (mode == 1 && c.plan.nnzb) GMCP_CUDA(cudaMemsetAsync(c.plan.vals.p, 0, 9 * c.plan.nnzb * sizeof(double), c.stream));
+    GMCP_CUDA(cudaEventRecord(c.rows_done, c.stream));
+  } else {
+    AssemblyPlan& P = c.plan;
+    launch_k7(c, mode);
+    // gradient rows first: grad + g_c goes down while the blocks are gathered
+    k_gather<false><<<grid_for(P.n_rows, kGatherThreads), kGatherThreads, 0, c.stream>>>(
+        P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p,
+        P.partial.p, c.grad.p);
+    GMCP_CUDA(cudaEventRecord(c.rows_done, c.stream));
+    if (mode == 1)
+      k_gather<true, false><<<grid_for(P.nnzb, kGatherThreads), kGatherThreads, 0, c.stream>>>(
+          P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p,
+          P.partial.p, c.grad.p);
+    k_run_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(P.n_runs, P.pbase.p, P.partial.p, c.red_d.p);
+    k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p, kRedBlocks, 1, c.red_d.p + kRedBlocks);
+    c.launches += 4 + (mode == 1);
+  }
+  if (grad) {
+    GMCP_CUDA(cudaStreamWaitEvent(c.aux, c.rows_done, 0));
+    k_add3<<<grid_for(n, 256), 256, 0, c.aux>>>(n, c.grad_sum.p, c.grad_in.p, c.grad.p);
+    ++c.launches;
+    GMCP_CUDA(cudaMemcpyAsync(grad, c.grad_sum.p, n * sizeof(double), cudaMemcpyDeviceToHost, c.aux));
+  }
+  if (c.ns) {
+    GMCP_CUDA(cudaMemcpyAsync(u, c.red_u.p, sizeof u, cudaMemcpyDeviceToHost, c.stream));
+    GMCP_CUDA(cudaMemcpyAsync(&e, c.red_d.p + kRedBlocks, sizeof e, cudaMemcpyDeviceToHost, c.stream));
+  }
+  c.sync();
+  if (grad) GMCP_CUDA(cudaStreamSynchronize(c.aux));
+  GMCP_CUDA(cudaGetLastError());
+  const int64_t first_bad = u[0] == ~0ull ? -1 : (int64_t)u[0];
+  const int64_t first_deg = u[1] == ~0ull ? -1 : (int64_t)u[1];
+  const bool fail = first_bad >= 0 || first_deg >= 0;
+  if (fail && grad) {  // the caller's gradient is left as it was
+    GMCP_CUDA(cudaMemcpyAsync(grad, c.grad_in.p, n * sizeof(double), cudaMemcpyDeviceToHost, c.aux));
+    GMCP_CUDA(cudaStreamSynchronize(c.aux));
+  }
   if (first_deg >= 0 && (first_bad < 0 || first_deg < first_bad))
     throw StatusError(GMCP_ERR_DEGENERATE, "contact sample on a degenerate slave triangle", first_deg);
   if (first_bad >= 0) {

@@ -38,10 +38,13 @@ struct AssemblyPlan {
     DBuf<int32_t> head, hscan, run_cnt, run_first, run_M, rowcnt, ucnt, nuniq;
     DBuf<int64_t> seg_start, psize, ccount, coff, ecount, eoff, cval, cval2, eval, eval2;
     DBuf<unsigned long long> pmask, ckey, ckey2, ekey, ekey2, ukey;
+    DBuf<uint32_t> bkey, bkey2;
+    DBuf<int32_t> bidx;
   } tmp;
   DBuf<double> vals;         // [nnzb][9]
   DBuf<int32_t> row_ent_off; // [N+1]
   DBuf<int32_t> blk_off;     // [nnzb+1] contribution list of each BCSR block
+  DBuf<int32_t> blk_perm;    // [nnzb] K8 visit order: blocks grouped by (kind, contribution count)
   DBuf<int64_t> contrib;     // (pbase << 12) | (M << 8) | (role << 4) | b, ascending run per block
   DBuf<int64_t> row_ent;     // (pbase << 12) | (M << 8) | role ; role < 3 slave i, else 3 + local master
   bool valid = false;
@@ -107,12 +110,25 @@ struct Ctx {
   cudaStream_t aux = nullptr;
   cudaEvent_t aux_done = nullptr;
   DBuf<double> grad_in;
+  // single-call host path (run_assembly_host): positions landed, contact
+  // gradient rows ready, caller gradient + contact gradient
+  cudaEvent_t x_ready = nullptr, rows_done = nullptr;
+  DBuf<double> grad_sum;
   Ctx() = default;
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;
   ~Ctx() {
     if (aux_done) cudaEventDestroy(aux_done);
+    if (x_ready) cudaEventDestroy(x_ready);
+    if (rows_done) cudaEventDestroy(rows_done);
     if (aux) cudaStreamDestroy(aux);
+  }
+  void ensure_aux() {
+    if (aux && x_ready) return;
+    GMCP_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    GMCP_CUDA(cudaEventCreateWithFlags(&aux_done, cudaEventDisableTiming));
+    GMCP_CUDA(cudaEventCreateWithFlags(&x_ready, cudaEventDisableTiming));
+    GMCP_CUDA(cudaEventCreateWithFlags(&rows_done, cudaEventDisableTiming));
   }
 
   DevSamples samples() const {
@@ -149,6 +165,13 @@ void add_into(Ctx& c, double* dst, const double* src, int64_t n);  // dst += src
 void build_assembly_plan(Ctx& c);  // host-side plan from the device samples
 // mode 0: gradient only, 1: gradient + Hessian. Returns energy; throws on infeasible.
 double run_assembly(Ctx& c, int mode, int64_t* bad);
+// One host call of the reference's add_contact_gradient[_hessian](state,
+// params, x, grad[, H]): x (host, 3N) goes up, the caller's grad (host, may be
+// null) travels up behind it while K7 runs, the contact gradient rows are
+// gathered first so grad + g_c comes down while the Hessian blocks are
+// gathered; one synchronisation. On an infeasible / degenerate sample the
+// caller's grad is left as it was and StatusError is thrown.
+double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_t* bad);
 void run_pressure(Ctx& c, gmcp_pressure_record* out_host);
 void run_force_summary(Ctx& c, double* out12);
 void run_kinematics(Ctx& c, double* g, int32_t* nv, int32_t* ids, double* dg);

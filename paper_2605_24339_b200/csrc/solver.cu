@@ -520,6 +520,11 @@ struct SystemImpl {
   std::vector<double> iter_ms;
   std::vector<int64_t> iter_pcg;
   std::vector<int64_t> iter_active;  // batched: scenes iterated per loop pass
+  // PCG chunk graphs timed with CUDA events on the solve stream (since the
+  // last reset): device ms and iterations, for the PCG roofline in bench.py
+  double pcg_ev_ms = 0;
+  int64_t pcg_ev_iters = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   int nv() const { return (int)(n_dof / 3); }
   void sync() { GMCP_CUDA(cudaStreamSynchronize(stream)); }
@@ -861,12 +866,22 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   GMCP_CUDA(cudaStreamEndCapture(S.stream, &graph));
   GMCP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   int it = 0;
+  if (!S.ev0) {
+    GMCP_CUDA(cudaEventCreate(&S.ev0));
+    GMCP_CUDA(cudaEventCreate(&S.ev1));
+  }
   while (it < maxit) {
+    GMCP_CUDA(cudaEventRecord(S.ev0, S.stream));
     GMCP_CUDA(cudaGraphLaunch(exec, S.stream));
+    GMCP_CUDA(cudaEventRecord(S.ev1, S.stream));
     S.launches += 2 * chunk;
     it += chunk;
     GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
     S.sync();
+    float ems = 0;
+    GMCP_CUDA(cudaEventElapsedTime(&ems, S.ev0, S.ev1));
+    S.pcg_ev_ms += ems;
+    S.pcg_ev_iters += chunk;
     if (!std::isfinite(h[4])) {
       cudaGraphExecDestroy(exec);
       cudaGraphDestroy(graph);
@@ -1852,6 +1867,8 @@ void gmcp_system_destroy(gmcp_system* s) {
   cudaStreamSynchronize(s->s.stream);
   cudaStream_t st = s->s.stream;
   for (auto& pr : s->s.pairs) pr->c->stream = nullptr;
+  if (s->s.ev0) cudaEventDestroy(s->s.ev0);
+  if (s->s.ev1) cudaEventDestroy(s->s.ev1);
   delete s;
   cudaStreamDestroy(st);
 }
@@ -1998,6 +2015,8 @@ int gmcp_system_time_newton(gmcp_system* sys, const gmcp_solver_settings* st, in
     sized_host(S);
     if (n_iters < 1) throw StatusError(GMCP_ERR_ARG, "n_iters must be positive");
     S.iter_limit = n_iters;
+    S.pcg_ev_ms = 0;
+    S.pcg_ev_iters = 0;
     S.iter_ms.clear();
     S.iter_pcg.clear();
     S.iter_active.clear();
@@ -2014,6 +2033,18 @@ int gmcp_system_time_newton(gmcp_system* sys, const gmcp_solver_settings* st, in
       ms_per_iter[i] = S.iter_ms[i];
       pcg_per_iter[i] = S.iter_pcg[i];
     }
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_pcg_stats(const gmcp_system* sys, double* ev_ms, int64_t* ev_iters, int64_t* n_rows,
+                          int64_t* nnzb) {
+  return sguard([&] {
+    const SystemImpl& S = sys->s;
+    *ev_ms = S.pcg_ev_ms;
+    *ev_iters = S.pcg_ev_iters;
+    *n_rows = S.nv();
+    *nnzb = S.u_valid ? S.u_nnzb : 0;
     return GMCP_OK;
   });
 }

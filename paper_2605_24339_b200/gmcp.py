@@ -265,6 +265,17 @@ class Context:
         _check(rc, bad.value)
         return e.value
 
+    def add_gradient(self, x, grad=None, hessian=False):
+        """One C-ABI call: positions x, accumulate into grad (host), energy back
+        (gmcp_add_gradient[_hessian]; transfers overlap the assembly)."""
+        x = _f64(x)
+        e, bad = C.c_double(), C.c_int64(-1)
+        fn = self.L.gmcp_add_gradient_hessian if hessian else self.L.gmcp_add_gradient
+        rc = fn(self.h, _p(x), C.c_int64(x.size), _p(grad), C.byref(e), C.byref(bad))
+        _check(rc, bad.value)
+        self.n_dof = x.size
+        return e.value
+
     def download_hessian(self):
         nnzb = C.c_int64()
         _check(self.L.gmcp_download_hessian(self.h, C.byref(nnzb), None, None, None))
@@ -395,14 +406,12 @@ def contact_energy(state: ContactState, params, x) -> float:
 
 
 def add_contact_gradient(state: ContactState, params, x, grad: np.ndarray) -> float:
-    state.ctx.set_positions(x)
-    return state.ctx.gradient(grad, hessian=False)
+    return state.ctx.add_gradient(x, grad, hessian=False)
 
 
 def add_contact_gradient_hessian(state: ContactState, params, x, grad: np.ndarray):
     """Returns (energy, (rowptr, cols, vals)) -- the Gauss-Newton Hessian as BCSR."""
-    state.ctx.set_positions(x)
-    e = state.ctx.gradient(grad, hessian=True)
+    e = state.ctx.add_gradient(x, grad, hessian=True)
     return e, state.ctx.download_hessian()
 
 

@@ -261,6 +261,14 @@ class System:
                                                       C.byref(done)))
         return ms[:done.value], pcg[:done.value]
 
+    def pcg_stats(self) -> dict:
+        """PCG chunk-graph device time (CUDA events) and iterations since the
+        last time_newton started, and the merged operand's shape."""
+        ms = C.c_double()
+        it, rows, nnzb = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(self.L, self.L.gmcp_system_pcg_stats(self.h, C.byref(ms), C.byref(it), C.byref(rows), C.byref(nnzb)))
+        return {"ms": ms.value, "iters": it.value, "rows": rows.value, "nnzb": nnzb.value}
+
     @property
     def launches(self) -> int:
         return int(self.L.gmcp_system_launch_count(self.h))

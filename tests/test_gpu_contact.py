@@ -129,6 +129,45 @@ def test_assembly_is_bitwise_deterministic(gm, orc):
     assert e1 == e2 and np.array_equal(g1, g2) and np.array_equal(v1, v2)
 
 
+def test_single_call_host_path_equals_two_calls(gm, orc):
+    """gmcp_add_gradient_hessian (x and grad in one call, transfers overlapped)
+    gives bitwise the energy, accumulated gradient and Hessian of
+    set_positions + gradient_hessian; the caller's buffer is accumulated into."""
+    name, slave, master, params, rest, x, dx = CASES[3]
+    ctx, ost = _setup(gm, orc, CASES[3])
+    g0 = np.random.default_rng(5).standard_normal(x.size)
+    g1 = g0.copy()
+    ctx.set_positions(x)
+    e1 = ctx.gradient(g1, hessian=True)
+    v1 = ctx.download_hessian()[2].copy()
+    ctx.set_positions(rest)  # the single call must install x itself
+    g2 = g0.copy()
+    e2 = ctx.add_gradient(x, g2, hessian=True)
+    v2 = ctx.download_hessian()[2]
+    assert e1 == e2 and np.array_equal(g1, g2) and np.array_equal(v1, v2)
+    g3 = g0.copy()
+    e3 = ctx.add_gradient(x, g3, hessian=False)
+    assert e3 == e1 and np.array_equal(g3, g1)
+    eo, go = ost.gradient(params, x)
+    assert _rel_inf(g2 - g0, go) <= 1e-8
+
+
+def test_single_call_infeasible_leaves_grad(gm, orc):
+    tp = F.tet_pair()
+    case = ("tp", tp["slave"], tp["master"], tp["params"], tp["rest"], tp["rest"], np.zeros_like(tp["rest"]))
+    ctx, ost = _setup(gm, orc, case)
+    bad = tp["rest"].copy()
+    bad[3 * 4 + 2::3][:4] -= 0.004  # test_contact.cpp:239-260
+    from pyoracle import OracleError
+    with pytest.raises(OracleError) as eo:
+        ost.energy(tp["params"], bad)
+    g = np.arange(bad.size, dtype=np.float64)
+    with pytest.raises(gm.InfeasibleGapError) as ei:
+        ctx.add_gradient(bad, g, hessian=True)
+    assert ei.value.sample_id == eo.value.bad and "non-positive gap" in str(ei.value)
+    assert np.array_equal(g, np.arange(bad.size, dtype=np.float64))
+
+
 def test_infeasible_names_first_sample(gm, orc):
     tp = F.tet_pair()
     case = ("tp", tp["slave"], tp["master"], tp["params"], tp["rest"], tp["rest"], np.zeros_like(tp["rest"]))

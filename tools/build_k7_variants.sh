@@ -8,5 +8,5 @@ F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -
 for spec in "$@"; do
   name=${spec%%=*}; defs=${spec#*=}
   nvcc $F $defs -c contact_eval.cu -o build/contact_eval_$name.o
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libgmcp_b200_$name.so build/capi.o build/contact_eval_$name.o build/exact.o build/sampler.o build/solver.o -lcudart
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libgmcp_b200_$name.so build/capi.o build/contact_eval_$name.o build/exact.o build/plan.o build/sampler.o build/solver.o -lcudart
 done
