@@ -88,13 +88,23 @@ constexpr int kLDS = kStage + 4;      // column stride (doubles): conflict-free 
 
 // Per-warp shared memory: staged U' / V rows (column-major); after the last
 // pass the same space holds C.
+#ifndef K7_TCFIN
+#define K7_TCFIN 1
+#endif
+#ifndef K7_EFOLD
+#define K7_EFOLD 1
+#endif
+constexpr int kLDT = 9;               // T tile row stride (doubles)
 struct RunSmem {
   union {
     struct {
       double u[kUC][kLDS];
       double v[kUC][kLDS];
     };
-    double C[kUC][kUC + 1];
+    struct {
+      double C[kUC][kUC + 1];
+      double T[16][kLDT];  // finalize: F C[0:8][0:8] rows, staged as DMMA A fragments
+    };
   };
   double tm[27];  // T_j(Mbr_i): [i][j][comp]
   double bm[27];  // Mrr A_j^T: [j][p][c]
@@ -134,7 +144,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     DevSamples S, const double* __restrict__ x, int64_t n_runs, const int64_t* __restrict__ run_off,
     const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm_off, const int32_t* __restrict__ lm_ids,
     const uint32_t* __restrict__ li4, const int64_t* __restrict__ pbase, double* __restrict__ partial,
-    unsigned long long* __restrict__ red) {
+    unsigned long long* __restrict__ red, double* __restrict__ warp_energy) {
   __shared__ RunSmem wsm[kRunWarps];
   __shared__ unsigned char pair_tab[kRunMasters + 1][kRunMasters * (kRunMasters + 1) / 2];  // t -> m | l << 4
   for (int q = threadIdx.x; q < (kRunMasters + 1) * kRunMasters; q += blockDim.x) {
@@ -158,6 +168,33 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
                   (c_ss_blk[blk][1] << 9);
     }
   }
+#if K7_TCFIN
+  // Tensor-core finalize, lane-constant parts. F (9 x 6, padded 16 x 8) maps
+  // the moment vector [b0 b1 b2 | r] to the slave gap gradients,
+  // dg_i = F_i [b; r] with F_i = [-n e_i^T | A_i]; this lane holds the DMMA
+  // fragments F[8 mt + g][4 ks + t4]. SS output slot (mt, nt, e) is
+  // SS[8 mt + g][8 nt + 2 t4 + e]: its partial offset (upper entries of the
+  // six stored blocks, 0xff = not stored) and mirror offset (diagonal blocks).
+  uint64_t ss_off = ~0ull, ss_mir = ~0ull;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int ia = 8 * mt + g, jc = 8 * nt + 2 * t4 + e, slot = 4 * mt + 2 * nt + e;
+        if (ia < 9 && jc < 9) {
+          const int i = ia / 3, a = ia % 3, j = jc / 3, c = jc % 3;
+          if (i < j || (i == j && a <= c)) {
+            const int bid = i == 0 ? j : (i == 1 ? 2 + j : 5);
+            const uint64_t clr = ~(0xffull << (8 * slot));
+            ss_off = (ss_off & clr) | ((uint64_t)(9 * bid + 3 * a + c) << (8 * slot));
+            if (i == j && a != c) ss_mir = (ss_mir & clr) | ((uint64_t)(9 * bid + 3 * c + a) << (8 * slot));
+          }
+        }
+      }
+#endif
+  double e_warp = 0;  // this warp's run energies, summed in its run order
   // persistent warps; the next run's metadata loads during this run
   struct Meta {
     int64_t s0, s1, pb;
@@ -188,10 +225,11 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
       const d3 e1 = a1 - a0, e2 = a2 - a0;
       const d3 cr = cross(e1, e2);
       const double cn = norm(cr);
-      const d3 n = cr / cn;
+      const double icn = cn > 0 ? 1.0 / cn : 0.0;
+      const d3 n = icn * cr;
       if (lane == 0) {
         const double gv[19] = {a0.x, a0.y, a0.z, a1.x, a1.y, a1.z, a2.x, a2.y, a2.z, e1.x,
-                               e1.y, e1.z, e2.x, e2.y, e2.z, n.x,  n.y,  n.z,  cn > 0 ? 1.0 / cn : 0.0};
+                               e1.y, e1.z, e2.x, e2.y, e2.z, n.x,  n.y,  n.z,  icn};
 #pragma unroll
         for (int q = 0; q < 19; ++q) W.geo[q] = gv[q];
         if (!(cn > 0)) atomicMin(&red[1], (unsigned long long)s0);
@@ -295,9 +333,103 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     __syncwarp();
     double* P = partial + pb;
     const int colF = 6 + M, colE = 7 + M;
-
     const double* A = W.A;
     const double* nn = W.geo + 15;
+#if K7_TCFIN
+    // T = F C[0:8][0:16] (8 DMMAs): column colF holds the slave gradients
+    // g_i = -Fb_i n + T_i(Fr), columns 6 + m hold a_{m,i} = -Hwb_{m,i} n +
+    // T_i(Hwr_m); then SS = T[:, 0:8] F^T (8 DMMAs) holds all nine slave
+    // blocks F_i Z F_j^T of the moment matrix Z = C[0:6][0:6].
+    double fa[2][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int ia = 8 * mt + g, p = 4 * ks + t4;
+        double v = 0.0;
+        if (ia < 9 && p < 6) {
+          const int i = ia / 3, a = ia % 3;
+          v = p < 3 ? (p == i ? -nn[a] : 0.0) : A[9 * i + 3 * a + (p - 3)];
+        }
+        fa[mt][ks] = v;
+      }
+    double t[2][2][2] = {{{0, 0}, {0, 0}}, {{0, 0}, {0, 0}}};
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const double b0 = C[4 * ks + t4][g], b1 = C[4 * ks + t4][8 + g];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        dmma(t[mt][0][0], t[mt][0][1], fa[mt][ks], b0);
+        dmma(t[mt][1][0], t[mt][1][1], fa[mt][ks], b1);
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int ia = 8 * mt + g, q = 8 * nt + 2 * t4 + e;
+          if (ia < 9) {
+            if (q == colF) P[4 + ia] = t[mt][nt][e];  // [4 + 3 i + a]
+            else if (Hess && q >= 6 && q < colF) P[m_base(M) + 10 * (q - 6) + 1 + ia] = t[mt][nt][e];
+          }
+        }
+    if (Hess) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        W.T[8 * mt + g][2 * t4] = t[mt][0][0];
+        W.T[8 * mt + g][2 * t4 + 1] = t[mt][0][1];
+      }
+      __syncwarp();
+      double sv[2][2][2] = {{{0, 0}, {0, 0}}, {{0, 0}, {0, 0}}};
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const double ta0 = W.T[g][4 * ks + t4], ta1 = W.T[8 + g][4 * ks + t4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma(sv[0][nt][0], sv[0][nt][1], ta0, fa[nt][ks]);
+          dmma(sv[1][nt][0], sv[1][nt][1], ta1, fa[nt][ks]);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int slot = 4 * mt + 2 * nt + e;
+            const int o = (int)((ss_off >> (8 * slot)) & 0xff), om = (int)((ss_mir >> (8 * slot)) & 0xff);
+            if (o != 0xff) P[kSSBase + o] = sv[mt][nt][e];
+            if (om != 0xff) P[kSSBase + om] = sv[mt][nt][e];
+          }
+      for (int tq = lane; tq < M * (M + 1) / 2; tq += 32) {  // master pairs, dense upper triangle
+        const int pr = pair_tab[M][tq];
+        P[pair_base(M) + tq] = C[6 + (pr & 15)][6 + (pr >> 4)];
+      }
+    }
+    const double Erun = C[6 + M][colE];
+    if (lane < 4) P[lane] = lane == 0 ? Erun : nn[lane - 1];
+    if (lane < M) {
+      P[kHdr + lane] = (double)my_lm;  // header: local master ids
+      P[m_base(M) + 10 * lane] = C[6 + lane][colF];  // s_m
+    } else if (lane == 28) {
+      P[kSlv] = (double)sid0;
+    } else if (lane == 29) {
+      P[kSlv + 1] = (double)sid1;
+    } else if (lane == 30) {
+      P[kSlv + 2] = (double)sid2;
+    } else if (lane == 31) {
+      P[kMcnt] = (double)M;
+    }
+    e_warp += Erun;
+    __syncwarp();
+  }
+#if K7_EFOLD
+  if (lane == 0) warp_energy[blockIdx.x * kRunWarps + (threadIdx.x >> 5)] = e_warp;
+#endif
+}
+#else
     // shared pieces of the SS blocks: T_j(Mbr_i) and Mrr A_j^T (upper entries of C)
     if (Hess && lane < 27) {
       const int i = lane / 9, j = (lane / 3) % 3, c = lane % 3;
@@ -363,9 +495,14 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     } else {
       if (lane < M) P[m_base(M) + 10 * lane] = C[6 + lane][colF];
     }
+    e_warp += C[6 + M][colE];
     __syncwarp();
   }
+#if K7_EFOLD
+  if (lane == 0) warp_energy[blockIdx.x * kRunWarps + (threadIdx.x >> 5)] = e_warp;
+#endif
 }
+#endif
 
 // Energy of the pass = sum of run energies in run order.
 __global__ void __launch_bounds__(kRedThreads) k_run_energy(int64_t n_runs, const int64_t* __restrict__ pbase,

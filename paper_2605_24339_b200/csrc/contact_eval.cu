@@ -27,7 +27,10 @@ void init_kernels() {
   done = true;
 }
 
-void launch_k7(Ctx& c, int mode) {
+// K7 warps write their run-energy sums at red_d[kWarpE + warp]
+constexpr int kWarpE = kRedBlocks + 8;
+
+int launch_k7(Ctx& c, int mode) {
   AssemblyPlan& P = c.plan;
   const DevSamples S = c.samples();
   static int resident = 0;  // persistent grid: resident blocks on all SMs
@@ -40,15 +43,34 @@ void launch_k7(Ctx& c, int mode) {
   }
   const int64_t blocks = (P.n_runs + kRunWarps - 1) / kRunWarps;
   const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, resident));
+  c.red_d.resize(kWarpE + (int64_t)gb * kRunWarps);
+  double* we = c.red_d.p + kWarpE;
   if (mode == 1)
     k_run_partials<true><<<gb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
                                                               P.lm_off.p, P.lm_ids.p, P.li4.p, P.pbase.p,
-                                                              P.partial.p, c.red_u.p);
+                                                              P.partial.p, c.red_u.p, we);
   else
     k_run_partials<false><<<gb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
                                                                P.lm_off.p, P.lm_ids.p, P.li4.p, P.pbase.p,
-                                                               P.partial.p, c.red_u.p);
+                                                               P.partial.p, c.red_u.p, we);
   ++c.launches;
+  return gb * kRunWarps;
+}
+
+// energy of the pass -> red_d[kRedBlocks]: the K7 warps' sums in warp order
+// (each warp summed its runs in its own run order), or run energies in run order
+void launch_energy_sum(Ctx& c, int k7_warps) {
+  AssemblyPlan& P = c.plan;
+#if K7_EFOLD
+  (void)P;
+  k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p + kWarpE, k7_warps, 1, c.red_d.p + kRedBlocks);
+  c.launches += 1;
+#else
+  (void)k7_warps;
+  k_run_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(P.n_runs, P.pbase.p, P.partial.p, c.red_d.p);
+  k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p, kRedBlocks, 1, c.red_d.p + kRedBlocks);
+  c.launches += 2;
+#endif
 }
 
 void launch_k8(Ctx& c, int mode) {
@@ -65,12 +87,9 @@ void launch_k8(Ctx& c, int mode) {
 }
 
 void launch_assembly(Ctx& c, int mode) {
-  AssemblyPlan& P = c.plan;
-  launch_k7(c, mode);
+  const int w = launch_k7(c, mode);
   launch_k8(c, mode);
-  k_run_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(P.n_runs, P.pbase.p, P.partial.p, c.red_d.p);
-  k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p, kRedBlocks, 1, c.red_d.p + kRedBlocks);
-  c.launches += 2;
+  launch_energy_sum(c, w);
   GMCP_CUDA(cudaGetLastError());
 }
 
@@ -274,7 +293,7 @@ double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_
     GMCP_CUDA(cudaEventRecord(c.rows_done, c.stream));
   } else {
     AssemblyPlan& P = c.plan;
-    launch_k7(c, mode);
+    const int w = launch_k7(c, mode);
     // gradient rows first: grad + g_c goes down while the blocks are gathered
     k_gather<false><<<grid_for(P.n_rows, kGatherThreads), kGatherThreads, 0, c.stream>>>(
         P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p,
@@ -284,9 +303,8 @@ double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_
       k_gather<true, false><<<grid_for(P.nnzb, kGatherThreads), kGatherThreads, 0, c.stream>>>(
           P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p,
           P.partial.p, c.grad.p);
-    k_run_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(P.n_runs, P.pbase.p, P.partial.p, c.red_d.p);
-    k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p, kRedBlocks, 1, c.red_d.p + kRedBlocks);
-    c.launches += 4 + (mode == 1);
+    launch_energy_sum(c, w);
+    c.launches += 2 + (mode == 1);
   }
   if (grad) {
     GMCP_CUDA(cudaStreamWaitEvent(c.aux, c.rows_done, 0));
