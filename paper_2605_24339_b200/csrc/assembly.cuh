@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     unsigned long long* __restrict__ red, double* __restrict__ warp_energy) {
   __shared__ RunSmem wsm[kRunWarps];
   __shared__ unsigned char pair_tab[kRunMasters + 1][kRunMasters * (kRunMasters + 1) / 2];  // t -> m | l << 4
+  pdl_trigger();  // K8 may take SM slots as K7's persistent blocks retire (it waits for K7's results)
   for (int q = threadIdx.x; q < (kRunMasters + 1) * kRunMasters; q += blockDim.x) {
     const int Mq = q / kRunMasters, m = q % kRunMasters;
     if (m < Mq)
@@ -587,6 +588,8 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(int64_t nnzb, int32_t
                                                            double* __restrict__ grad) {
   const int64_t nb = Hess ? nnzb : 0;
   const int64_t items = nb + (Rows ? n_rows : 0);
+  pdl_trigger();
+  pdl_wait();  // K7's partials
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < items; k += (int64_t)gridDim.x * blockDim.x) {
     if (k < nb) {
 #ifndef K8_PERM

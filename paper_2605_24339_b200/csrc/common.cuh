@@ -151,6 +151,43 @@ struct DevSamples {
 __device__ __forceinline__ int n_master(int8_t t) { return t == GMCP_FACE ? 3 : (t == GMCP_EDGE ? 2 : 1); }
 
 // Warp-level deterministic reductions (fixed butterfly order).
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// launch_pdl may become resident while the previous kernel on the stream is
+// still running; it must execute pdl_wait() before reading that kernel's
+// results. A primary that calls pdl_trigger() lets its dependents launch at
+// once (their blocks take SM slots as the primary's blocks retire).
+#ifndef GMCP_PDL
+#define GMCP_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if GMCP_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if GMCP_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <class... P, class... A>
+void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, cudaStream_t s, A&&... args) {
+#if GMCP_PDL
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  GMCP_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
+#else
+  kernel<<<grid, block, 0, s>>>(std::forward<A>(args)...);
+#endif
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -63,7 +63,8 @@ void launch_energy_sum(Ctx& c, int k7_warps) {
   AssemblyPlan& P = c.plan;
 #if K7_EFOLD
   (void)P;
-  k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p + kWarpE, k7_warps, 1, c.red_d.p + kRedBlocks);
+  launch_pdl(k_sum_parts, 1, kRedThreads, c.stream, (const double*)(c.red_d.p + kWarpE), k7_warps, 1,
+             c.red_d.p + kRedBlocks);
   c.launches += 1;
 #else
   (void)k7_warps;
@@ -78,11 +79,11 @@ void launch_k8(Ctx& c, int mode) {
   const int64_t items = (mode == 1 ? P.nnzb : 0) + P.n_rows;
   const int gb = grid_for(items, kGatherThreads);
   if (mode == 1)
-    k_gather<true><<<gb, kGatherThreads, 0, c.stream>>>(P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p,
-                                                        P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
+    launch_pdl(k_gather<true>, gb, kGatherThreads, c.stream, P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p,
+               P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   else
-    k_gather<false><<<gb, kGatherThreads, 0, c.stream>>>(P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p,
-                                                         P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
+    launch_pdl(k_gather<false>, gb, kGatherThreads, c.stream, P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p,
+               P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   ++c.launches;
 }
 
@@ -295,9 +296,9 @@ double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_
     AssemblyPlan& P = c.plan;
     const int w = launch_k7(c, mode);
     // gradient rows first: grad + g_c goes down while the blocks are gathered
-    k_gather<false><<<grid_for(P.n_rows, kGatherThreads), kGatherThreads, 0, c.stream>>>(
-        P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p,
-        P.partial.p, c.grad.p);
+    launch_pdl(k_gather<false>, grid_for(P.n_rows, kGatherThreads), kGatherThreads, c.stream, P.nnzb, P.n_rows,
+               P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p,
+               c.grad.p);
     GMCP_CUDA(cudaEventRecord(c.rows_done, c.stream));
     if (mode == 1)
       k_gather<true, false><<<grid_for(P.nnzb, kGatherThreads), kGatherThreads, 0, c.stream>>>(

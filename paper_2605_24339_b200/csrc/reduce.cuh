@@ -23,6 +23,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 // Sums `parts` (n values, one per block of a fixed grid) in index order.
 __global__ void k_sum_parts(const double* __restrict__ parts, int n, int stride, double* __restrict__ out) {
   __shared__ double sh[kRedThreads / 32];
+  pdl_wait();  // no-op unless launched with launch_pdl
   for (int c = 0; c < stride; ++c) {
     double v = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) v += parts[(int64_t)i * stride + c];
