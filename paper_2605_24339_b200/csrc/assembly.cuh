@@ -88,12 +88,6 @@ constexpr int kLDS = kStage + 4;      // column stride (doubles): conflict-free 
 
 // Per-warp shared memory: staged U' / V rows (column-major); after the last
 // pass the same space holds C.
-#ifndef K7_TCFIN
-#define K7_TCFIN 1
-#endif
-#ifndef K7_EFOLD
-#define K7_EFOLD 1
-#endif
 constexpr int kLDT = 9;               // T tile row stride (doubles)
 struct RunSmem {
   union {
@@ -106,14 +100,10 @@ struct RunSmem {
       double T[16][kLDT];  // finalize: F C[0:8][0:8] rows, staged as DMMA A fragments
     };
   };
-  double tm[27];  // T_j(Mbr_i): [i][j][comp]
-  double bm[27];  // Mrr A_j^T: [j][p][c]
   double A[27];   // A_i with T_i(v) = A_i v: [i][row][col]
   double geo[19];  // a0 a1 a2 | e1 e2 | n | 1/|c|
 };
 
-__constant__ unsigned char c_ss_entry[45][3];  // (block, a, c) of the 45 unique SS entries
-__constant__ unsigned char c_ss_blk[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
 
 // row a of the matrix A_i with T_i(v) = A_i v
 __device__ __forceinline__ d3 Trow(int i, int a, d3 e1, d3 e2) {
@@ -157,19 +147,6 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
   const int lane = threadIdx.x & 31;
   RunSmem& W = wsm[threadIdx.x >> 5];
   const int g = lane >> 2, t4 = lane & 3;
-  // lane-constant SS entry assignments (o = lane, lane + 32), packed
-  // blk | a << 3 | c << 5 | i << 7 | j << 9
-  int ss_pk[2] = {0, 0};
-#pragma unroll
-  for (int h2 = 0; h2 < 2; ++h2) {
-    const int o = lane + 32 * h2;
-    if (o < 45) {
-      const int blk = c_ss_entry[o][0];
-      ss_pk[h2] = blk | (c_ss_entry[o][1] << 3) | (c_ss_entry[o][2] << 5) | (c_ss_blk[blk][0] << 7) |
-                  (c_ss_blk[blk][1] << 9);
-    }
-  }
-#if K7_TCFIN
   // Tensor-core finalize, lane-constant parts. F (9 x 6, padded 16 x 8) maps
   // the moment vector [b0 b1 b2 | r] to the slave gap gradients,
   // dg_i = F_i [b; r] with F_i = [-n e_i^T | A_i]; this lane holds the DMMA
@@ -194,7 +171,6 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
           }
         }
       }
-#endif
   double e_warp = 0;  // this warp's run energies, summed in its run order
   // persistent warps; the next run's metadata loads during this run
   struct Meta {
@@ -336,7 +312,6 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     const int colF = 6 + M, colE = 7 + M;
     const double* A = W.A;
     const double* nn = W.geo + 15;
-#if K7_TCFIN
     // T = F C[0:8][0:16] (8 DMMAs): column colF holds the slave gradients
     // g_i = -Fb_i n + T_i(Fr), columns 6 + m hold a_{m,i} = -Hwb_{m,i} n +
     // T_i(Hwr_m); then SS = T[:, 0:8] F^T (8 DMMAs) holds all nine slave
@@ -426,95 +401,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     e_warp += Erun;
     __syncwarp();
   }
-#if K7_EFOLD
   if (lane == 0) warp_energy[blockIdx.x * kRunWarps + (threadIdx.x >> 5)] = e_warp;
-#endif
-}
-#else
-    // shared pieces of the SS blocks: T_j(Mbr_i) and Mrr A_j^T (upper entries of C)
-    if (Hess && lane < 27) {
-      const int i = lane / 9, j = (lane / 3) % 3, c = lane % 3;
-      const double* Ajc = A + 9 * j + 3 * c;  // tm[i][j][c] = (A_j Mbr_i)[c]
-      W.tm[lane] = (Ajc[0] * C[i][3] + Ajc[1] * C[i][4]) + Ajc[2] * C[i][5];
-      // bm[i][j][c] = sum_q Mrr[j][q] A_i[c][q]
-      const double* Aic = A + 9 * i + 3 * c;
-      const double m0 = j == 0 ? C[3][3] : (j == 1 ? C[3][4] : C[3][5]);
-      const double m1 = j == 0 ? C[3][4] : (j == 1 ? C[4][4] : C[4][5]);
-      const double m2 = j == 0 ? C[3][5] : (j == 1 ? C[4][5] : C[5][5]);
-      W.bm[lane] = (m0 * Aic[0] + m1 * Aic[1]) + m2 * Aic[2];
-    }
-    __syncwarp();
-    if (lane < 4) {
-      P[lane] = lane == 0 ? C[6 + M][colE] : nn[lane - 1];
-    } else if (lane < 13) {  // slave gradients g_i = -Fb_i n + T_i(Fr)
-      const int i = (lane - 4) / 3, a = (lane - 4) % 3;
-      const double* Aia = A + 9 * i + 3 * a;
-      P[lane] = (-C[i][colF]) * nn[a] + ((Aia[0] * C[3][colF] + Aia[1] * C[4][colF]) + Aia[2] * C[5][colF]);
-    }
-    if (Hess) {
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {  // SS entries
-        if (lane + 32 * h2 < 45) {
-          const int pk = ss_pk[h2];
-          const int blk = pk & 7, a = (pk >> 3) & 3, c = (pk >> 5) & 3, i = (pk >> 7) & 3, j = (pk >> 9) & 3;
-          const double* ra = A + 9 * i + 3 * a;
-          const double* B = W.bm + 9 * j;
-          const double qv = (ra[0] * B[c] + ra[1] * B[3 + c]) + ra[2] * B[6 + c];
-          const double na = nn[a], nc = nn[c];
-          const double mbb = C[i][j];  // i <= j
-          const double v = ((mbb * (na * nc) - na * W.tm[9 * i + 3 * j + c]) - W.tm[9 * j + 3 * i + a] * nc) + qv;
-          P[kSSBase + 9 * blk + 3 * a + c] = v;
-          if (i == j && a != c) P[kSSBase + 9 * blk + 3 * c + a] = v;
-        }
-      }
-      for (int t = lane; t < M * (M + 1) / 2; t += 32) {  // master pairs, dense upper triangle
-        const int pr = pair_tab[M][t];
-        const int m = pr & 15, l = pr >> 4;
-        P[pair_base(M) + t] = C[6 + m][6 + l];
-      }
-    }
-    if (lane < M) P[kHdr + lane] = (double)my_lm;  // header: local master ids
-    else if (lane == 28) P[kSlv] = (double)sid0;
-    else if (lane == 29) P[kSlv + 1] = (double)sid1;
-    else if (lane == 30) P[kSlv + 2] = (double)sid2;
-    else if (lane == 31) P[kMcnt] = (double)M;
-    if (Hess) {
-      for (int t = lane; t < 10 * M; t += 32) {  // s_m, a_{m,i}[a] = -Hwb_{m,i} n_a + (A_i Hwr_m)[a]
-        const int m = t / 10, q = t % 10;
-        const double* Cm = C[6 + m];
-        double val;
-        if (q == 0) {
-          val = Cm[colF];
-        } else {
-          const int i = (q - 1) / 3, a = (q - 1) % 3;
-          const double* Aia = A + 9 * i + 3 * a;
-          const int cm = 6 + m;  // Hwb / Hwr from the upper entries C[b_i][W_m], C[r_c][W_m]
-          val = (-C[i][cm]) * nn[a] + ((Aia[0] * C[3][cm] + Aia[1] * C[4][cm]) + Aia[2] * C[5][cm]);
-        }
-        P[m_base(M) + t] = val;
-      }
-    } else {
-      if (lane < M) P[m_base(M) + 10 * lane] = C[6 + lane][colF];
-    }
-    e_warp += C[6 + M][colE];
-    __syncwarp();
-  }
-#if K7_EFOLD
-  if (lane == 0) warp_energy[blockIdx.x * kRunWarps + (threadIdx.x >> 5)] = e_warp;
-#endif
-}
-#endif
-
-// Energy of the pass = sum of run energies in run order.
-__global__ void __launch_bounds__(kRedThreads) k_run_energy(int64_t n_runs, const int64_t* __restrict__ pbase,
-                                                             const double* __restrict__ partial,
-                                                             double* __restrict__ parts) {
-  __shared__ double sh[kRedThreads / 32];
-  double e = 0;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_runs; r += (int64_t)gridDim.x * blockDim.x)
-    e += partial[pbase[r]];
-  const double v = block_sum<kRedThreads>(e, sh);
-  if (threadIdx.x == 0) parts[blockIdx.x] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -572,15 +459,12 @@ __device__ __forceinline__ void contrib_block(int role, int b, const double* __r
 
 constexpr int kGatherThreads = 256;
 
-// Items [0, nnzb) are BCSR blocks (Hess only), then one item per vertex row.
-// Blocks are visited in the plan's blk_perm order (grouped by kind and
-// contribution count: warp-uniform code path and trip count); the next
-// contribution code is loaded while the current one is summed.
+// Items [0, nnzb) are BCSR blocks (Hess only), then one item per vertex row
+// (Rows). The next contribution code is loaded while the current one is summed.
 template <bool Hess, bool Rows = true>
 __global__ void __launch_bounds__(kGatherThreads) k_gather(int64_t nnzb, int32_t n_rows,
                                                            const int32_t* __restrict__ blk_off,
                                                            const int64_t* __restrict__ contrib,
-                                                           const int32_t* __restrict__ blk_perm,
                                                            double* __restrict__ vals,
                                                            const int32_t* __restrict__ ent_off,
                                                            const int64_t* __restrict__ ent,
@@ -592,34 +476,11 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(int64_t nnzb, int32_t
   pdl_wait();  // K7's partials
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < items; k += (int64_t)gridDim.x * blockDim.x) {
     if (k < nb) {
-#ifndef K8_PERM
-#define K8_PERM 0
-#endif
-      const int64_t bk = K8_PERM ? blk_perm[k] : k;
+      const int64_t bk = k;  // natural order: neighbouring blocks share run partials in L1
       double acc[9];
 #pragma unroll
       for (int q = 0; q < 9; ++q) acc[q] = 0.0;
       const int c0 = blk_off[bk], c1 = blk_off[bk + 1];
-#ifndef K8_U2
-#define K8_U2 0
-#endif
-#if K8_U2
-      for (int c = c0; c < c1; c += 2) {  // two contributions' loads in flight, summed in order
-        const bool two = c + 1 < c1;
-        const int64_t code0 = contrib[c], code1 = two ? contrib[c + 1] : code0;
-        double b0[9], b1[9];
-        contrib_block((int)((code0 >> 4) & 0xf), (int)(code0 & 0xf), partial + (code0 >> 12),
-                      (int)((code0 >> 8) & 0xf), b0);
-        contrib_block((int)((code1 >> 4) & 0xf), (int)(code1 & 0xf), partial + (code1 >> 12),
-                      (int)((code1 >> 8) & 0xf), b1);
-#pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q] += b0[q];
-        if (two) {
-#pragma unroll
-          for (int q = 0; q < 9; ++q) acc[q] += b1[q];
-        }
-      }
-#else
       int64_t code = contrib[c0];
       for (int c = c0; c < c1; ++c) {
         const int64_t nxt = c + 1 < c1 ? contrib[c + 1] : 0;
@@ -630,7 +491,6 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(int64_t nnzb, int32_t
         for (int q = 0; q < 9; ++q) acc[q] += blk[q];
         code = nxt;
       }
-#endif
       double* out = vals + 9 * bk;
 #pragma unroll
       for (int q = 0; q < 9; ++q) out[q] = acc[q];
@@ -657,25 +517,6 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(int64_t nnzb, int32_t
 __global__ void k_flush(double* buf, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     buf[i] = buf[i] * 0.5 + 1.0;
-}
-
-void init_ss_table() {
-  static bool done = false;
-  if (done) return;
-  unsigned char tab[45][3];
-  int k = 0;
-  const int blks[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
-  for (int b = 0; b < 6; ++b)
-    for (int a = 0; a < 3; ++a)
-      for (int cc = 0; cc < 3; ++cc) {
-        if (blks[b][0] == blks[b][1] && cc < a) continue;
-        tab[k][0] = (unsigned char)b;
-        tab[k][1] = (unsigned char)a;
-        tab[k][2] = (unsigned char)cc;
-        ++k;
-      }
-  GMCP_CUDA(cudaMemcpyToSymbol(c_ss_entry, tab, sizeof tab));
-  done = true;
 }
 
 }  // namespace

@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -37,6 +40,34 @@ struct StatusError : std::runtime_error {
       throw ::gmcp_b200::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
+// Device memory comes from the device's stream-ordered pool with an
+// unbounded release threshold: freed blocks stay cached in the process, so
+// the buffers a rebuild regrows or a scratch DBuf re-creates are served
+// without new driver mappings (plain cudaMalloc of fresh memory measured
+// 10-300 ms on the box, in the batched Newton loop's rebuilds). A free first
+// synchronizes the device (as cudaFree does), so no kernel still reads it.
+inline void* dev_alloc(size_t bytes) {
+  static bool configured[64] = {};
+  int dev = 0;
+  GMCP_CUDA(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaMemPool_t pool;
+    GMCP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~0ull;
+    GMCP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    configured[dev] = true;
+  }
+  void* p = nullptr;
+  GMCP_CUDA(cudaMallocAsync(&p, bytes, 0));
+  GMCP_CUDA(cudaStreamSynchronize(0));
+  return p;
+}
+inline void dev_free(void* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, 0);
+}
+
 // Device buffer (grow-only).
 template <class T>
 struct DBuf {
@@ -45,15 +76,21 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() {
-    if (p) cudaFree(p);
-  }
+  ~DBuf() { dev_free(p); }
   void resize(size_t m) {
     if (m > cap) {
-      if (p) GMCP_CUDA(cudaFree(p));
+      static const bool trace = std::getenv("GMCP_TRACE_ALLOC") != nullptr;
+      const auto t0 = std::chrono::steady_clock::now();
+      dev_free(p);
       p = nullptr;
-      cap = std::max(m + m / 8 + 16, 2 * cap);  // geometric growth: few reallocations (each one synchronizes)
-      GMCP_CUDA(cudaMalloc(&p, cap * sizeof(T)));
+      const size_t old = cap;
+      // 1.5x headroom, then doubling: per-rebuild sizes that drift by a few
+      // percent (re-sampled scenes) never regrow a buffer inside a solve
+      cap = std::max(m + m / 2 + 16, 2 * cap);
+      p = static_cast<T*>(dev_alloc(cap * sizeof(T)));
+      if (trace)
+        std::fprintf(stderr, "[gmcp alloc] %zu -> %zu B in %.2f ms\n", old * sizeof(T), cap * sizeof(T),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
     n = m;
   }

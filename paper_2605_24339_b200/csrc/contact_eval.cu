@@ -20,12 +20,6 @@ int grid_for(int64_t n, int threads) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
 }
 
-void init_kernels() {
-  static bool done = false;
-  if (done) return;
-  init_ss_table();
-  done = true;
-}
 
 // K7 warps write their run-energy sums at red_d[kWarpE + warp]
 constexpr int kWarpE = kRedBlocks + 8;
@@ -58,20 +52,11 @@ int launch_k7(Ctx& c, int mode) {
 }
 
 // energy of the pass -> red_d[kRedBlocks]: the K7 warps' sums in warp order
-// (each warp summed its runs in its own run order), or run energies in run order
+// (each warp summed its runs in its own, fixed, run order)
 void launch_energy_sum(Ctx& c, int k7_warps) {
-  AssemblyPlan& P = c.plan;
-#if K7_EFOLD
-  (void)P;
   launch_pdl(k_sum_parts, 1, kRedThreads, c.stream, (const double*)(c.red_d.p + kWarpE), k7_warps, 1,
              c.red_d.p + kRedBlocks);
   c.launches += 1;
-#else
-  (void)k7_warps;
-  k_run_energy<<<kRedBlocks, kRedThreads, 0, c.stream>>>(P.n_runs, P.pbase.p, P.partial.p, c.red_d.p);
-  k_sum_parts<<<1, kRedThreads, 0, c.stream>>>(c.red_d.p, kRedBlocks, 1, c.red_d.p + kRedBlocks);
-  c.launches += 2;
-#endif
 }
 
 void launch_k8(Ctx& c, int mode) {
@@ -80,10 +65,10 @@ void launch_k8(Ctx& c, int mode) {
   const int gb = grid_for(items, kGatherThreads);
   if (mode == 1)
     launch_pdl(k_gather<true>, gb, kGatherThreads, c.stream, P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p,
-               P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
+               P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   else
     launch_pdl(k_gather<false>, gb, kGatherThreads, c.stream, P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p,
-               P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
+               P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p, c.grad.p);
   ++c.launches;
 }
 
@@ -234,7 +219,6 @@ void splice_samples(Ctx& c, const std::vector<int64_t>& soff_old, const std::vec
 }
 
 double run_assembly(Ctx& c, int mode, int64_t* bad) {
-  init_kernels();
   if (!c.plan.valid) build_assembly_plan(c);
   c.grad.resize(std::max<int64_t>(c.n_dof, 1));
   c.red_d.resize(kRedBlocks + 8);
@@ -270,7 +254,6 @@ __global__ void k_add3(int64_t n, double* __restrict__ dst, const double* __rest
 }
 
 double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_t* bad) {
-  init_kernels();
   *bad = -1;
   const int64_t n = c.n_dof;
   c.ensure_aux();
@@ -297,12 +280,12 @@ double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_
     const int w = launch_k7(c, mode);
     // gradient rows first: grad + g_c goes down while the blocks are gathered
     launch_pdl(k_gather<false>, grid_for(P.n_rows, kGatherThreads), kGatherThreads, c.stream, P.nnzb, P.n_rows,
-               P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p,
+               P.blk_off.p, P.contrib.p, P.vals.p, P.row_ent_off.p, P.row_ent.p, P.partial.p,
                c.grad.p);
     GMCP_CUDA(cudaEventRecord(c.rows_done, c.stream));
     if (mode == 1)
       k_gather<true, false><<<grid_for(P.nnzb, kGatherThreads), kGatherThreads, 0, c.stream>>>(
-          P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.blk_perm.p, P.vals.p, P.row_ent_off.p, P.row_ent.p,
+          P.nnzb, P.n_rows, P.blk_off.p, P.contrib.p, P.vals.p, P.row_ent_off.p, P.row_ent.p,
           P.partial.p, c.grad.p);
     launch_energy_sum(c, w);
     c.launches += 2 + (mode == 1);
@@ -338,7 +321,6 @@ double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_
 }
 
 void time_assembly(Ctx& c, int reps, int flush_l2, double* ms_pass, double* ms_kernel) {
-  init_kernels();
   if (!c.plan.valid) build_assembly_plan(c);
   c.grad.resize(std::max<int64_t>(c.n_dof, 1));
   c.red_d.resize(kRedBlocks + 8);

@@ -38,13 +38,10 @@ struct AssemblyPlan {
     DBuf<int32_t> head, hscan, run_cnt, run_first, run_M, rowcnt, ucnt, nuniq;
     DBuf<int64_t> seg_start, psize, ccount, coff, ecount, eoff, cval, cval2, eval, eval2;
     DBuf<unsigned long long> pmask, ckey, ckey2, ekey, ekey2, ukey;
-    DBuf<uint32_t> bkey, bkey2;
-    DBuf<int32_t> bidx;
   } tmp;
   DBuf<double> vals;         // [nnzb][9]
   DBuf<int32_t> row_ent_off; // [N+1]
   DBuf<int32_t> blk_off;     // [nnzb+1] contribution list of each BCSR block
-  DBuf<int32_t> blk_perm;    // [nnzb] K8 visit order: blocks grouped by (kind, contribution count)
   DBuf<int64_t> contrib;     // (pbase << 12) | (M << 8) | (role << 4) | b, ascending run per block
   DBuf<int64_t> row_ent;     // (pbase << 12) | (M << 8) | role ; role < 3 slave i, else 3 + local master
   bool valid = false;

@@ -216,20 +216,6 @@ __global__ void k_block_cols(int64_t nnzb, const unsigned long long* __restrict_
     atomicAdd(&rowcnt[(int64_t)(uk[k] >> 32)], 1);  // integer counts: order-free
   }
 }
-// K8 visit order key of block k: kind (slave/master row x slave/master column,
-// the same for every contribution of a block) then contribution count, so a
-// warp's threads take one code path for the same number of contributions
-__global__ void k_block_kind(int64_t nnzb, const int32_t* __restrict__ blk_off, const int64_t* __restrict__ contrib,
-                             uint32_t* __restrict__ key, int32_t* __restrict__ idx) {
-  GRID_LOOP(k, nnzb) {
-    const int64_t code = contrib[blk_off[k]];
-    const uint32_t kind = (((code >> 4) & 0xf) >= 3 ? 2u : 0u) | ((code & 0xf) >= 3 ? 1u : 0u);
-    const uint32_t cnt = (uint32_t)min(blk_off[k + 1] - blk_off[k], 0xffff);
-    key[k] = (kind << 16) | cnt;
-    idx[k] = (int32_t)k;
-  }
-}
-
 __global__ void k_key_rows(int64_t n, const unsigned long long* __restrict__ keys, int32_t* __restrict__ rowcnt) {
   GRID_LOOP(k, n) atomicAdd(&rowcnt[(int64_t)keys[k]], 1);
 }
@@ -368,15 +354,6 @@ void build_assembly_plan(Ctx& c) {
   if (nc > 0) GMCP_CUDA(cudaMemcpyAsync(P.contrib.p, T.cval2.p, nc * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   if (ne > 0) GMCP_CUDA(cudaMemcpyAsync(P.row_ent.p, T.eval2.p, ne * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   P.vals.resize(std::max<int64_t>(9 * nnzb, 1));
-  P.blk_perm.resize(std::max<int64_t>(nnzb, 1));
-  if (nnzb > 0) {
-    T.bkey.resize(nnzb);
-    T.bkey2.resize(nnzb);
-    T.bidx.resize(nnzb);
-    k_block_kind<<<grid_for(nnzb, 256), 256, 0, s>>>(nnzb, P.blk_off.p, P.contrib.p, T.bkey.p, T.bidx.p);
-    ++c.launches;
-    sort_pairs(T.bkey.p, T.bkey2.p, T.bidx.p, P.blk_perm.p, nnzb, s, 18);
-  }
   c.sync();
   GMCP_CUDA(cudaGetLastError());
   P.valid = true;

@@ -1387,22 +1387,40 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
   DBuf<uint8_t> flag_d;
   DBuf<unsigned long long> motion_d;
   std::vector<int64_t> soff_new;
+  static const bool trace_rb = std::getenv("GMCP_TRACE") != nullptr;
   auto rebuild_scenes = [&](int p, const std::vector<uint8_t>& flag) {
     PairRt& pr = *S.pairs[p];
     Ctx& c = *pr.c;
     S.u_valid = false;
+    double tms[6];
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](int k) {
+      if (!trace_rb) return;
+      S.sync();
+      const auto t1 = std::chrono::steady_clock::now();
+      tms[k] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+      t0 = t1;
+    };
     snapshot_samples(c);
+    lap(0);
     int64_t counts[3];
     run_broadphase(c, pr.params.detection_radius, counts);
+    lap(1);
     run_sampler(c, eps_ref.p);
+    lap(2);
     DBuf<int64_t> tmp;
     scene_sample_offsets(c, vscene_d.p, NS, soff_new, tmp);
     std::vector<int64_t> merged;
     splice_samples(c, soff_h[p], soff_new, flag, merged);
     soff_h[p] = merged;
     soff_d[p].upload(merged, s);
+    lap(3);
     c.plan.valid = false;
     build_assembly_plan(c);
+    lap(4);
+    if (trace_rb)
+      std::fprintf(stderr, "[gmcp rebuild] snapshot %.1f broadphase %.1f sampler %.1f splice %.1f plan %.1f ms\n",
+                   tms[0], tms[1], tms[2], tms[3], tms[4]);
     flag_d.upload(flag, s);
     k_sys_scene_refpos<<<grid_for(n, 256), 256, 0, s>>>(n, vscene_d.p, flag_d.p, S.x.p, pr.ref_pos.p);
     ++S.launches;
@@ -1458,6 +1476,15 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
   std::vector<int64_t> deg(NS);
   std::vector<uint8_t> accepted(NS);
   std::vector<double> energy(NS);
+  // GMCP_TRACE=1: per loop pass phase times (device-synchronized) on stderr
+  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+  auto tnow = [&]() {
+    if (trace) S.sync();
+    return std::chrono::steady_clock::now();
+  };
+  auto ms_since = [](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  };
   for (int step = 1; step <= st.load_steps; ++step) {
     const double lambda = (double)step / st.load_steps;
     gmcp_step_stats ss{};
@@ -1490,6 +1517,8 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
       }
       // scene-segmented PCG over the active scenes; scenes that do not reach
       // the tolerance retry with their own diagonal shift (solver.hpp:352-361)
+      const auto t_pcg = tnow();
+      const double ms_asm = ms_since(t_it);
       S.dx.zero(s);
       std::vector<double> rel, shift(NS, 0.0);
       int pit = pcg_batched(S, segT, st.pcg_tol, st.pcg_max_iters, active, shift, rel);
@@ -1519,6 +1548,9 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
       ss.newton_iters += 1;
       for (int sc = 0; sc < NS; ++sc) S.scene_iters[sc] += active[sc];
 
+      const double ms_pcg = ms_since(t_pcg);
+      const auto t_ls = tnow();
+      int n_trials = 0;
       // per-scene step size: min over pairs of min(1, filter, cap)
       for (int sc = 0; sc < NS; ++sc) alpha[sc] = active[sc] ? 1.0 : 0.0;
       for (int p = 0; p < np; ++p) {
@@ -1531,6 +1563,7 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
       scene_el();  // g_el.dx, dx.K dx, f.dx per scene
       for (int sc = 0; sc < NS; ++sc) accepted[sc] = !active[sc];
       for (int ls = 0; ls < st.max_line_search; ++ls) {
+        ++n_trials;
         alpha_d.upload(alpha, s);
         k_sys_scene_axpy<<<gn, 256, 0, s>>>(n, vscene_d.p, alpha_d.p, S.x.p, S.dx.p, S.xtry.p);
         ++S.launches;
@@ -1563,6 +1596,9 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
         if (!accepted[sc])
           throw StatusError(GMCP_ERR_SOLVER, "load step " + std::to_string(step) + ", scene " + std::to_string(sc) +
                                                  ": line search failed to find a feasible decrease");
+      const double ms_ls = ms_since(t_ls);
+      const auto t_rb = tnow();
+      int n_flag_total = 0;
       // re-sample the scenes whose vertices outran their frozen sampling
       // (solver.hpp:201-209, per scene)
       bool rebuild = false;
@@ -1587,6 +1623,7 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
           rebuild_scenes(p, flag);
           rebuild = true;
         }
+        n_flag_total += nflag;
       }
       if (rebuild) {
         ss.rebuilds += 1;
@@ -1598,6 +1635,11 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
           energy[sc] = el[5 * sc + 3] + ce[sc] - lambda * el[5 * sc + 4];
         }
       }
+      if (trace)
+        std::fprintf(stderr,
+                     "[gmcp batched] step %d it %d active %d: assemble+resid %.2f ms, pcg %.2f ms (%d it), "
+                     "alpha+line search %.2f ms (%d trials), rebuild %.2f ms (%d scenes)\n",
+                     step, it, n_active, ms_asm, ms_pcg, pit, ms_ls, n_trials, ms_since(t_rb), n_flag_total);
       if (S.iter_limit > 0) {  // timing mode (gmcp_system_time_newton): loop passes
         S.sync();
         S.iter_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_it).count());
