@@ -144,8 +144,12 @@ class Device {
   }
   // Uploads st unless it is the state uploaded last (same object, same size).
   void bind(const ContactState& st, const BarrierParams& p, const VecX& x) {
-    params(p);
     positions(x);
+    bind_state(st, p);
+  }
+  // params + samples only (the single-call entries take x themselves)
+  void bind_state(const ContactState& st, const BarrierParams& p) {
+    params(p);
     if (&st != bound_ || st.samples.size() != bound_n_) {
       detail::SampleArrays a;
       a.from(st);
@@ -236,10 +240,10 @@ inline Real contact_energy(Device& d, const ContactState& st, const BarrierParam
 
 inline Real add_contact_gradient(Device& d, const ContactState& st, const BarrierParams& p, const VecX& x,
                                  VecX& grad) {
-  d.bind(st, p, x);
+  d.bind_state(st, p);
   Real e = 0;
   int64_t bad = -1;
-  const int rc = gmcp_gradient(d.raw(), grad.data(), &e, &bad);
+  const int rc = gmcp_add_gradient(d.raw(), x.data(), (int64_t)x.size(), grad.data(), &e, &bad);
   if (rc) detail::rethrow(rc, gmcp_last_error(), (long)bad);
   return e;
 }
@@ -248,10 +252,10 @@ inline Real add_contact_gradient(Device& d, const ContactState& st, const Barrie
 // device keeps the BCSR for the device-resident solver.
 inline Real add_contact_gradient_hessian(Device& d, const ContactState& st, const BarrierParams& p, const VecX& x,
                                          VecX& grad, std::vector<Eigen::Triplet<Real>>& H) {
-  d.bind(st, p, x);
+  d.bind_state(st, p);
   Real e = 0;
   int64_t bad = -1;
-  const int rc = gmcp_gradient_hessian(d.raw(), grad.data(), &e, &bad);
+  const int rc = gmcp_add_gradient_hessian(d.raw(), x.data(), (int64_t)x.size(), grad.data(), &e, &bad);
   if (rc) detail::rethrow(rc, gmcp_last_error(), (long)bad);
   int64_t nnzb = 0;
   detail::check(gmcp_download_hessian(d.raw(), &nnzb, nullptr, nullptr, nullptr));
