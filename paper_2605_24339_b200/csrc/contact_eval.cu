@@ -10,6 +10,7 @@
 #include <numeric>
 
 #include "assembly.cuh"
+#include "cubutil.cuh"
 
 namespace gmcp_b200 {
 
@@ -84,6 +85,16 @@ void launch_assembly(Ctx& c, int mode) {
 // ===========================================================================
 // host entry points
 
+__global__ void k_face_flags(int64_t n, const int8_t* __restrict__ type, int64_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = type[i] == GMCP_FACE ? 1 : 0;
+}
+__global__ void k_face_scatter(int64_t n, const int64_t* __restrict__ flag, const int64_t* __restrict__ pos,
+                               int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[pos[i]] = i;
+}
+
 void derive_sample_fields(Ctx& c) {
   const int64_t n = c.ns;
   c.s_wm.resize(3 * n);
@@ -95,13 +106,23 @@ void derive_sample_fields(Ctx& c) {
     ++c.launches;
     GMCP_CUDA(cudaGetLastError());
   }
-  // face sample index list (pressure-field order)
-  std::vector<int8_t> t = c.s_type.to_host(c.stream);
-  std::vector<int64_t> f;
-  for (int64_t i = 0; i < n; ++i)
-    if (t[i] == GMCP_FACE) f.push_back(i);
-  c.face_idx.upload(f, c.stream);
-  c.face_idx.n = f.size();
+  // face sample index list (pressure-field order): flags, scan, scatter
+  c.face_flag.resize(n + 1);
+  c.face_pos.resize(n + 1);
+  int64_t nf = 0;
+  if (n) {
+    k_face_flags<<<grid_for(n, 256), 256, 0, c.stream>>>(n, c.s_type.p, c.face_flag.p);
+    GMCP_CUDA(cudaMemsetAsync(c.face_flag.p + n, 0, sizeof(int64_t), c.stream));
+    exclusive_scan(c.face_flag.p, c.face_pos.p, n + 1, c.stream);
+    GMCP_CUDA(cudaMemcpyAsync(&nf, c.face_pos.p + n, sizeof nf, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  }
+  c.face_idx.resize(std::max<int64_t>(nf, 1));
+  if (nf) {
+    k_face_scatter<<<grid_for(n, 256), 256, 0, c.stream>>>(n, c.face_flag.p, c.face_pos.p, c.face_idx.p);
+    c.launches += 2;
+  }
+  c.face_idx.n = nf;
   c.plan.valid = false;
 }
 

@@ -74,6 +74,10 @@ struct Ctx {
   // batched scenes: scene id per vertex (empty = one scene)
   DBuf<int32_t> vscene;
   int32_t n_scenes = 1;
+  // batched re-sampling: when set, the broadphase queries only slave
+  // triangles of scenes with scene_mask[s] != 0 (the others get no samples)
+  DBuf<uint8_t> scene_mask;
+  bool use_scene_mask = false;
 
   // candidate pairs (CSR per slave tri)
   DBuf<int64_t> pair_off[3];
@@ -86,6 +90,7 @@ struct Ctx {
   DBuf<int32_t> s_slave, s_master;
   DBuf<double> s_beta_s, s_beta_m, s_wm, s_eta, s_weight, s_gamma, s_eps, s_gref, s_coef;
   DBuf<int64_t> face_idx;  // indices of face samples (pressure field order)
+  DBuf<int64_t> face_flag, face_pos;  // derive_sample_fields scratch
 
   AssemblyPlan plan;
 

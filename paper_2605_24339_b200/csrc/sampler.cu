@@ -240,9 +240,14 @@ __global__ void k_query(int32_t nst, const int32_t* __restrict__ stris, const do
                         int n_leaf, const Box* __restrict__ nodes, const int32_t* __restrict__ left,
                         const int32_t* __restrict__ right, const int32_t* __restrict__ sorted_idx,
                         int64_t* __restrict__ cnt, const int64_t* __restrict__ off, int32_t* __restrict__ out,
-                        int* overflow, const int32_t* __restrict__ vscene, const int2* __restrict__ srange) {
+                        int* overflow, const int32_t* __restrict__ vscene, const int2* __restrict__ srange,
+                        const uint8_t* __restrict__ scene_mask) {
   GRID_LOOP(st, nst) {
     const int qs = vscene ? vscene[stris[3 * st]] : -1;  // batched scenes: own scene only
+    if (scene_mask && !scene_mask[qs]) {  // scene not being re-sampled
+      if (!Mode) cnt[st] = 0;
+      continue;
+    }
     Box q = tri_box(x, stris + 3 * st);
     for (int k = 0; k < 3; ++k) {  // Aabb::inflated, core.hpp:77-82
       q.lo[k] = q.lo[k] - r;
@@ -1041,6 +1046,7 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   auto& idx_sorted = B.idx_sorted;
   auto& srange = B.srange;
   // K2: count, scan, emit+sort
+  const uint8_t* smask = vsc && c.use_scene_mask ? c.scene_mask.p : nullptr;
   auto& cnt = RT.cnt;
   auto& ovf = RT.ovf;
   cnt.resize(nst + 1);
@@ -1048,13 +1054,13 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   ovf.resize(1);
   ovf.zero(s);
   k_query<0><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
-                                                 idx_sorted.p, cnt.p, nullptr, nullptr, ovf.p, vsc, srange.p);
+                                                 idx_sorted.p, cnt.p, nullptr, nullptr, ovf.p, vsc, srange.p, smask);
   exclusive_scan(cnt.p, c.pair_off[0].p, nst + 1, s);
   const int64_t ntri = last_of(c.pair_off[0], nst, s);
   c.pair_ids[0].resize(std::max<int64_t>(ntri, 1));
   k_query<1><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
                                                  idx_sorted.p, nullptr, c.pair_off[0].p, c.pair_ids[0].p, ovf.p, vsc,
-                                                 srange.p);
+                                                 srange.p, smask);
   c.pair_ids[0].n = ntri;
   // K3: candidate edges / verts
   auto& tmp_e = RT.tmp_e;

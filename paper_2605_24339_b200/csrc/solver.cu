@@ -1404,9 +1404,18 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
     snapshot_samples(c);
     lap(0);
     int64_t counts[3];
-    run_broadphase(c, pr.params.detection_radius, counts);
-    lap(1);
-    run_sampler(c, eps_ref.p);
+    // sample the flagged scenes only: the others keep their old segments
+    c.scene_mask.upload(flag, s);
+    c.use_scene_mask = true;
+    try {
+      run_broadphase(c, pr.params.detection_radius, counts);
+      lap(1);
+      run_sampler(c, eps_ref.p);
+    } catch (...) {
+      c.use_scene_mask = false;
+      throw;
+    }
+    c.use_scene_mask = false;
     lap(2);
     DBuf<int64_t> tmp;
     scene_sample_offsets(c, vscene_d.p, NS, soff_new, tmp);
