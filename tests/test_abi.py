@@ -1,5 +1,6 @@
 """CPU checks of the drop-in boundary: the C-ABI library loads and exports
-every entry point include/gmcp_b200.h declares (no compute without a GPU)."""
+every entry point include/gmcp_b200.h and include/gmcp_solver.h declare (no
+compute without a GPU)."""
 import ctypes as C
 import os
 import re
@@ -18,7 +19,9 @@ def test_library_exports_every_declared_symbol():
     lib = gmcp.library()
     names = _declared("gmcp_b200.h")
     assert len(names) >= 25
-    missing = [n for n in names if not hasattr(lib, n)]
+    solver = _declared("gmcp_solver.h")
+    assert len(solver) >= 15
+    missing = [n for n in names + solver if not hasattr(lib, n)]
     assert not missing, missing
 
 

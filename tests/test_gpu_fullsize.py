@@ -1,0 +1,111 @@
+"""Parity at the BASELINE.json size: C3, the GelSight pad (slab 155/124 with
+the textured indenter, 1,008,248 mortar samples), the workload bench.py
+measures.
+
+* The rebuild path is compared with the restated oracle (itself pinned
+  bitwise to the compiled reference, tests/test_oracle.py) at full size:
+  every sample field is bitwise equal. The oracle samples C3 in seconds.
+* Energy, gradient and step filter are compared with the oracle at the
+  evaluation state, at the SURVEY.md 8d tolerances.
+* The assembled Hessian is checked through size-independent properties:
+  * exact symmetry (test_contact.cpp:125);
+  * positive semi-definiteness on random directions (Gauss-Newton blocks are
+    rank-1 PSD, test_contact.cpp:127-130);
+  * rigid-translation invariance of energy and gradient, and a zero net
+    contact force sum_v g_v = 0 (test_contact.cpp:137-153);
+  * bitwise determinism of repeated assemblies."""
+import numpy as np
+import pytest
+
+from paper_2605_24339_b200 import scenes as S
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def c3():
+    return S.slab_scene(155, 124, texture_amp=2e-4)
+
+
+@pytest.fixture(scope="module")
+def c3_ctx(c3):
+    from paper_2605_24339_b200 import gmcp as gm
+    ctx = gm.Context(0)
+    ctx.set_params(c3.params)
+    ctx.set_surfaces(c3.slave, c3.master)
+    ctx.set_positions(c3.rest)
+    ctx.broadphase(c3.params.detection_radius)
+    n = ctx.build_samples()
+    assert n == 1008248
+    return ctx
+
+
+def _bcsr_matvec(rowptr, cols, vals, v):
+    rows = np.repeat(np.arange(rowptr.size - 1), np.diff(rowptr))
+    y = np.einsum("kab,kb->ka", vals, v.reshape(-1, 3)[cols])
+    out = np.zeros((rowptr.size - 1, 3))
+    np.add.at(out, rows, y)
+    return out.ravel()
+
+
+def test_c3_samples_energy_gradient_filter_match_oracle(c3, c3_ctx, orc):
+    pairs = orc.candidate_pairs(c3.slave, c3.master, c3.rest, c3.params.detection_radius)
+    ost = orc.contact_state(c3.slave, c3.master, pairs, c3.rest, c3.params)
+    so, sg = ost.samples(), c3_ctx.download_samples()
+    assert len(ost) == sg["type"].size == 1008248
+    for k in so:
+        assert np.array_equal(so[k], sg[k]), k
+    x, dx = c3.x_eval, c3.dx
+    c3_ctx.set_positions(x)
+    c3_ctx.set_step(dx)
+    eo, go = ost.gradient(c3.params, x)
+    g = np.zeros_like(x)
+    e = c3_ctx.gradient(g, hessian=True)
+    assert abs(e - eo) <= TOL * abs(eo)
+    assert np.abs(g - go).max() <= TOL * np.abs(go).max()
+    assert c3_ctx.step_filter() == ost.step_filter(x, dx)  # bit-exact
+    assert c3_ctx.displacement_cap() == ost.displacement_cap(c3.params, x, dx)
+
+
+def test_c3_hessian_symmetric_psd_deterministic(c3, c3_ctx):
+    x = c3.x_eval
+    c3_ctx.set_positions(x)
+    g1 = np.zeros_like(x)
+    e1 = c3_ctx.gradient(g1, hessian=True)
+    rowptr, cols, vals = c3_ctx.download_hessian()
+    vals = vals.copy()
+    assert cols.size > 700000
+    # exact symmetry: block (r, c) is the transpose of block (c, r)
+    rows = np.repeat(np.arange(rowptr.size - 1), np.diff(rowptr))
+    key = rows.astype(np.int64) * (rowptr.size - 1) + cols
+    tkey = cols.astype(np.int64) * (rowptr.size - 1) + rows
+    order = np.argsort(key)
+    pos = order[np.searchsorted(key, tkey, sorter=order)]
+    assert np.array_equal(key[pos], tkey)
+    assert np.array_equal(vals, vals[pos].transpose(0, 2, 1))
+    # PSD on random directions
+    rng = np.random.default_rng(7)
+    hn = np.abs(vals).max()
+    for _ in range(4):
+        v = rng.standard_normal(x.size)
+        assert v @ _bcsr_matvec(rowptr, cols, vals, v) >= -1e-10 * hn * (v @ v)
+    # determinism
+    g2 = np.zeros_like(x)
+    e2 = c3_ctx.gradient(g2, hessian=True)
+    assert e1 == e2 and np.array_equal(g1, g2) and np.array_equal(vals, c3_ctx.download_hessian()[2])
+    # zero net contact force (Newton's third law across the interface)
+    assert np.abs(g1.reshape(-1, 3).sum(axis=0)).max() <= 1e-12 * np.abs(g1).sum()
+
+
+def test_c3_translation_invariance(c3, c3_ctx):
+    x = c3.x_eval
+    t = np.tile([0.125, -0.25, 0.0625], x.size // 3)  # exactly representable shift
+    c3_ctx.set_positions(x)
+    g0 = np.zeros_like(x)
+    e0 = c3_ctx.gradient(g0)
+    c3_ctx.set_positions(x + t)
+    g1 = np.zeros_like(x)
+    e1 = c3_ctx.gradient(g1)
+    assert abs(e1 - e0) <= 1e-9 * abs(e0)
+    assert np.abs(g1 - g0).max() <= 1e-9 * np.abs(g0).max()

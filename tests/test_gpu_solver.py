@@ -149,3 +149,13 @@ def test_newton_budget_raises_solver_error():
         s.solve(SY.SolverSettings(load_steps=1, max_newton_iters=1))
     assert "load step 1" in str(ei.value)
     assert np.isfinite(ei.value.residual)
+
+
+def test_time_newton_reports_pcg_device_time():
+    """gmcp_system_time_newton + gmcp_system_pcg_stats (bench.py's PCG
+    roofline): event-timed PCG chunks, iteration count, operand shape."""
+    s = SY.build_patch_scene()
+    ms, pcg = s.time_newton(SY.SolverSettings(), 3)
+    st = s.pcg_stats()
+    assert ms.size == 3 and st["iters"] >= int(pcg.sum()) > 0
+    assert st["ms"] > 0 and st["rows"] == s.rest.size // 3 and st["nnzb"] > st["rows"]
