@@ -1251,6 +1251,141 @@ struct SegPcgTmp {
   DBuf<int64_t> voff;
 };
 
+// Batched scenes with up to kCtaSceneRows rows each: one CTA runs one scene's
+// whole PCG in a single launch. Scene matrices are independent (block
+// diagonal), so a CTA needs no grid-level synchronisation: per iteration the
+// SpMV (8-lane row groups over the merged BCSR, as k_spmv_cg<8>), the fixed-
+// order block reductions of p.q and (r.z, r.r) and the vector updates are
+// separated by __syncthreads, and the CTA stops at its own convergence. This
+// removes the four whole-batch launches per iteration of the segmented path
+// and lets converged scenes leave the GPU to the others.
+constexpr int kCtaSceneRows = 16384;
+constexpr int kCtaThreads = 128;  // 8 CTAs per SM: all 1024 C5 scenes resident in one wave
+
+__device__ __forceinline__ void cta_sum2(double& a, double& b, double (*sh)[kCtaThreads / 32]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();  // sh free (previous readers done)
+  if (lane == 0) {
+    sh[0][wid] = a;
+    sh[1][wid] = b;
+  }
+  __syncthreads();
+  double s0 = 0, s1 = 0;
+  for (int i = 0; i < kCtaThreads / 32; ++i) {  // every thread, same order: uniform result
+    s0 += sh[0][i];
+    s1 += sh[1][i];
+  }
+  a = s0;
+  b = s1;
+}
+
+// st[8 s + 0] rz, [1] pq, [2] alpha, [3] beta, [4] rr, [5] bb, [6] iterations
+__global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const double* __restrict__ mask,
+                                                          const int64_t* __restrict__ voff,
+                                                          const int32_t* __restrict__ act,
+                                                          const double* __restrict__ shift_s,
+                                                          const double* __restrict__ minv,
+                                                          const double* __restrict__ grad, double* __restrict__ x,
+                                                          double* __restrict__ r, double* __restrict__ z,
+                                                          double* __restrict__ p, double* __restrict__ q,
+                                                          double tol2, int maxit, double* __restrict__ st) {
+  __shared__ double sh[2][kCtaThreads / 32];
+  const int sc = blockIdx.x;
+  if (!act[sc]) return;  // scenes not being solved keep their x (dx)
+  const int v0 = (int)voff[sc], v1 = (int)voff[sc + 1];
+  const double shift = shift_s[sc];
+  // init: x = 0, r = -mask .* grad, z = Minv r, p = z
+  double rz = 0, rr = 0;
+  for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
+    const d3 m = ld3(mask, v), g = ld3(grad, v);
+    const d3 rv = mk3(-m.x * g.x, -m.y * g.y, -m.z * g.z);
+    const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
+    const double ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
+    for (int k = 0; k < 3; ++k) {
+      x[3 * v + k] = 0;
+      r[3 * v + k] = ra[k];
+      z[3 * v + k] = za[k];
+      p[3 * v + k] = za[k];
+    }
+    rz += dot(rv, zv);
+    rr += dot(rv, rv);
+  }
+  cta_sum2(rz, rr, sh);
+  const double bb = rr;
+  int it = 0;
+  double pq = 0, alpha = 0, beta = 0;
+  const int lane = threadIdx.x & 31, sub = lane & 7;
+  while (rr > tol2 * bb && it < maxit) {
+    __syncthreads();  // p complete
+    // q = mask .* ((H + shift I) p); pq
+    double pqa = 0, unused = 0;
+    for (int vb = v0 + (threadIdx.x >> 3); vb - (lane >> 3) < v1; vb += kCtaThreads / 8) {
+      const int v = vb;  // 8 lanes per row; a warp covers 4 rows
+      d3 acc = mk3(0, 0, 0);
+      if (v < v1) acc = row_mv8<8>(M.el, v, p, p, 0.0, sub);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+      }
+      if (sub == 0 && v < v1) {
+        const d3 m = ld3(mask, v), pv = ld3(p, v);
+        if (shift != 0) acc = acc + shift * pv;
+        const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
+        q[3 * v] = y.x;
+        q[3 * v + 1] = y.y;
+        q[3 * v + 2] = y.z;
+        pqa += dot(pv, y);
+      }
+    }
+    cta_sum2(pqa, unused, sh);  // includes the barrier that publishes q
+    pq = pqa;
+    alpha = pq != 0 ? rz / pq : 0.0;
+    // x += alpha p, r -= alpha q, z = Minv r; (r.z, r.r)
+    double rzn = 0, rrn = 0;
+    for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
+      const d3 xv = ld3(x, v) + alpha * ld3(p, v);
+      const d3 rv = ld3(r, v) - alpha * ld3(q, v);
+      const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
+      const double xa[3] = {xv.x, xv.y, xv.z}, ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        x[3 * v + c] = xa[c];
+        r[3 * v + c] = ra[c];
+        z[3 * v + c] = za[c];
+      }
+      rzn += dot(rv, zv);
+      rrn += dot(rv, rv);
+    }
+    cta_sum2(rzn, rrn, sh);
+    beta = rz != 0 ? rzn / rz : 0.0;
+    rz = rzn;
+    rr = rrn;
+    ++it;
+    if (!isfinite(rr)) break;
+    // p = z + beta p (own rows; the barrier at the loop head publishes it)
+    for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
+      const d3 pv = ld3(z, v) + beta * ld3(p, v);
+      p[3 * v] = pv.x;
+      p[3 * v + 1] = pv.y;
+      p[3 * v + 2] = pv.z;
+    }
+  }
+  if (threadIdx.x == 0) {
+    double* o = st + 8 * sc;
+    o[0] = rz;
+    o[1] = pq;
+    o[2] = alpha;
+    o[3] = beta;
+    o[4] = rr;
+    o[5] = bb;
+    o[6] = (double)it;
+  }
+}
+
 // Runs the segmented PCG for the scenes with active[s]; returns iterations of
 // the slowest scene; rel[s] = sqrt(rr_s / bb_s) at exit (0 when bb_s = 0).
 int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::vector<int32_t>& active,
@@ -1264,10 +1399,29 @@ int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::v
   T.act.upload(active, s);
   T.shift.upload(shift, s);
   k_block_jacobi_seg<<<grid_for(nv, 256), 256, 0, s>>>(nv, M, S.mask_d.p, T.vscene.p, T.shift.p, S.minv.p);
+  ++S.launches;
+  int64_t max_rows = 0;
+  for (int sc = 0; sc < NS; ++sc) max_rows = std::max(max_rows, S.scene_voff[sc + 1] - S.scene_voff[sc]);
+  if (max_rows <= kCtaSceneRows && !std::getenv("GMCP_SEG_PCG")) {  // one CTA per scene
+    k_pcg_scene<<<NS, kCtaThreads, 0, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.minv.p, S.grad.p, S.dx.p,
+                                           S.r.p, S.z.p, S.p.p, S.q.p, tol * tol, maxit, T.st.p);
+    ++S.launches;
+    std::vector<double> st = T.st.to_host(s);
+    rel.resize(NS, 0.0);
+    int it_max = 0;
+    for (int sc = 0; sc < NS; ++sc) {
+      if (!active[sc]) continue;
+      if (!std::isfinite(st[8 * sc + 4])) throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
+      rel[sc] = st[8 * sc + 5] > 0 ? std::sqrt(st[8 * sc + 4] / st[8 * sc + 5]) : 0.0;
+      it_max = std::max(it_max, (int)st[8 * sc + 6]);
+    }
+    GMCP_CUDA(cudaGetLastError());
+    return it_max;
+  }
   k_init_seg<<<grid_for(nv, 256), 256, 0, s>>>(nv, T.vscene.p, T.act.p, S.grad.p, S.mask_d.p, S.minv.p, S.dx.p,
                                               S.r.p, S.z.p, S.p.p, T.dv.p);
   k_seg_sums<2><<<NS, kSceneBlk, 0, s>>>(T.voff.p, T.dv.p, nv, 0.0, T.st.p, T.act.p);
-  S.launches += 3;
+  S.launches += 2;
   const double tol2 = tol * tol;
   const int chunk = 16;
   const int lanes = nv / std::max(NS, 1) < kSmallRows ? 8 : 4;
