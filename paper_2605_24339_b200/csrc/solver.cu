@@ -123,6 +123,16 @@ __device__ __forceinline__ d3 row_mv(const Bcsr& A, int v, const double* __restr
 // 8 below kSmallRows rows, where the iteration is latency-bound
 constexpr int kSmallRows = 32768;
 constexpr double kRegularization = 1e-8;  // SolverSettings::regularization (solver.hpp:40)
+// Stagnation = the solve failed (a singular step: e.g. a body held only by
+// contact that is not yet engaged, with a load along the free mode). The
+// reference's LDL^T fails at once there and retries regularized
+// (solver.hpp:352-361); CG instead plateaus at the inconsistent part of the
+// rhs. A solve whose best rr over the last kStagWindow iterations did not
+// halve the best rr before that window, while still above 1e-8 bb, is
+// declared failed, so the regularized retry starts after ~2k iterations
+// rather than pcg_max_iters. Converging solves shrink rr by orders of
+// magnitude per window and never trip it.
+constexpr int kStagWindow = 1024;
 
 // A_vj x for block k, read through the read-only path (either layout)
 __device__ __forceinline__ d3 bmv_ro(const Bcsr& A, int64_t k, d3 p) {
@@ -866,6 +876,7 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   GMCP_CUDA(cudaStreamEndCapture(S.stream, &graph));
   GMCP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   int it = 0;
+  double win_min = INFINITY, prev_min = INFINITY;  // stagnation windows
   if (!S.ev0) {
     GMCP_CUDA(cudaEventCreate(&S.ev0));
     GMCP_CUDA(cudaEventCreate(&S.ev1));
@@ -888,6 +899,12 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
       throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
     }
     if (!(h[4] > target)) break;  // rr <= tol^2 bb
+    win_min = std::min(win_min, h[4]);
+    if (it % kStagWindow == 0) {
+      if (it >= 2 * kStagWindow && !(win_min < 0.5 * prev_min) && h[4] > 1e-8 * bb) break;  // stagnated
+      prev_min = std::min(prev_min, win_min);
+      win_min = INFINITY;
+    }
   }
   cudaGraphExecDestroy(exec);
   cudaGraphDestroy(graph);
@@ -1316,6 +1333,7 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
   const double bb = rr;
   int it = 0;
   double pq = 0, alpha = 0, beta = 0;
+  double win_min = INFINITY, prev_min = INFINITY;  // stagnation windows (kStagWindow)
   const int lane = threadIdx.x & 31, sub = lane & 7;
   while (rr > tol2 * bb && it < maxit) {
     __syncthreads();  // p complete
@@ -1366,6 +1384,12 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
     rr = rrn;
     ++it;
     if (!isfinite(rr)) break;
+    win_min = fmin(win_min, rr);
+    if (it % kStagWindow == 0) {
+      if (it >= 2 * kStagWindow && !(win_min < 0.5 * prev_min) && rr > 1e-8 * bb) break;  // stagnated
+      prev_min = fmin(prev_min, win_min);
+      win_min = INFINITY;
+    }
     // p = z + beta p (own rows; the barrier at the loop head publishes it)
     for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
       const d3 pv = ld3(z, v) + beta * ld3(p, v);
@@ -1414,6 +1438,20 @@ int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::v
       if (!std::isfinite(st[8 * sc + 4])) throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
       rel[sc] = st[8 * sc + 5] > 0 ? std::sqrt(st[8 * sc + 4] / st[8 * sc + 5]) : 0.0;
       it_max = std::max(it_max, (int)st[8 * sc + 6]);
+    }
+    static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+    if (trace) {
+      std::vector<int> its;
+      int failed = 0;
+      for (int sc = 0; sc < NS; ++sc)
+        if (active[sc]) {
+          its.push_back((int)st[8 * sc + 6]);
+          failed += !(rel[sc] <= tol);
+        }
+      std::sort(its.begin(), its.end());
+      if (!its.empty())
+        std::fprintf(stderr, "[gmcp pcg/cta] %zu scenes: iterations min %d median %d max %d, not converged %d\n",
+                     its.size(), its.front(), its[its.size() / 2], its.back(), failed);
     }
     GMCP_CUDA(cudaGetLastError());
     return it_max;
