@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -535,6 +536,13 @@ struct SystemImpl {
   double pcg_ev_ms = 0;
   int64_t pcg_ev_iters = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // instantiated PCG chunk graph and the launch parameters it was captured with
+  struct PcgKey {
+    MatSet M;
+    int nv, lanes, gsp, gup;
+    const void* ptrs[11];
+  } pcg_key;
+  cudaGraphExec_t pcg_exec = nullptr;
 
   int nv() const { return (int)(n_dof / 3); }
   void sync() { GMCP_CUDA(cudaStreamSynchronize(stream)); }
@@ -859,22 +867,52 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   const int lanes = nv < kSmallRows ? 8 : 4;
   const int gsp = std::min(grid_for((int64_t)nv * lanes, kThreads), kBlocks);
   const int gup = std::min(grid_for((int64_t)nv, kThreads), kBlocks);  // one vertex per thread
-  // one chunk of iterations as a CUDA graph (pointers fixed for this solve)
-  cudaGraph_t graph;
-  cudaGraphExec_t exec;
-  GMCP_CUDA(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
-  for (int k = 0; k < chunk; ++k) {  // p ping-pongs between S.p and S.w (chunk is even)
-    double* p_old = (k & 1) ? S.w.p : S.p.p;
-    double* p_new = (k & 1) ? S.p.p : S.w.p;
-    if (lanes == 8)
-      k_spmv_cg<8><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p, S.slot(1));
-    else
-      k_spmv_cg<4><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p, S.slot(1));
-    k_update_cg<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
-                                                    S.slot(2));
+  // one chunk of iterations as a CUDA graph; the instantiated graph is kept
+  // while its launch parameters (operand, vectors, shift, grids) are unchanged,
+  // i.e. across the Newton iterations between rebuilds
+  SystemImpl::PcgKey key;
+  std::memset(&key, 0, sizeof key);
+  key.M = M;
+  key.nv = nv;
+  key.lanes = lanes;
+  key.gsp = gsp;
+  key.gup = gup;
+  const void* ptrs[11] = {S.mask_d.p, S.z.p, S.p.p, S.w.p, S.q.p, S.dx.p, S.r.p, S.minv.p, S.scal.p, S.parts.p,
+                          S.counter.p};
+  std::memcpy(key.ptrs, ptrs, sizeof ptrs);
+  auto same_bcsr = [](const Bcsr& a, const Bcsr& b) {
+    return a.rowptr == b.rowptr && a.cols == b.cols && a.vals == b.vals && a.bs == b.bs && a.cs == b.cs;
+  };
+  auto same_key = [&](const SystemImpl::PcgKey& a, const SystemImpl::PcgKey& b) {
+    if (!same_bcsr(a.M.el, b.M.el) || a.M.np != b.M.np || a.M.shift != b.M.shift) return false;
+    for (int k = 0; k < a.M.np; ++k)
+      if (!same_bcsr(a.M.c[k], b.M.c[k])) return false;
+    return a.nv == b.nv && a.lanes == b.lanes && a.gsp == b.gsp && a.gup == b.gup &&
+           std::memcmp(a.ptrs, b.ptrs, sizeof a.ptrs) == 0;
+  };
+  if (!S.pcg_exec || !same_key(key, S.pcg_key)) {
+    if (S.pcg_exec) cudaGraphExecDestroy(S.pcg_exec);
+    S.pcg_exec = nullptr;
+    cudaGraph_t graph;
+    GMCP_CUDA(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < chunk; ++k) {  // p ping-pongs between S.p and S.w (chunk is even)
+      double* p_old = (k & 1) ? S.w.p : S.p.p;
+      double* p_new = (k & 1) ? S.p.p : S.w.p;
+      if (lanes == 8)
+        k_spmv_cg<8><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
+                                                      S.slot(1));
+      else
+        k_spmv_cg<4><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
+                                                      S.slot(1));
+      k_update_cg<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
+                                                  S.slot(2));
+    }
+    GMCP_CUDA(cudaStreamEndCapture(S.stream, &graph));
+    GMCP_CUDA(cudaGraphInstantiate(&S.pcg_exec, graph, 0));
+    cudaGraphDestroy(graph);
+    S.pcg_key = key;
   }
-  GMCP_CUDA(cudaStreamEndCapture(S.stream, &graph));
-  GMCP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphExec_t exec = S.pcg_exec;
   int it = 0;
   double win_min = INFINITY, prev_min = INFINITY;  // stagnation windows
   if (!S.ev0) {
@@ -893,11 +931,7 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
     GMCP_CUDA(cudaEventElapsedTime(&ems, S.ev0, S.ev1));
     S.pcg_ev_ms += ems;
     S.pcg_ev_iters += chunk;
-    if (!std::isfinite(h[4])) {
-      cudaGraphExecDestroy(exec);
-      cudaGraphDestroy(graph);
-      throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
-    }
+    if (!std::isfinite(h[4])) throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
     if (!(h[4] > target)) break;  // rr <= tol^2 bb
     win_min = std::min(win_min, h[4]);
     if (it % kStagWindow == 0) {
@@ -906,8 +940,6 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
       win_min = INFINITY;
     }
   }
-  cudaGraphExecDestroy(exec);
-  cudaGraphDestroy(graph);
   *rel_out = std::sqrt(h[4] / bb);
   GMCP_CUDA(cudaGetLastError());
   return it;
@@ -2110,6 +2142,7 @@ void gmcp_system_destroy(gmcp_system* s) {
   cudaStreamSynchronize(s->s.stream);
   cudaStream_t st = s->s.stream;
   for (auto& pr : s->s.pairs) pr->c->stream = nullptr;
+  if (s->s.pcg_exec) cudaGraphExecDestroy(s->s.pcg_exec);
   if (s->s.ev0) cudaEventDestroy(s->s.ev0);
   if (s->s.ev1) cudaEventDestroy(s->s.ev1);
   delete s;
