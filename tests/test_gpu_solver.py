@@ -159,3 +159,18 @@ def test_time_newton_reports_pcg_device_time():
     st = s.pcg_stats()
     assert ms.size == 3 and st["iters"] >= int(pcg.sum()) > 0
     assert st["ms"] > 0 and st["rows"] == s.rest.size // 3 and st["nnzb"] > st["rows"]
+
+
+def test_c2_flat_punch_uniform_pressure():
+    """C2: flat punch on the slab pair (slab 50/40, ~106k
+    mortar samples), the make_patch_scene BCs at scale: the non-matching
+    interface transmits the applied pressure uniformly (acceptance criterion 1
+    thresholds, acceptance.cpp:268-272) and balances the load (criterion 9)."""
+    s = SY.build_slab_system(50, 40)
+    st = s.solve(SY.SolverSettings(load_steps=4))
+    assert s.num_samples(0) > 100000
+    assert all(ss.min_gap > 0 and ss.energy_monotone for ss in st.steps)
+    f = s.contact_force_summary(0)
+    assert abs(f[3, 2] - 10.0) <= 0.01 * 10.0
+    zz, spur = SY.patch_stress_metrics(s, 10.0)
+    assert zz <= 1e-2 and spur <= 1e-1
