@@ -317,12 +317,18 @@ double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_
     ++c.launches;
     GMCP_CUDA(cudaMemcpyAsync(grad, c.grad_sum.p, n * sizeof(double), cudaMemcpyDeviceToHost, c.aux));
   }
+  unsigned long long* hu = static_cast<unsigned long long*>(c.host_scalars);  // pinned
+  double* he = reinterpret_cast<double*>(hu + 4);
   if (c.ns) {
-    GMCP_CUDA(cudaMemcpyAsync(u, c.red_u.p, sizeof u, cudaMemcpyDeviceToHost, c.stream));
-    GMCP_CUDA(cudaMemcpyAsync(&e, c.red_d.p + kRedBlocks, sizeof e, cudaMemcpyDeviceToHost, c.stream));
+    GMCP_CUDA(cudaMemcpyAsync(hu, c.red_u.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
+    GMCP_CUDA(cudaMemcpyAsync(he, c.red_d.p + kRedBlocks, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
   }
   c.sync();
   if (grad) GMCP_CUDA(cudaStreamSynchronize(c.aux));
+  if (c.ns) {
+    for (int k = 0; k < 4; ++k) u[k] = hu[k];
+    e = *he;
+  }
   GMCP_CUDA(cudaGetLastError());
   const int64_t first_bad = u[0] == ~0ull ? -1 : (int64_t)u[0];
   const int64_t first_deg = u[1] == ~0ull ? -1 : (int64_t)u[1];

@@ -116,10 +116,12 @@ struct Ctx {
   // gradient rows ready, caller gradient + contact gradient
   cudaEvent_t x_ready = nullptr, rows_done = nullptr;
   DBuf<double> grad_sum;
+  void* host_scalars = nullptr;  // pinned: status words + energy of the single-call path
   Ctx() = default;
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;
   ~Ctx() {
+    if (host_scalars) cudaFreeHost(host_scalars);
     if (aux_done) cudaEventDestroy(aux_done);
     if (x_ready) cudaEventDestroy(x_ready);
     if (rows_done) cudaEventDestroy(rows_done);
@@ -131,6 +133,7 @@ struct Ctx {
     GMCP_CUDA(cudaEventCreateWithFlags(&aux_done, cudaEventDisableTiming));
     GMCP_CUDA(cudaEventCreateWithFlags(&x_ready, cudaEventDisableTiming));
     GMCP_CUDA(cudaEventCreateWithFlags(&rows_done, cudaEventDisableTiming));
+    GMCP_CUDA(cudaMallocHost(&host_scalars, 64));
   }
 
   DevSamples samples() const {

@@ -33,10 +33,12 @@ __global__ void k_sum_parts(const double* __restrict__ parts, int n, int stride,
 }
 
 
+// status words: [0] first infeasible sample, [1] first degenerate, [2] spare
+// (all ~0 = none), [3] = 0; memsets, no pageable host copy
 inline void reset_red(Ctx& c) {
   c.red_u.resize(4);
-  const unsigned long long init[4] = {~0ull, ~0ull, ~0ull, 0ull};
-  GMCP_CUDA(cudaMemcpyAsync(c.red_u.p, init, sizeof init, cudaMemcpyHostToDevice, c.stream));
+  GMCP_CUDA(cudaMemsetAsync(c.red_u.p, 0xff, 3 * sizeof(unsigned long long), c.stream));
+  GMCP_CUDA(cudaMemsetAsync(c.red_u.p + 3, 0, sizeof(unsigned long long), c.stream));
 }
 
 }  // namespace
