@@ -461,8 +461,11 @@ constexpr int kGatherThreads = 256;
 
 // Items [0, nnzb) are BCSR blocks (Hess only), then one item per vertex row
 // (Rows). The next contribution code is loaded while the current one is summed.
+#ifndef K8_MINB
+#define K8_MINB 5  // 48 registers, 40 warps/SM: more loads in flight (pass -3%; 6 and 8 spill)
+#endif
 template <bool Hess, bool Rows = true>
-__global__ void __launch_bounds__(kGatherThreads) k_gather(int64_t nnzb, int32_t n_rows,
+__global__ void __launch_bounds__(kGatherThreads, K8_MINB) k_gather(int64_t nnzb, int32_t n_rows,
                                                            const int32_t* __restrict__ blk_off,
                                                            const int64_t* __restrict__ contrib,
                                                            double* __restrict__ vals,
