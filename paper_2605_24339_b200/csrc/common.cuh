@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -47,15 +48,15 @@ struct StatusError : std::runtime_error {
 // 10-300 ms on the box, in the batched Newton loop's rebuilds). A free first
 // synchronizes the device (as cudaFree does), so no kernel still reads it.
 inline void* dev_alloc(size_t bytes) {
-  static bool configured[64] = {};
+  static std::atomic<bool> configured[64] = {};
   int dev = 0;
   GMCP_CUDA(cudaGetDevice(&dev));
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaMemPool_t pool;
+  if (dev >= 0 && dev < 64 && !configured[dev].load(std::memory_order_acquire)) {
+    cudaMemPool_t pool;  // idempotent: racing threads set the same attribute
     GMCP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t keep = ~0ull;
     GMCP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    configured[dev] = true;
+    configured[dev].store(true, std::memory_order_release);
   }
   void* p = nullptr;
   GMCP_CUDA(cudaMallocAsync(&p, bytes, 0));
