@@ -244,7 +244,11 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
           const d3 a2 = mk3(W.geo[6], W.geo[7], W.geo[8]), n = mk3(W.geo[15], W.geo[16], W.geo[17]);
           const d3 xs = (ub[0] * a0 + ub[1] * a1) + ub[2] * a2;
           d3 xm = mk3(0, 0, 0);
-          for (int j = 0; j < nm; ++j) xm = xm + w[j] * ld3(x, mid[j]);
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {  // branch-free: absent masters have w = 0 (index clamped)
+            const int mj = j < nm ? mid[j] : mid[0];
+            xm = xm + (j < nm ? w[j] : 0.0) * ld3(x, mj);
+          }
           const d3 d = xm - xs;
           const double gap = dot(n, d);
           if (!(gap > 0)) {
@@ -282,10 +286,13 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
           if (lane < rows) W.u[6 + M][row] = 1.0;
           W.v[6 + M][row] = f;
           W.v[7 + M][row] = eb;
-          for (int j = 0; j < nm; ++j) {
-            const int m = (li >> (8 * j)) & 0xff;
-            W.u[6 + m][row] = w[j];
-            W.v[6 + m][row] = h * w[j];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            if (j < nm) {
+              const int m = (li >> (8 * j)) & 0xff;
+              W.u[6 + m][row] = w[j];
+              W.v[6 + m][row] = h * w[j];
+            }
           }
         }
         __syncwarp();
