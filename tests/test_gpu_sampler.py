@@ -72,3 +72,38 @@ def test_distant_bodies_no_candidates():
     sb = S.make_contact_surface(S.extract_boundary_surface(b), a.vertices.shape[0])
     pairs = gm.build_candidate_pairs(sa, sb, rest, 0.01)
     assert pairs.total_candidates() == 0
+
+
+def test_empty_contact_state_through_every_entry():
+    """No candidates -> no samples: every per-iteration entry is well defined
+    on the empty state (the reference's loops simply do nothing): zero energy,
+    the caller's gradient unchanged, an all-zero Hessian, alpha = 1, no
+    pressure records, a zero force summary."""
+    from paper_2605_24339_b200 import gmcp as gm
+    a = S.make_block((1, 1, 1), (1, 1, 1))
+    b = S.make_block((1, 1, 1), (1, 1, 1), (0, 0, 5))
+    rest = np.concatenate([a.vertices.ravel(), b.vertices.ravel()])
+    sa = S.make_contact_surface(S.extract_boundary_surface(a), 0)
+    sb = S.make_contact_surface(S.extract_boundary_surface(b), a.vertices.shape[0])
+    params = S.resolve_barrier_params(S.BarrierParams(), S.mean_edge_length(sa, rest))
+    ctx = gm.Context(0)
+    ctx.set_params(params)
+    ctx.set_surfaces(sa, sb)
+    ctx.set_positions(rest)
+    ctx.broadphase(0.01)
+    assert ctx.build_samples() == 0
+    g0 = np.arange(rest.size, dtype=np.float64)
+    g = g0.copy()
+    assert ctx.add_gradient(rest, g, hessian=True) == 0.0
+    assert np.array_equal(g, g0)
+    g = g0.copy()
+    ctx.set_positions(rest)
+    assert ctx.gradient(g, hessian=True) == 0.0 and np.array_equal(g, g0)
+    _, _, vals = ctx.download_hessian()
+    assert not np.any(vals)
+    e, mg, feas = ctx.try_energy()
+    assert e == 0.0 and feas
+    ctx.set_step(np.full(rest.size, -0.1))
+    assert ctx.step_filter() == 1.0
+    assert ctx.pressure_field()["pressure"].size == 0
+    assert not np.any(ctx.force_summary())
