@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(kGatherThreads, K8_MINB) k_gather(int64_t nnzb
                                                            double* __restrict__ grad) {
   const int64_t nb = Hess ? nnzb : 0;
   const int64_t items = nb + (Rows ? n_rows : 0);
+  __shared__ double stage[kGatherThreads / 32][9 * 32];  // per-warp block-value transpose
   pdl_trigger();
   pdl_wait();  // K7's partials
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < items; k += (int64_t)gridDim.x * blockDim.x) {
@@ -501,9 +502,22 @@ __global__ void __launch_bounds__(kGatherThreads, K8_MINB) k_gather(int64_t nnzb
         for (int q = 0; q < 9; ++q) acc[q] += blk[q];
         code = nxt;
       }
-      double* out = vals + 9 * bk;
+      const int64_t k0 = k - (threadIdx.x & 31);  // the warp's first item (warp-uniform)
+      if (k0 + 31 < nb) {  // whole warp on blocks: transpose through shared memory, coalesced stores
+        double* st = stage[threadIdx.x >> 5];
+        const int lane = threadIdx.x & 31;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) out[q] = acc[q];
+        for (int q = 0; q < 9; ++q) st[9 * lane + q] = acc[q];
+        __syncwarp();
+        double* out = vals + 9 * k0;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) out[32 * j + lane] = st[32 * j + lane];
+        __syncwarp();
+      } else {
+        double* out = vals + 9 * bk;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) out[q] = acc[q];
+      }
     } else {
       const int64_t v = k - nb;
       d3 g = mk3(0, 0, 0);
