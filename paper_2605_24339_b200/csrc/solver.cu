@@ -219,19 +219,40 @@ __global__ void __launch_bounds__(kThreads) k_update_cg(int nv, const double* __
                                                         const double* __restrict__ minv, double* scal, RedSlot rs) {
   const double a = scal[2];
   double dots[2] = {0, 0};
-  for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
-    const d3 xv = ld3nc(x, v) + a * ld3nc(p, v);
-    const d3 rv = ld3nc(r, v) - a * ld3nc(q, v);
-    const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
+  // per-warp transpose of the 24-byte-per-thread results: coalesced stores
+  __shared__ double stg[kThreads / 32][3][96];
+  const int lane = threadIdx.x & 31;
+  double(*st)[96] = stg[threadIdx.x >> 5];
+  for (int v = blockIdx.x * kThreads + threadIdx.x; v - lane < nv; v += gridDim.x * kThreads) {
+    const bool in = v < nv;
+    const int vv = in ? v : nv - 1;
+    const d3 xv = ld3nc(x, vv) + a * ld3nc(p, vv);
+    const d3 rv = ld3nc(r, vv) - a * ld3nc(q, vv);
+    const d3 zv = bmv(minv + 9 * (int64_t)vv, rv);
     const double xa[3] = {xv.x, xv.y, xv.z}, ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      x[3 * v + c] = xa[c];
-      r[3 * v + c] = ra[c];
-      z[3 * v + c] = za[c];
+      st[0][3 * lane + c] = xa[c];
+      st[1][3 * lane + c] = ra[c];
+      st[2][3 * lane + c] = za[c];
     }
-    dots[0] += dot(rv, zv);
-    dots[1] += dot(rv, rv);
+    __syncwarp();
+    const int64_t base = 3 * (int64_t)(v - lane);
+    const int64_t lim = 3 * (int64_t)nv - base;  // valid entries of this warp's slice
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int o = 32 * j + lane;
+      if (o < lim) {
+        x[base + o] = st[0][o];
+        r[base + o] = st[1][o];
+        z[base + o] = st[2][o];
+      }
+    }
+    __syncwarp();
+    if (in) {
+      dots[0] += dot(rv, zv);
+      dots[1] += dot(rv, rv);
+    }
   }
   double out[2];
   if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
