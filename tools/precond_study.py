@@ -8,7 +8,8 @@ build_slab_system (system.py): linear elastic K (E = 1000, nu = 0) + the contact
 Gauss-Newton Hessian from the oracle at the slab's evaluation state, Dirichlet
 dofs eliminated by the mask (P H P + I - P).
 
-  python tools/precond_study.py [nb nt [agg]]      (default 50 40 = C2, agg 5)
+  python tools/precond_study.py [nb nt [agg ...]]  (default 50 40 = C2, agg 5 10)
+  python tools/precond_study.py hertz [g ...]      (C1 / one C5 scene, g^3 grid aggregates)
 """
 import os
 import sys
@@ -62,6 +63,59 @@ def build(nb, nt):
     Pm = sp.diags(m)
     A = (Pm @ H @ Pm + sp.diags(1 - m)).tocsr()
     return sl, A, m
+
+
+def build_hertz(refine=0.7):
+    """C1 (one C5 scene): block + ball, the ball lowered so its pole gap is
+    eps_max / 2 (scenes.c5_batch), Dirichlet dofs from the scene."""
+    sc = S.hertz_scene(S.HertzConfig(refine=refine))
+    n = sc.rest.size
+    H = elastic_K(sc.block, 0, n, sc.cfg.E, sc.cfg.nu) + elastic_K(sc.ball, sc.ball_offset, n, sc.cfg.E, sc.cfg.nu)
+    x = sc.rest.reshape(-1, 3).copy()
+    x[sc.ball_offset:, 2] -= sc.cfg.initial_gap - 0.5 * sc.cfg.eps_max
+    x = x.ravel()
+    orc = Oracle("restated")
+    pairs = orc.candidate_pairs(sc.slave, sc.master, sc.rest, sc.params.detection_radius)
+    st = orc.contact_state(sc.slave, sc.master, pairs, sc.rest, sc.params)
+    _, _, brow, bcol, bval, _ = st.gradient_hessian(sc.params, x)
+    bval = np.asarray(bval).reshape(-1, 3, 3)
+    r = (3 * np.asarray(brow)[:, None, None] + np.arange(3)[None, :, None]).repeat(3, 2).ravel()
+    c = (3 * np.asarray(bcol)[:, None, None] + np.arange(3)[None, None, :]).repeat(3, 1).ravel()
+    H = H + sp.csr_matrix((bval.ravel(), (r, c)), shape=(n, n))
+    m = np.ones(n)
+    m[3 * sc.fixed[:, 0] + sc.fixed[:, 1]] = 0
+    Pm = sp.diags(m)
+    A = (Pm @ H @ Pm + sp.diags(1 - m)).tocsr()
+    bodies = [(sc.block, 0), (sc.ball, sc.ball_offset)]
+    return bodies, sc.rest, A, m
+
+
+def grid_coarse_space(bodies, rest, m, g):
+    """Rigid-body modes per aggregate = one cell of a g x g x g grid over each
+    body's bounding box (graded meshes), masked."""
+    r3 = rest.reshape(-1, 3)
+    cols, rows, vals = [], [], []
+    k = 0
+    for mesh, off in bodies:
+        vs_all = off + np.arange(mesh.vertices.shape[0])
+        p = r3[vs_all]
+        lo, hi = p.min(0), p.max(0)
+        cell = np.minimum(((p - lo) / np.maximum(hi - lo, 1e-30) * g).astype(int), g - 1)
+        key = (cell[:, 0] * g + cell[:, 1]) * g + cell[:, 2]
+        for u in np.unique(key):
+            vs = vs_all[key == u]
+            d = r3[vs] - r3[vs].mean(axis=0)
+            modes = [np.tile(np.eye(3)[a], (vs.size, 1)) for a in range(3)]
+            modes += [np.cross(np.eye(3)[a], d) for a in range(3)]
+            for md in modes:
+                dof = (3 * vs[:, None] + np.arange(3)).ravel()
+                val = md.ravel() * m[dof]
+                if np.abs(val).max() > 0:
+                    rows.append(dof)
+                    cols.append(np.full(dof.size, k))
+                    vals.append(val)
+                    k += 1
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(m.size, k))
 
 
 def block_jacobi(A):
@@ -133,7 +187,24 @@ def pcg(A, b, prec, tol=1e-8, maxit=20000):
     return maxit, x
 
 
+def main_hertz(gs):
+    bodies, rest, A, m = build_hertz()
+    print(f"Hertz C1 (refine 0.7): {A.shape[0]} dofs, {A.nnz} nonzeros")
+    b = m * np.random.default_rng(1).standard_normal(A.shape[0])
+    Dj = block_jacobi(A)
+    print(f"block-Jacobi: {pcg(A, b, Dj)[0]} iterations")
+    for g in gs:
+        P = grid_coarse_space(bodies, rest, m, g)
+        lam, Q = np.linalg.eigh((P.T @ A @ P).toarray())
+        keep = lam > 1e-12 * lam.max()
+        Ci = (Q[:, keep] / lam[keep]) @ Q[:, keep].T
+        it2 = pcg(A, b, lambda r, P=P, Ci=Ci: Dj(r) + P @ (Ci @ (P.T @ r)))[0]
+        print(f"two-level additive, {g}^3 grid cells per body ({P.shape[1]} coarse dofs): {it2} iterations")
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "hertz":
+        return main_hertz([int(a) for a in sys.argv[2:]] or [4, 6])
     nb = int(sys.argv[1]) if len(sys.argv) > 1 else 50
     nt = int(sys.argv[2]) if len(sys.argv) > 2 else 40
     aggs = [int(a) for a in sys.argv[3:]] or [5, 10]
