@@ -137,12 +137,13 @@ def pcg_roofline(ps: dict) -> dict:
       SpMV   76 B per 3x3 block of the merged operand (72 B values + 4 B column)
              + per row 4 B row pointer and 24 B each of z, p_old, mask read and
              p_new, q written (124 B);
-      update 24 B each of p, q, x, r read, x, r, z written + 72 B block-Jacobi
-             inverse (240 B per row)."""
+      update 24 B each of p, q, x, r read, x, r, z written, the vertex-pair
+             block-Jacobi rows (3x6 = 144 B) and the partner's r and q (48 B):
+             360 B per row."""
     if not ps["iters"]:
         return None
     peak, src = peaks()
-    per_iter = 76 * ps["nnzb"] + (124 + 240) * ps["rows"]
+    per_iter = 76 * ps["nnzb"] + (124 + 360) * ps["rows"]
     ms = ps["ms"] / ps["iters"]
     achieved = per_iter / (ms / 1e3) / 1e9
     return {"bound": "hbm", "kernels": "k_spmv_cg + k_update_cg (one PCG iteration)", "achieved": achieved,

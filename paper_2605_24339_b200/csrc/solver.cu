@@ -27,6 +27,9 @@ namespace {
 constexpr int kMaxPairs = 4;
 constexpr int kThreads = 256;
 constexpr int kBlocks = 592;  // fixed grid: deterministic reductions
+#ifndef GMCP_PAIR_JACOBI
+#define GMCP_PAIR_JACOBI 1  // vertex-pair 6x6 block-Jacobi for the single-system PCG
+#endif
 
 // ---------------------------------------------------------------------------
 // deterministic single-kernel reductions: per-block partials + "last block"
@@ -260,6 +263,180 @@ __global__ void __launch_bounds__(kThreads) k_update_cg(int nv, const double* __
     scal[3] = rz_old != 0 ? out[0] / rz_old : 0.0;  // beta
     scal[0] = out[0];                                // rz
     scal[4] = out[1];                                // rr
+  }
+}
+
+// Vertex-pair block-Jacobi (6x6): M = blockdiag over the pairs of the masked
+// merged operator restricted to {v, partner}; unpaired vertices keep the 3x3
+// block. Row v of M^-1 is stored as minv2[v] = [ (M^-1)_vv | (M^-1)_vp ]
+// (3x6), so z_v = (M^-1)_vv r_v + (M^-1)_vp r_p. Both vertices of a pair
+// invert the same 6x6 in the same (lower id first) order.
+__device__ __forceinline__ bool get_block(const Bcsr& A, int v, int w, double* d) {
+  int lo = A.rowptr[v], hi = A.rowptr[v + 1];
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A.cols[mid] < w) lo = mid + 1; else hi = mid;
+  }
+  if (!(lo < A.rowptr[v + 1] && A.cols[lo] == w)) return false;
+  const double* b = A.vals + (int64_t)lo * A.bs;
+  for (int q = 0; q < 9; ++q) d[q] = b[q * A.cs];
+  return true;
+}
+__device__ __forceinline__ void add_block(const MatSet& M, int v, int w, double* d) {
+  double t[9];
+  if (get_block(M.el, v, w, t))
+    for (int q = 0; q < 9; ++q) d[q] += t[q];
+  for (int k = 0; k < M.np; ++k)
+    if (get_block(M.c[k], v, w, t))
+      for (int q = 0; q < 9; ++q) d[q] += t[q];
+}
+__global__ void k_pair_jacobi(int nv, MatSet M, const double* __restrict__ mask, const int32_t* __restrict__ pair,
+                              double* __restrict__ minv2) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const int pv = pair[v];
+    const int a = pv < 0 ? v : min(v, pv), b = pv < 0 ? v : max(v, pv);
+    const int n = pv < 0 ? 3 : 6;
+    double G[6][6];
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j) G[i][j] = (i == j && i >= n) ? 1.0 : 0.0;
+    const int ids[2] = {a, b};
+    for (int I = 0; I < n / 3; ++I)
+      for (int J = 0; J < n / 3; ++J) {
+        double d[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        add_block(M, ids[I], ids[J], d);
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) {
+            double g = d[3 * i + j] + (I == J && i == j ? M.shift : 0.0);
+            const double mi = mask[3 * ids[I] + i], mj = mask[3 * ids[J] + j];
+            if (mi == 0 || mj == 0) g = (I == J && i == j) ? 1.0 : 0.0;
+            G[3 * I + i][3 * J + j] = g;
+          }
+      }
+    // Gauss-Jordan inverse (SPD: no pivoting), in place
+    double Inv[6][6];
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j) Inv[i][j] = (i == j) ? 1.0 : 0.0;
+    for (int c = 0; c < 6; ++c) {
+      const double ip = 1.0 / G[c][c];
+      for (int j = 0; j < 6; ++j) {
+        G[c][j] *= ip;
+        Inv[c][j] *= ip;
+      }
+      for (int i = 0; i < 6; ++i)
+        if (i != c) {
+          const double f = G[i][c];
+          for (int j = 0; j < 6; ++j) {
+            G[i][j] -= f * G[c][j];
+            Inv[i][j] -= f * Inv[c][j];
+          }
+        }
+    }
+    const int me = (v == a) ? 0 : 3, ot = 3 - me;
+    double* o = minv2 + 18 * (int64_t)v;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        o[3 * i + j] = Inv[me + i][me + j];
+        o[9 + 3 * i + j] = pv < 0 ? 0.0 : Inv[me + i][ot + j];
+      }
+  }
+}
+
+__device__ __forceinline__ d3 pair_apply(const double* __restrict__ minv2, int v, d3 rv, d3 rp) {
+  const double* m = minv2 + 18 * (int64_t)v;
+  return bmv(m, rv) + bmv(m + 9, rp);
+}
+
+// K9b with the pair preconditioner: r ping-pongs (r_in -> r_out) so a thread
+// can form its partner's new residual r_p = r_in[p] - alpha q[p] itself.
+__global__ void __launch_bounds__(kThreads) k_update_cg_pair(int nv, const double* __restrict__ p,
+                                                             const double* __restrict__ q, double* __restrict__ x,
+                                                             const double* __restrict__ r_in,
+                                                             double* __restrict__ r_out, double* __restrict__ z,
+                                                             const double* __restrict__ minv2,
+                                                             const int32_t* __restrict__ pair, double* scal,
+                                                             RedSlot rs) {
+  const double a = scal[2];
+  double dots[2] = {0, 0};
+  __shared__ double stg[kThreads / 32][3][96];
+  const int lane = threadIdx.x & 31;
+  double(*st)[96] = stg[threadIdx.x >> 5];
+  for (int v = blockIdx.x * kThreads + threadIdx.x; v - lane < nv; v += gridDim.x * kThreads) {
+    const bool in = v < nv;
+    const int vv = in ? v : nv - 1;
+    const d3 xv = ld3nc(x, vv) + a * ld3nc(p, vv);
+    const d3 rv = ld3nc(r_in, vv) - a * ld3nc(q, vv);
+    const int pp = pair[vv];
+    const d3 rp = pp < 0 ? mk3(0, 0, 0) : ld3nc(r_in, pp) - a * ld3nc(q, pp);
+    const d3 zv = pair_apply(minv2, vv, rv, rp);
+    const double xa[3] = {xv.x, xv.y, xv.z}, ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      st[0][3 * lane + c] = xa[c];
+      st[1][3 * lane + c] = ra[c];
+      st[2][3 * lane + c] = za[c];
+    }
+    __syncwarp();
+    const int64_t base = 3 * (int64_t)(v - lane);
+    const int64_t lim = 3 * (int64_t)nv - base;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int o = 32 * j + lane;
+      if (o < lim) {
+        x[base + o] = st[0][o];
+        r_out[base + o] = st[1][o];
+        z[base + o] = st[2][o];
+      }
+    }
+    __syncwarp();
+    if (in) {
+      dots[0] += dot(rv, zv);
+      dots[1] += dot(rv, rv);
+    }
+  }
+  double out[2];
+  if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
+    const double rz_old = scal[0];
+    scal[3] = rz_old != 0 ? out[0] / rz_old : 0.0;  // beta
+    scal[0] = out[0];                                // rz
+    scal[4] = out[1];                                // rr
+  }
+}
+
+// PCG init with the pair preconditioner (z = M^-1 r, r = -mask .* grad)
+__global__ void __launch_bounds__(kThreads) k_pcg_init_pair(int nv, const double* __restrict__ grad,
+                                                            const double* __restrict__ mask,
+                                                            const double* __restrict__ minv2,
+                                                            const int32_t* __restrict__ pair,
+                                                            double* __restrict__ x, double* __restrict__ r,
+                                                            double* __restrict__ z, double* __restrict__ p,
+                                                            double* scal, RedSlot rs) {
+  double dots[2] = {0, 0};
+  for (int v = blockIdx.x * kThreads + threadIdx.x; v < nv; v += gridDim.x * kThreads) {
+    const d3 m = ld3(mask, v), g = ld3(grad, v);
+    const d3 rv = mk3(-m.x * g.x, -m.y * g.y, -m.z * g.z);
+    const int pp = pair[v];
+    d3 rp = mk3(0, 0, 0);
+    if (pp >= 0) {
+      const d3 mp = ld3(mask, pp), gp = ld3(grad, pp);
+      rp = mk3(-mp.x * gp.x, -mp.y * gp.y, -mp.z * gp.z);
+    }
+    const d3 zv = pair_apply(minv2, v, rv, rp);
+    const double ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
+    for (int k = 0; k < 3; ++k) {
+      x[3 * v + k] = 0;
+      p[3 * v + k] = 0;
+      r[3 * v + k] = ra[k];
+      z[3 * v + k] = za[k];
+    }
+    dots[0] += dot(rv, zv);
+    dots[1] += dot(rv, rv);
+  }
+  double out[2];
+  if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
+    scal[0] = out[0];
+    scal[3] = 0;
+    scal[4] = out[1];
+    scal[5] = out[1];
   }
 }
 
@@ -525,6 +702,9 @@ struct SystemImpl {
   std::vector<std::unique_ptr<PairRt>> pairs;
   // device
   DBuf<double> x, dx, xtry, rest_d, fext_d, mask_d, grad, gel, r, z, p, q, w, minv, scal, parts, lsco, eel;
+  DBuf<double> minv2, r2;   // vertex-pair block-Jacobi: [v][3x6] rows, r ping-pong
+  DBuf<int32_t> pair_d;      // vertex-pair partner (-1: none), from the elastic matrix
+  bool has_pairs = false;
   DBuf<unsigned int> counter;
   DBuf<unsigned long long> redu;
   DBuf<int32_t> k_rowptr, k_cols;
@@ -663,6 +843,36 @@ void build_elastic(SystemImpl& S) {
   S.k_cols.upload(cols, S.stream);
   S.k_vals.upload(vals, S.stream);
   S.el_nnzb = (int64_t)cols.size();
+#if GMCP_PAIR_JACOBI
+  S.has_pairs = false;
+  if (S.n_scenes <= 1) {  // vertex pairs (single systems; batched scenes use the per-scene CTA PCG) for the 6x6 block-Jacobi: greedy matching of the strongest
+     // normalized elastic couplings |K_vw|_F^2 / (|K_vv|_F |K_ww|_F) (ties by index)
+    std::vector<double> dn(nv, 0.0);
+    for (int v = 0; v < nv; ++v)
+      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k)
+        if (cols[k] == v)
+          for (int q = 0; q < 9; ++q) dn[v] += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
+    struct Edge { double s; int32_t a, b; };
+    std::vector<Edge> edges;
+    for (int v = 0; v < nv; ++v)
+      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
+        const int w = cols[k];
+        if (w <= v || !(dn[v] > 0) || !(dn[w] > 0)) continue;
+        double f = 0;
+        for (int q = 0; q < 9; ++q) f += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
+        edges.push_back({f / std::sqrt(dn[v] * dn[w]), v, w});
+      }
+    std::stable_sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) { return x.s > y.s; });
+    std::vector<int32_t> mate(nv, -1);
+    for (const Edge& e : edges)
+      if (mate[e.a] < 0 && mate[e.b] < 0) {
+        mate[e.a] = e.b;
+        mate[e.b] = e.a;
+      }
+    S.pair_d.upload(mate, S.stream);
+    S.has_pairs = true;
+  }
+#endif
   S.el_built = true;
 }
 
@@ -871,9 +1081,18 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   const int nv = S.nv();
   MatSet M = mats(S);
   M.shift = shift;
-  k_block_jacobi<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, M, S.mask_d.p, S.minv.p);
-  k_pcg_init<<<kBlocks, kThreads, 0, S.stream>>>(nv, S.grad.p, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p, S.p.p,
-                                                 S.scal.p, S.slot(0));
+  const bool pairs = S.has_pairs && S.pair_d.n == nv;
+  if (pairs) {
+    S.minv2.resize(18 * (int64_t)nv);
+    S.r2.resize(3 * (int64_t)nv);
+    k_pair_jacobi<<<grid_for(nv, 128), 128, 0, S.stream>>>(nv, M, S.mask_d.p, S.pair_d.p, S.minv2.p);
+    k_pcg_init_pair<<<kBlocks, kThreads, 0, S.stream>>>(nv, S.grad.p, S.mask_d.p, S.minv2.p, S.pair_d.p, S.dx.p,
+                                                        S.r.p, S.z.p, S.p.p, S.scal.p, S.slot(0));
+  } else {
+    k_block_jacobi<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, M, S.mask_d.p, S.minv.p);
+    k_pcg_init<<<kBlocks, kThreads, 0, S.stream>>>(nv, S.grad.p, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p, S.p.p,
+                                                   S.scal.p, S.slot(0));
+  }
   S.launches += 2;
   double h[9];
   GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
@@ -898,8 +1117,9 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   key.lanes = lanes;
   key.gsp = gsp;
   key.gup = gup;
-  const void* ptrs[11] = {S.mask_d.p, S.z.p, S.p.p, S.w.p, S.q.p, S.dx.p, S.r.p, S.minv.p, S.scal.p, S.parts.p,
-                          S.counter.p};
+  const void* ptrs[11] = {S.mask_d.p, S.z.p, S.p.p, S.w.p, S.q.p, S.dx.p, S.r.p,
+                          pairs ? (const void*)S.minv2.p : (const void*)S.minv.p, S.scal.p,
+                          pairs ? (const void*)S.r2.p : (const void*)S.parts.p, S.counter.p};
   std::memcpy(key.ptrs, ptrs, sizeof ptrs);
   auto same_bcsr = [](const Bcsr& a, const Bcsr& b) {
     return a.rowptr == b.rowptr && a.cols == b.cols && a.vals == b.vals && a.bs == b.bs && a.cs == b.cs;
@@ -925,8 +1145,13 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
       else
         k_spmv_cg<4><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
                                                       S.slot(1));
-      k_update_cg<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
-                                                  S.slot(2));
+      if (pairs)  // r ping-pongs with p (chunk is even: r ends in S.r)
+        k_update_cg_pair<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, (k & 1) ? S.r2.p : S.r.p,
+                                                         (k & 1) ? S.r.p : S.r2.p, S.z.p, S.minv2.p, S.pair_d.p,
+                                                         S.scal.p, S.slot(2));
+      else
+        k_update_cg<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
+                                                    S.slot(2));
     }
     GMCP_CUDA(cudaStreamEndCapture(S.stream, &graph));
     GMCP_CUDA(cudaGraphInstantiate(&S.pcg_exec, graph, 0));
