@@ -316,8 +316,10 @@ __global__ void k_pair_jacobi(int nv, MatSet M, const double* __restrict__ mask,
     double Inv[6][6];
     for (int i = 0; i < 6; ++i)
       for (int j = 0; j < 6; ++j) Inv[i][j] = (i == j) ? 1.0 : 0.0;
+    bool ok = true;
     for (int c = 0; c < 6; ++c) {
-      const double ip = 1.0 / G[c][c];
+      ok = ok && G[c][c] > 0;  // SPD: positive pivots (else: identity, as a singular 3x3 block)
+      const double ip = G[c][c] > 0 ? 1.0 / G[c][c] : 0.0;
       for (int j = 0; j < 6; ++j) {
         G[c][j] *= ip;
         Inv[c][j] *= ip;
@@ -335,8 +337,8 @@ __global__ void k_pair_jacobi(int nv, MatSet M, const double* __restrict__ mask,
     double* o = minv2 + 18 * (int64_t)v;
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
-        o[3 * i + j] = Inv[me + i][me + j];
-        o[9 + 3 * i + j] = pv < 0 ? 0.0 : Inv[me + i][ot + j];
+        o[3 * i + j] = ok ? Inv[me + i][me + j] : (i == j ? 1.0 : 0.0);
+        o[9 + 3 * i + j] = (pv < 0 || !ok) ? 0.0 : Inv[me + i][ot + j];
       }
   }
 }
