@@ -7,7 +7,13 @@ measures.
   every sample field is bitwise equal. The oracle samples C3 in seconds.
 * Energy, gradient and step filter are compared with the oracle at the
   evaluation state, at the SURVEY.md 8d tolerances.
-* The assembled Hessian is checked through size-independent properties:
+* Candidate sets (tris, edges, verts per slave tri) are bitwise equal to the
+  oracle's at full size.
+* Every one of the ~700k assembled 3x3 BCSR blocks is within 1e-9 (norm-wise,
+  SURVEY.md 8d) of the oracle's summed Gauss-Newton triplets
+  (contact_energy.hpp:146-179), and the per-face-sample pressure field is
+  within 1e-9 with positions and gaps bitwise (contact_energy.hpp:225-242).
+* The assembled Hessian is also checked through size-independent properties:
   * exact symmetry (test_contact.cpp:125);
   * positive semi-definiteness on random directions (Gauss-Newton blocks are
     rank-1 PSD, test_contact.cpp:127-130);
@@ -49,9 +55,22 @@ def _bcsr_matvec(rowptr, cols, vals, v):
     return out.ravel()
 
 
-def test_c3_samples_energy_gradient_filter_match_oracle(c3, c3_ctx, orc):
+@pytest.fixture(scope="module")
+def c3_oracle(c3, orc):
     pairs = orc.candidate_pairs(c3.slave, c3.master, c3.rest, c3.params.detection_radius)
-    ost = orc.contact_state(c3.slave, c3.master, pairs, c3.rest, c3.params)
+    return pairs, orc.contact_state(c3.slave, c3.master, pairs, c3.rest, c3.params)
+
+
+def test_c3_candidate_sets_match_oracle(c3, c3_ctx, c3_oracle):
+    po = c3_oracle[0]
+    pg = c3_ctx.download_pairs()
+    assert po["tris"][0].size == c3.slave.tris.shape[0] + 1
+    for k in ("tris", "edges", "verts"):
+        assert np.array_equal(pg[k][0], po[k][0]) and np.array_equal(pg[k][1], po[k][1]), k
+
+
+def test_c3_samples_energy_gradient_filter_match_oracle(c3, c3_ctx, c3_oracle):
+    ost = c3_oracle[1]
     so, sg = ost.samples(), c3_ctx.download_samples()
     assert len(ost) == sg["type"].size == 1008248
     for k in so:
@@ -66,6 +85,37 @@ def test_c3_samples_energy_gradient_filter_match_oracle(c3, c3_ctx, orc):
     assert np.abs(g - go).max() <= TOL * np.abs(go).max()
     assert c3_ctx.step_filter() == ost.step_filter(x, dx)  # bit-exact
     assert c3_ctx.displacement_cap() == ost.displacement_cap(c3.params, x, dx)
+
+
+def test_c3_hessian_blocks_and_pressure_match_oracle(c3, c3_ctx, c3_oracle):
+    ost = c3_oracle[1]
+    x = c3.x_eval
+    c3_ctx.set_positions(x)
+    eh, gh, brow, bcol, bval, _ = ost.gradient_hessian(c3.params, x)
+    g = np.zeros_like(x)
+    e = c3_ctx.gradient(g, hessian=True)
+    assert abs(e - eh) <= TOL * abs(eh)
+    assert np.abs(g - gh).max() <= TOL * np.abs(gh).max()
+    rowptr, cols, vals = c3_ctx.download_hessian()
+    assert brow.size == 696667  # SURVEY.md 8 (C3 unique contact blocks)
+    n = rowptr.size - 1
+    rows = np.repeat(np.arange(n), np.diff(rowptr)).astype(np.int64)
+    kg = rows * n + cols
+    ko = brow.astype(np.int64) * n + bcol
+    pos = np.searchsorted(kg, ko)
+    assert np.all(pos < kg.size) and np.array_equal(kg[pos], ko), "oracle block missing from the GPU pattern"
+    scale = np.abs(bval).max()
+    assert np.abs(vals[pos] - bval).max() <= TOL * scale
+    rest_blocks = np.ones(kg.size, bool)
+    rest_blocks[pos] = False  # structurally present, never emitted by the oracle (all-zero products)
+    assert not rest_blocks.any() or np.abs(vals[rest_blocks]).max() <= TOL * scale
+    po, pg = ost.pressure(c3.params, x), c3_ctx.pressure_field()
+    assert pg.size == 647592
+    assert np.array_equal(po["sample"], pg["sample"])
+    assert np.array_equal(po["gap"], pg["gap"]) and np.array_equal(po["position"], pg["position"])
+    # hypot: CUDA's is within 2 ulp, glibc's correctly rounded
+    assert np.abs(pg["radius"] - po["radius"]).max() <= 1e-15 * np.abs(po["radius"]).max()
+    assert np.abs(pg["pressure"] - po["pressure"]).max() <= TOL * np.abs(po["pressure"]).max()
 
 
 def test_c3_hessian_symmetric_psd_deterministic(c3, c3_ctx):

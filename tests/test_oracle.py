@@ -73,6 +73,33 @@ def test_restated_matches_reference_bitwise(scene, orc, ref):
         assert _same(u, v)
 
 
+ORDERS = [(qf, qe) for qf in (1, 2, 3, 4) for qe in (1, 2, 3, 4, 5)]
+
+
+@pytest.mark.parametrize("qf,qe", ORDERS, ids=[f"f{a}e{b}" for a, b in ORDERS])
+@pytest.mark.parametrize("scene", [SCENES[0], SCENES[2]], ids=["patch", "slab12x10tex"])
+def test_restated_matches_reference_every_quadrature_order(scene, qf, qe, orc, ref):
+    """Every accepted (quad_order_face, quad_order_edge) pair (barrier.hpp:44-45,
+    quadrature.hpp:20-81): samples, energy, gradient and summed Hessian blocks
+    bitwise."""
+    name, slave, master, p0, rest, x, dx = scene
+    params = S.BarrierParams(**p0.__dict__)
+    params.quad_order_face, params.quad_order_edge = qf, qe
+    pr = ref.candidate_pairs(slave, master, rest, params.detection_radius)
+    sr = ref.contact_state(slave, master, pr, rest, params)
+    so = orc.contact_state(slave, master, pr, rest, params)
+    a, b = sr.samples(), so.samples()
+    assert len(sr) == len(so) > 0
+    for k in a:
+        assert _same(a[k], b[k]), f"sample field {k}"
+    hr, ho = sr.gradient_hessian(params, x), so.gradient_hessian(params, x)
+    assert hr[0] == ho[0] and _same(hr[1], ho[1]) and hr[5] == ho[5]
+    for i in (2, 3, 4):
+        assert _same(hr[i], ho[i])
+    assert sr.step_filter(x, dx) == so.step_filter(x, dx)
+    assert _same(sr.pressure(params, x).view(np.uint8), so.pressure(params, x).view(np.uint8))
+
+
 def test_brute_force_equals_tree(ref):
     sl = S.slab_scene(9, 7, seed=1)
     a = ref.candidate_pairs(sl.slave, sl.master, sl.x_eval, sl.params.detection_radius, True)
