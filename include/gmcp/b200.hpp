@@ -1,9 +1,11 @@
 // Drop-in B200 backend for the reference's contact path (C++ side).
 //
 // Include AFTER the reference headers (proj/include/gmcp/*.hpp, Eigen 3.3+)
-// and link libgmcp_b200.so. Every function keeps the reference signature
-// plus a leading gmcp::b200::Device&, takes the reference's own types, and
-// rethrows the reference exceptions (core.hpp:25-56):
+// and link libgmcp_b200.so. Every function exists twice: with the reference
+// signature verbatim (runs on the calling thread's default_device(), so a
+// call site only gains the gmcp::b200:: qualifier), and with a leading
+// gmcp::b200::Device& (explicit device / stream ownership). Both take the
+// reference's own types and rethrow the reference exceptions (core.hpp:25-56):
 //
 //   reference (proj/include/gmcp/)                      here (namespace gmcp::b200)
 //   build_candidate_pairs   contact_sampling.hpp:281    build_candidate_pairs
@@ -23,6 +25,8 @@
 // loop device-resident and touches the host only at the StepCallback.
 #pragma once
 
+#include <cstdlib>
+#include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
@@ -105,6 +109,22 @@ struct SampleArrays {
       g_ref[i] = s.g_ref;
     }
   }
+  bool matches(const ContactState& st) const {
+    const size_t n = st.samples.size();
+    if (c.type == nullptr || type.size() != n) return false;
+    auto same = [](double a, double b) { return std::memcmp(&a, &b, sizeof a) == 0; };
+    for (size_t i = 0; i < n; ++i) {
+      const ContactSample& s = st.samples[i];
+      if (type[i] != (int8_t)s.type || !same(eta[i], s.eta) || !same(weight[i], s.weight) ||
+          !same(gamma[i], s.gamma) || !same(eps[i], s.eps) || !same(g_ref[i], s.g_ref))
+        return false;
+      for (int k = 0; k < 3; ++k)
+        if (slave[3 * i + k] != s.slave[k] || master[3 * i + k] != s.master[k] ||
+            !same(beta_s[3 * i + k], s.beta_s[k]) || !same(beta_m[3 * i + k], s.beta_m[k]))
+          return false;
+    }
+    return true;
+  }
   void to(ContactState& st) const {
     st.samples.resize(type.size());
     for (size_t i = 0; i < type.size(); ++i) {
@@ -127,7 +147,12 @@ struct SampleArrays {
 
 }  // namespace detail
 
-// One GPU context (one CUDA stream). Caches the last uploaded ContactState.
+// One GPU context (one CUDA stream). Caches the last uploaded ContactState by
+// CONTENT: the reference reassigns a pair's state in place on a rebuild
+// (solver.hpp:295), so neither the object's address nor its sample count
+// identifies it. bind_state compares every field bitwise against the host
+// copy of the samples it uploaded last (O(n) host work, no device traffic)
+// and re-uploads on any difference.
 class Device {
  public:
   explicit Device(int device = 0) { detail::check(gmcp_ctx_create(device, &ctx_)); }
@@ -140,9 +165,11 @@ class Device {
   void step(const VecX& dx) { detail::check(gmcp_set_step(ctx_, dx.data(), (int64_t)dx.size())); }
   void params(const BarrierParams& p) {
     const gmcp_barrier_params c = detail::to_c(p);
+    if (have_params_ && std::memcmp(&c, &params_, sizeof c) == 0) return;
     detail::check(gmcp_set_params(ctx_, &c));
+    params_ = c;
+    have_params_ = true;
   }
-  // Uploads st unless it is the state uploaded last (same object, same size).
   void bind(const ContactState& st, const BarrierParams& p, const VecX& x) {
     positions(x);
     bind_state(st, p);
@@ -150,20 +177,43 @@ class Device {
   // params + samples only (the single-call entries take x themselves)
   void bind_state(const ContactState& st, const BarrierParams& p) {
     params(p);
-    if (&st != bound_ || st.samples.size() != bound_n_) {
-      detail::SampleArrays a;
-      a.from(st);
-      detail::check(gmcp_upload_samples(ctx_, &a.c));
-      bound_ = &st;
-      bound_n_ = st.samples.size();
+    bind_samples(st);
+  }
+  // samples only (step_filter takes no params, contact_energy.hpp:184): keeps
+  // the bound params, or binds placeholder stiffnesses the filter never reads
+  void bind_samples(const ContactState& st) {
+    if (!have_params_) {
+      BarrierParams q;
+      q.kappa_edge = q.kappa_point = q.kappa_face;
+      params(q);
+    }
+    if (!bound_.matches(st)) {
+      bound_.from(st);
+      detail::check(gmcp_upload_samples(ctx_, &bound_.c));
+      ++uploads_;
     }
   }
+  // samples uploaded so far (a test hook for the content cache)
+  long uploads() const { return uploads_; }
 
  private:
   gmcp_ctx* ctx_ = nullptr;
-  const ContactState* bound_ = nullptr;
-  size_t bound_n_ = 0;
+  detail::SampleArrays bound_;
+  gmcp_barrier_params params_{};
+  bool have_params_ = false;
+  long uploads_ = 0;
 };
+
+// The device behind the reference-signature overloads below: one per host
+// thread, on CUDA device GMCP_B200_DEVICE (default 0).
+inline Device& default_device() {
+  thread_local std::unique_ptr<Device> d;
+  if (!d) {
+    const char* e = std::getenv("GMCP_B200_DEVICE");
+    d = std::make_unique<Device>(e ? std::atoi(e) : 0);
+  }
+  return *d;
+}
 
 inline ContactPairSet build_candidate_pairs(Device& d, const ContactSurface& slave, const ContactSurface& master,
                                             const VecX& x, Real detection_radius) {
@@ -272,8 +322,9 @@ inline Real add_contact_gradient_hessian(Device& d, const ContactState& st, cons
   return e;
 }
 
-inline Real step_filter(Device& d, const ContactState& st, const BarrierParams& p, const VecX& x, const VecX& dx) {
-  d.bind(st, p, x);
+inline Real step_filter(Device& d, const ContactState& st, const VecX& x, const VecX& dx) {
+  d.positions(x);
+  d.bind_samples(st);
   d.step(dx);
   Real a = 1;
   detail::check(gmcp_step_filter(d.raw(), &a));
@@ -318,6 +369,48 @@ inline ContactForceSummary contact_force_summary(Device& d, const ContactState& 
   s.point = Vec3(o[6], o[7], o[8]);
   s.total = Vec3(o[9], o[10], o[11]);
   return s;
+}
+
+// ---------------------------------------------------------------------------
+// Reference signatures, verbatim (contact_sampling.hpp:281,382;
+// contact_energy.hpp:95-276): a call site switches by qualifying the call
+// with gmcp::b200:: and nothing else. They run on default_device().
+
+inline ContactPairSet build_candidate_pairs(const ContactSurface& slave, const ContactSurface& master, const VecX& x,
+                                            Real detection_radius, bool /*use_tree*/ = true) {
+  // the tree and brute-force sets are identical (test_sampling.cpp:390-397); the LBVH always runs
+  return build_candidate_pairs(default_device(), slave, master, x, detection_radius);
+}
+inline ContactState build_contact_state(const ContactSurface& slave, const ContactSurface& master,
+                                        const ContactPairSet& pairs, const VecX& x, const BarrierParams& params,
+                                        const VecX* eps_reference = nullptr) {
+  return build_contact_state(default_device(), slave, master, pairs, x, params, eps_reference);
+}
+inline ContactEnergyResult try_contact_energy(const ContactState& st, const BarrierParams& p, const VecX& x) {
+  return try_contact_energy(default_device(), st, p, x);
+}
+inline Real contact_energy(const ContactState& st, const BarrierParams& p, const VecX& x) {
+  return contact_energy(default_device(), st, p, x);
+}
+inline Real add_contact_gradient(const ContactState& st, const BarrierParams& p, const VecX& x, VecX& grad) {
+  return add_contact_gradient(default_device(), st, p, x, grad);
+}
+inline Real add_contact_gradient_hessian(const ContactState& st, const BarrierParams& p, const VecX& x, VecX& grad,
+                                         std::vector<Eigen::Triplet<Real>>& H) {
+  return add_contact_gradient_hessian(default_device(), st, p, x, grad, H);
+}
+inline Real step_filter(const ContactState& st, const VecX& x, const VecX& dx) {
+  return step_filter(default_device(), st, x, dx);
+}
+inline Real displacement_cap(const ContactState& st, const BarrierParams& p, const VecX& x, const VecX& dx) {
+  return displacement_cap(default_device(), st, p, x, dx);
+}
+inline std::vector<PressureRecord> contact_pressure_field(const ContactState& st, const BarrierParams& p,
+                                                          const VecX& x) {
+  return contact_pressure_field(default_device(), st, p, x);
+}
+inline ContactForceSummary contact_force_summary(const ContactState& st, const BarrierParams& p, const VecX& x) {
+  return contact_force_summary(default_device(), st, p, x);
 }
 
 #ifdef GMCP_B200_WITH_SOLVER

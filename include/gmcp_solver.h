@@ -83,6 +83,23 @@ int64_t gmcp_system_num_samples(gmcp_system* sys, int32_t pair);
 int gmcp_system_pair_force_summary(gmcp_system* sys, int32_t pair, double* out12);
 int gmcp_system_pair_pressure(gmcp_system* sys, int32_t pair, int64_t* n, gmcp_pressure_record* out);
 int64_t gmcp_system_launch_count(const gmcp_system* sys);
+/* Linear-solve parity (solver.hpp:349-356: the reference accepts a solve iff
+ * ||M s - rhs||_inf <= 1e-6 ||rhs||_inf). After every PCG solve the residual
+ * of the masked Newton system is RECOMPUTED (not PCG's recursive residual);
+ * a solve is accepted only if it converged and passes the reference's
+ * inf-norm test, else it is retried regularized like the reference. Returns
+ * the maxima of ||H dx - rhs||_2/||rhs||_2 and of the inf-norm ratio over the
+ * solves since the last reset, and their count. */
+int gmcp_system_linear_stats(gmcp_system* sys, int32_t reset, double* max_rel2, double* max_relinf,
+                             int64_t* n_solves);
+/* Inspection: when on, every solve copies its linear system to the host (the
+ * operand as one AoS BCSR with all sources summed, Dirichlet mask, gradient
+ * (rhs = -mask .* grad), solution dx, diagonal shift); the last one is read
+ * back with gmcp_system_captured_linear_system (pass null arrays to query
+ * nnzb; rowptr has n_vertices + 1 entries, vectors n_dof). */
+int gmcp_system_capture_linear_system(gmcp_system* sys, int32_t on);
+int gmcp_system_captured_linear_system(gmcp_system* sys, int64_t* nnzb, int32_t* rowptr, int32_t* cols, double* vals,
+                                       double* mask, double* grad, double* dx, double* shift);
 
 /* Batched independent scenes. scene[v] numbers the scenes
  * 0, 1, ... over contiguous vertex ranges (no body spans two scenes); NULL

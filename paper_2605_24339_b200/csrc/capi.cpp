@@ -13,6 +13,13 @@ struct gmcp_ctx {
   Ctx c;
 };
 
+namespace gmcp_b200 {
+CubScratch*& bound_scratch() {
+  thread_local CubScratch* s = nullptr;
+  return s;
+}
+}  // namespace gmcp_b200
+
 namespace {
 thread_local std::string g_err;
 
@@ -80,9 +87,9 @@ int gmcp_ctx_create(int device, gmcp_ctx** out) {
     int n = 0;
     GMCP_CUDA(cudaGetDeviceCount(&n));
     if (device < 0 || device >= n) throw StatusError(GMCP_ERR_CUDA, "no such CUDA device");
-    GMCP_CUDA(cudaSetDevice(device));
     auto* ctx = new gmcp_ctx;
     ctx->c.device = device;
+    const DeviceBind bind_(device, &ctx->c.cub);  // the caller's current device is restored
     GMCP_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
     *out = ctx;
     return GMCP_OK;
@@ -91,11 +98,14 @@ int gmcp_ctx_create(int device, gmcp_ctx** out) {
 
 void gmcp_ctx_destroy(gmcp_ctx* ctx) {
   if (!ctx) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   cudaStream_t s = ctx->c.stream;
   delete ctx;
   cudaStreamDestroy(s);
+  cudaSetDevice(prev);
 }
 
 int64_t gmcp_launch_count(const gmcp_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
@@ -126,6 +136,7 @@ int gmcp_resolve_barrier_params(gmcp_barrier_params* p, double m) {
 int gmcp_set_params(gmcp_ctx* ctx, const gmcp_barrier_params* p) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     need(p != nullptr, "null params");
     if (!(p->kappa_face > 0) || !(p->kappa_edge > 0) || !(p->kappa_point > 0) || !(p->eps_max > 0))
       throw StatusError(GMCP_ERR_CONFIG, "gmcp_set_params: parameters must be resolved (positive stiffnesses)");
@@ -139,6 +150,7 @@ int gmcp_set_params(gmcp_ctx* ctx, const gmcp_barrier_params* p) {
 int gmcp_set_surfaces(gmcp_ctx* ctx, const gmcp_surface* slave, const gmcp_surface* master) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     set_surface(ctx->c, ctx->c.slave, slave);
     set_surface(ctx->c, ctx->c.master, master);
     ctx->c.have_pairs = false;
@@ -150,6 +162,7 @@ int gmcp_set_surfaces(gmcp_ctx* ctx, const gmcp_surface* slave, const gmcp_surfa
 int gmcp_set_vertex_scenes(gmcp_ctx* ctx, const int32_t* scene, int64_t n_vertices) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     Ctx& c = ctx->c;
     c.have_pairs = false;
     if (!scene) {
@@ -173,6 +186,7 @@ int gmcp_set_vertex_scenes(gmcp_ctx* ctx, const int32_t* scene, int64_t n_vertic
 int gmcp_set_positions(gmcp_ctx* ctx, const double* x, int64_t n_dof) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     need(x != nullptr && n_dof >= 0 && n_dof % 3 == 0, "positions: need 3N doubles");
     Ctx& c = ctx->c;
     if (n_dof != c.n_dof) c.plan.valid = false;
@@ -190,6 +204,7 @@ int gmcp_set_positions(gmcp_ctx* ctx, const double* x, int64_t n_dof) {
 int gmcp_set_step(gmcp_ctx* ctx, const double* dx, int64_t n_dof) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     need(dx != nullptr && n_dof == ctx->c.n_dof, "step: size must match positions");
     ctx->c.dx.upload(dx, n_dof, ctx->c.stream);
     ctx->c.sync();
@@ -203,6 +218,7 @@ double* gmcp_step_device(gmcp_ctx* ctx) { return ctx ? ctx->c.dx.p : nullptr; }
 int gmcp_upload_samples(gmcp_ctx* ctx, const gmcp_samples* s) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     need(s != nullptr && s->n >= 0, "null samples");
     Ctx& c = ctx->c;
     need(c.have_params, "gmcp_upload_samples: call gmcp_set_params first");
@@ -245,6 +261,7 @@ int64_t gmcp_num_samples(const gmcp_ctx* ctx) { return ctx ? ctx->c.ns : 0; }
 int gmcp_download_samples(gmcp_ctx* ctx, gmcp_samples* o) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     Ctx& c = ctx->c;
     const int64_t n = c.ns;
     need(o != nullptr && o->n >= n, "samples out: too small");
@@ -266,6 +283,7 @@ int gmcp_download_samples(gmcp_ctx* ctx, gmcp_samples* o) {
 int gmcp_try_energy(gmcp_ctx* ctx, double* energy, double* min_gap, int32_t* feasible) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     const EnergyOut o = run_energy(ctx->c, true);
     if (o.first_degenerate >= 0 && (o.first_bad < 0 || o.first_degenerate < o.first_bad))
       throw StatusError(GMCP_ERR_DEGENERATE, "triangle_normal: degenerate triangle (area below cutoff)",
@@ -280,6 +298,7 @@ int gmcp_try_energy(gmcp_ctx* ctx, double* energy, double* min_gap, int32_t* fea
 int gmcp_energy(gmcp_ctx* ctx, double* energy, int64_t* bad) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     if (bad) *bad = -1;
     const EnergyOut o = run_energy(ctx->c, false);
     if (o.first_degenerate >= 0 && (o.first_bad < 0 || o.first_degenerate < o.first_bad))
@@ -297,6 +316,7 @@ int gmcp_energy(gmcp_ctx* ctx, double* energy, int64_t* bad) {
 static int grad_common(gmcp_ctx* ctx, int mode, double* grad, double* energy, int64_t* bad) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     Ctx& c = ctx->c;
     int64_t b = -1;
     if (bad) *bad = -1;
@@ -335,6 +355,7 @@ static int add_common(gmcp_ctx* ctx, int mode, const double* x, int64_t n_dof, d
                       int64_t* bad) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     need(x != nullptr && n_dof >= 0 && n_dof % 3 == 0, "positions: need 3N doubles");
     Ctx& c = ctx->c;
     if (n_dof != c.n_dof) {
@@ -369,6 +390,7 @@ int gmcp_add_gradient_hessian(gmcp_ctx* ctx, const double* x, int64_t n_dof, dou
 int gmcp_download_hessian(gmcp_ctx* ctx, int64_t* nnzb, int32_t* rowptr, int32_t* cols, double* vals) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     Ctx& c = ctx->c;
     need(c.plan.valid, "no assembled Hessian (call gmcp_gradient_hessian first)");
     *nnzb = c.plan.nnzb;
@@ -383,6 +405,7 @@ int gmcp_download_hessian(gmcp_ctx* ctx, int64_t* nnzb, int32_t* rowptr, int32_t
 int gmcp_step_filter(gmcp_ctx* ctx, double* alpha) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     *alpha = run_step_filter(ctx->c);
     return GMCP_OK;
   });
@@ -391,6 +414,7 @@ int gmcp_step_filter(gmcp_ctx* ctx, double* alpha) {
 int gmcp_displacement_cap(gmcp_ctx* ctx, double* alpha) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     *alpha = run_displacement_cap(ctx->c);
     return GMCP_OK;
   });
@@ -399,6 +423,7 @@ int gmcp_displacement_cap(gmcp_ctx* ctx, double* alpha) {
 int gmcp_pressure_field(gmcp_ctx* ctx, int64_t* n, gmcp_pressure_record* out) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     *n = (int64_t)ctx->c.face_idx.n;
     if (out) run_pressure(ctx->c, out);
     return GMCP_OK;
@@ -408,6 +433,7 @@ int gmcp_pressure_field(gmcp_ctx* ctx, int64_t* n, gmcp_pressure_record* out) {
 int gmcp_force_summary(gmcp_ctx* ctx, double* out12) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     run_force_summary(ctx->c, out12);
     return GMCP_OK;
   });
@@ -416,6 +442,7 @@ int gmcp_force_summary(gmcp_ctx* ctx, double* out12) {
 int gmcp_kinematics(gmcp_ctx* ctx, double* g, int32_t* nv, int32_t* ids, double* dg) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     run_kinematics(ctx->c, g, nv, ids, dg);
     return GMCP_OK;
   });
@@ -424,6 +451,7 @@ int gmcp_kinematics(gmcp_ctx* ctx, double* g, int32_t* nv, int32_t* ids, double*
 int gmcp_broadphase(gmcp_ctx* ctx, double r, int64_t* counts) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     if (!(r > 0)) throw StatusError(GMCP_ERR_CONFIG, "build_candidate_pairs: detection radius must be positive");
     run_broadphase(ctx->c, r, counts);
     return GMCP_OK;
@@ -433,6 +461,7 @@ int gmcp_broadphase(gmcp_ctx* ctx, double r, int64_t* counts) {
 int gmcp_download_pairs(gmcp_ctx* ctx, int which, int64_t* offsets, int32_t* ids) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     Ctx& c = ctx->c;
     need(c.have_pairs, "no candidate pairs");
     need(which >= 0 && which < 3, "which must be 0..2");
@@ -447,6 +476,7 @@ int gmcp_upload_pairs(gmcp_ctx* ctx, const int64_t* to, const int32_t* ti, const
                       const int64_t* vo, const int32_t* vi) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     Ctx& c = ctx->c;
     const int32_t nst = c.slave.n_tris;
     const int64_t* offs[3] = {to, eo, vo};
@@ -465,6 +495,7 @@ int gmcp_upload_pairs(gmcp_ctx* ctx, const int64_t* to, const int32_t* ti, const
 int gmcp_build_samples(gmcp_ctx* ctx, const double* eps_reference, int64_t* n_samples) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     Ctx& c = ctx->c;
     need(c.have_pairs, "gmcp_build_samples: no candidate pairs (call gmcp_broadphase)");
     need(c.have_params, "gmcp_build_samples: call gmcp_set_params first");
@@ -481,6 +512,7 @@ int gmcp_build_samples(gmcp_ctx* ctx, const double* eps_reference, int64_t* n_sa
 int gmcp_time_assembly(gmcp_ctx* ctx, int reps, int flush_l2, double* ms_pass, double* ms_kernel) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     need(reps > 0, "reps must be positive");
     time_assembly(ctx->c, reps, flush_l2, ms_pass, ms_kernel);
     return GMCP_OK;
@@ -493,6 +525,7 @@ int gmcp_embed_in_surface(gmcp_ctx* ctx, const double* points, int64_t n_points,
                           double* bary, double* offset, int64_t* bad) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     need(n_points >= 0 && n_host_vertices >= 0 && n_host_tris >= 0, "embedding: negative sizes");
     need((points || !n_points) && host_vertices && host_tris && (tri || !n_points) && (bary || !n_points) &&
              (offset || !n_points),
@@ -517,6 +550,7 @@ int gmcp_apply_embedding(gmcp_ctx* ctx, const int32_t* tri, const double* bary, 
                          int64_t n_host_vertices, double* out, int64_t* bad) {
   return guarded([&] {
     check_ctx(ctx);
+    const DeviceBind bind_(ctx->c.device, &ctx->c.cub);
     need(n >= 0 && (tri || !n) && (bary || !n) && (offset || !n) && (out || !n) && host_tris && host_positions,
          "apply_embedding: null buffer");
     for (int64_t i = 0; i < n; ++i) need(tri[i] >= 0 && tri[i] < n_host_tris, "apply_embedding: triangle out of range");

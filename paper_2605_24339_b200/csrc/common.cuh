@@ -120,6 +120,42 @@ struct DBuf {
 };
 
 // ---------------------------------------------------------------------------
+// Per-context binding. Every C-ABI entry binds its context's device and CUB
+// temp storage to the calling thread for the duration of the call (RAII), so
+// contexts on different devices (or several on one device) may be driven
+// from different host threads: nothing device-side is process-global.
+
+struct CubScratch {
+  DBuf<unsigned char> tmp;
+  void* get(size_t bytes) {
+    tmp.resize(bytes > 0 ? bytes : 1);
+    return tmp.p;
+  }
+};
+
+CubScratch*& bound_scratch();  // thread-local; defined in capi.cpp
+
+class DeviceBind {
+ public:
+  DeviceBind(int device, CubScratch* s) : prev_s_(bound_scratch()) {
+    GMCP_CUDA(cudaGetDevice(&prev_dev_));
+    if (prev_dev_ != device) GMCP_CUDA(cudaSetDevice(device));
+    bound_scratch() = s;
+    dev_ = device;
+  }
+  ~DeviceBind() {
+    bound_scratch() = prev_s_;
+    if (prev_dev_ != dev_) cudaSetDevice(prev_dev_);
+  }
+  DeviceBind(const DeviceBind&) = delete;
+  DeviceBind& operator=(const DeviceBind&) = delete;
+
+ private:
+  int prev_dev_ = 0, dev_ = 0;
+  CubScratch* prev_s_;
+};
+
+// ---------------------------------------------------------------------------
 // vector algebra (reference evaluation order)
 
 struct d3 {

@@ -28,7 +28,7 @@ constexpr int kWarpE = kRedBlocks + 8;
 int launch_k7(Ctx& c, int mode) {
   AssemblyPlan& P = c.plan;
   const DevSamples S = c.samples();
-  static int resident = 0;  // persistent grid: resident blocks on all SMs
+  int& resident = c.k7_resident;  // persistent grid: resident blocks on all SMs of c's device
   if (!resident) {
     int occ = 0, dev = 0, sms = 148;
     GMCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_run_partials<true>, 32 * kRunWarps, 0));

@@ -54,6 +54,8 @@ struct TmpBase {
 
 struct Ctx {
   int device = 0;
+  CubScratch cub;        // CUB temp storage (bound per C-ABI call)
+  int k7_resident = 0;   // K7 persistent grid size on this context's device
   std::unique_ptr<TmpBase> rebuild_tmp;  // broadphase + sampler scratch (sampler.cu)
   std::unique_ptr<TmpBase> embed_tmp;    // dual-mesh embedding scratch (sampler.cu)
   std::unique_ptr<TmpBase> scene_tmp;    // scene-segmented reductions scratch (exact.cu)

@@ -1,5 +1,6 @@
-// CUB scan / sort / run-length helpers with a per-translation-unit scratch
-// buffer (temp storage reused across calls; all work on the caller's stream).
+// CUB scan / sort / run-length helpers. Temp storage is the CubScratch of the
+// context (or System) the current C-ABI call bound to this thread
+// (common.cuh DeviceBind); all work on the caller's stream.
 #pragma once
 
 #include <cub/cub.cuh>
@@ -9,14 +10,14 @@
 namespace gmcp_b200 {
 namespace {
 
-struct Scratch {
-  DBuf<unsigned char> tmp;
-  void* get(size_t bytes) {
-    tmp.resize(std::max<size_t>(bytes, 1));
-    return tmp.p;
+struct BoundScratch {
+  void* get(size_t bytes) const {
+    CubScratch* s = bound_scratch();
+    if (!s) throw CudaError("gmcp_b200: CUB call outside a bound context");
+    return s->get(bytes);
   }
 };
-Scratch g_scratch;
+constexpr BoundScratch g_scratch{};
 
 template <class T>
 void exclusive_scan(const T* in, T* out, int64_t n, cudaStream_t s) {

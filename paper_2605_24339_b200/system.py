@@ -269,6 +269,34 @@ class System:
         _check(self.L, self.L.gmcp_system_pcg_stats(self.h, C.byref(ms), C.byref(it), C.byref(rows), C.byref(nnzb)))
         return {"ms": ms.value, "iters": it.value, "rows": rows.value, "nnzb": nnzb.value}
 
+    def linear_stats(self, reset: bool = False) -> dict:
+        """Recomputed true residuals of the linear solves since the last reset:
+        max ||H dx - rhs||_2/||rhs||_2, max inf-norm ratio (the reference's
+        acceptance test, solver.hpp:349-356), number of solves."""
+        r2, ri, n = C.c_double(), C.c_double(), C.c_int64()
+        _check(self.L, self.L.gmcp_system_linear_stats(self.h, C.c_int32(1 if reset else 0), C.byref(r2), C.byref(ri),
+                                                       C.byref(n)))
+        return {"max_rel2": r2.value, "max_relinf": ri.value, "solves": n.value}
+
+    def capture_linear_system(self, on: bool = True):
+        _check(self.L, self.L.gmcp_system_capture_linear_system(self.h, C.c_int32(1 if on else 0)))
+
+    def captured_linear_system(self) -> dict:
+        """The last captured solve: BCSR operand (all sources summed), mask,
+        gradient (rhs = -mask * grad), dx and the diagonal shift."""
+        nnzb, shift = C.c_int64(), C.c_double()
+        _check(self.L, self.L.gmcp_system_captured_linear_system(self.h, C.byref(nnzb), None, None, None, None, None,
+                                                                 None, C.byref(shift)))
+        nv, n = self.rest.size // 3, self.rest.size
+        rowptr, cols = np.zeros(nv + 1, np.int32), np.zeros(nnzb.value, np.int32)
+        vals = np.zeros((nnzb.value, 3, 3))
+        mask, grad, dx = np.zeros(n), np.zeros(n), np.zeros(n)
+        _check(self.L, self.L.gmcp_system_captured_linear_system(self.h, C.byref(nnzb), _g._p(rowptr), _g._p(cols),
+                                                                 _g._p(vals), _g._p(mask), _g._p(grad), _g._p(dx),
+                                                                 C.byref(shift)))
+        return {"rowptr": rowptr, "cols": cols, "vals": vals, "mask": mask, "grad": grad, "dx": dx,
+                "shift": shift.value}
+
     @property
     def launches(self) -> int:
         return int(self.L.gmcp_system_launch_count(self.h))
@@ -405,6 +433,7 @@ class HertzResult:
     profile: np.ndarray | None = None  # (n, 3): radius, pressure, analytic pressure
     stats: RunStats | None = None
     face_samples: int = 0
+    system: object = None  # the device System that ran the solve
 
 
 def build_hertz_system(cfg: S.HertzConfig | None = None, device: int = 0, scene: S.HertzScene | None = None):
@@ -431,6 +460,7 @@ def run_hertz(cfg: S.HertzConfig | None = None, settings: SolverSettings | None 
     settings = settings or SolverSettings()
     settings.load_steps = cfg.load_steps
     res.stats = sys_.solve(settings, on_step)
+    res.system = sys_
     field = sys_.contact_pressure_field(0)
     res.face_samples = int(field.size)
     r, p = field["radius"].astype(np.float64), field["pressure"].astype(np.float64)

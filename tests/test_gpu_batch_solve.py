@@ -25,7 +25,9 @@ def test_batched_scenes_match_individual_solves():
         so = one.solve(settings)
         xb = bs.x[3 * k * N:3 * (k + 1) * N]
         u = one.x - one.rest
-        # same equilibrium up to the Newton tolerance's slack (rebuilds are
-        # triggered per batch, so iterates differ slightly)
-        assert np.max(np.abs(xb - one.x)) <= 1e-3 * np.max(np.abs(u))
+        # same equilibrium: both converge every load step to the same Newton
+        # tolerance, and the per-CTA PCG of the batch sums its dot products in
+        # another order than the single-scene PCG, so iterates agree to the
+        # Newton tolerance's slack (measured 7e-13 relative), not bitwise
+        assert np.max(np.abs(xb - one.x)) <= 1e-9 * np.max(np.abs(u))
         assert abs(int(iters[k]) - so.total_newton_iters) <= 6
