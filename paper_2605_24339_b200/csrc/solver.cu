@@ -19,6 +19,7 @@
 #include "ctx.hpp"
 #include "kin.cuh"
 #include "cubutil.cuh"
+#include "coarse.cuh"
 
 namespace gmcp_b200 {
 
@@ -40,9 +41,9 @@ struct RedSlot {
   unsigned int* counter;  // arrival counter (reset by the last block)
 };
 
-template <int W>
+template <int W, int NT = kThreads>
 __device__ __forceinline__ bool block_reduce_last(double (&v)[W], RedSlot rs, double (&out)[W]) {
-  __shared__ double sh[W][kThreads / 32];
+  __shared__ double sh[W][NT / 32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -55,7 +56,7 @@ __device__ __forceinline__ bool block_reduce_last(double (&v)[W], RedSlot rs, do
 #pragma unroll
     for (int q = 0; q < W; ++q) {
       double t = 0;
-      for (int i = 0; i < kThreads / 32; ++i) t += sh[q][i];
+      for (int i = 0; i < NT / 32; ++i) t += sh[q][i];
       rs.parts[blockIdx.x * W + q] = t;
     }
     __threadfence();
@@ -67,7 +68,7 @@ __device__ __forceinline__ bool block_reduce_last(double (&v)[W], RedSlot rs, do
 #pragma unroll
   for (int q = 0; q < W; ++q) {
     double t = 0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads) t += __ldcg(rs.parts + i * W + q);
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) t += __ldcg(rs.parts + i * W + q);
     t = warp_sum(t);
     if (lane == 0) sh[q][wid] = t;
   }
@@ -76,7 +77,7 @@ __device__ __forceinline__ bool block_reduce_last(double (&v)[W], RedSlot rs, do
 #pragma unroll
     for (int q = 0; q < W; ++q) {
       double t = 0;
-      for (int i = 0; i < kThreads / 32; ++i) t += sh[q][i];
+      for (int i = 0; i < NT / 32; ++i) t += sh[q][i];
       out[q] = t;
     }
     *rs.counter = 0;
@@ -137,7 +138,10 @@ constexpr double kRegularization = 1e-8;  // SolverSettings::regularization (sol
 // rather than pcg_max_iters. Converging solves shrink rr by orders of
 // magnitude per window and never trip it.
 constexpr int kStagWindow = 1024;
+constexpr int kStagWindowCoarse = 256;
 constexpr double kAcceptRelInf = 1e-6;  // solver.hpp:349-356 acceptance of a linear solve
+constexpr double kCoarseDrop = 1e-10;   // scaled coarse pivots below this drop their rigid mode
+constexpr double kCoarseStale = 1.25;   // refresh the coarse inverse when a solve needs 25% more iterations
 
 // A_vj x for block k, read through the read-only path (either layout)
 __device__ __forceinline__ d3 bmv_ro(const Bcsr& A, int64_t k, d3 p) {
@@ -217,6 +221,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const do
 }
 
 // K9b: x += alpha p, r -= alpha q, z = Minv r; rz_new, rr -> beta (last block).
+template <bool kCoarse>
 __global__ void __launch_bounds__(kThreads) k_update_cg(int nv, const double* __restrict__ p,
                                                         const double* __restrict__ q, double* __restrict__ x,
                                                         double* __restrict__ r, double* __restrict__ z,
@@ -260,10 +265,14 @@ __global__ void __launch_bounds__(kThreads) k_update_cg(int nv, const double* __
   }
   double out[2];
   if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
-    const double rz_old = scal[0];
-    scal[3] = rz_old != 0 ? out[0] / rz_old : 0.0;  // beta
-    scal[0] = out[0];                                // rz
-    scal[4] = out[1];                                // rr
+    if (kCoarse) {  // r.z completed by the coarse solve (k_coarse_apply)
+      scal[6] = out[0];
+    } else {
+      const double rz_old = scal[0];
+      scal[3] = rz_old != 0 ? out[0] / rz_old : 0.0;  // beta
+      scal[0] = out[0];                                // rz
+    }
+    scal[4] = out[1];  // rr
   }
 }
 
@@ -313,14 +322,20 @@ __global__ void k_pair_jacobi(int nv, MatSet M, const double* __restrict__ mask,
             G[3 * I + i][3 * J + j] = g;
           }
       }
-    // Gauss-Jordan inverse (SPD: no pivoting), in place
+    // Gauss-Jordan inverse (SPD: no pivoting), in place. A pivot below 1e-12 x
+    // the largest diagonal entry (singular or nearly singular pair block)
+    // makes both vertices of the pair fall back to their own 3x3 block inverse
+    // (k_block_jacobi's rule), so M^-1 keeps the stiffness scaling.
+    double gmax = 0;
+    for (int i = 0; i < n; ++i) gmax = fmax(gmax, fabs(G[i][i]));
+    const double thr = 1e-12 * gmax;
     double Inv[6][6];
     for (int i = 0; i < 6; ++i)
       for (int j = 0; j < 6; ++j) Inv[i][j] = (i == j) ? 1.0 : 0.0;
     bool ok = true;
     for (int c = 0; c < 6; ++c) {
-      ok = ok && G[c][c] > 0;  // SPD: positive pivots (else: identity, as a singular 3x3 block)
-      const double ip = G[c][c] > 0 ? 1.0 / G[c][c] : 0.0;
+      ok = ok && G[c][c] > thr;
+      const double ip = G[c][c] > thr ? 1.0 / G[c][c] : 0.0;
       for (int j = 0; j < 6; ++j) {
         G[c][j] *= ip;
         Inv[c][j] *= ip;
@@ -336,11 +351,35 @@ __global__ void k_pair_jacobi(int nv, MatSet M, const double* __restrict__ mask,
     }
     const int me = (v == a) ? 0 : 3, ot = 3 - me;
     double* o = minv2 + 18 * (int64_t)v;
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        o[3 * i + j] = ok ? Inv[me + i][me + j] : (i == j ? 1.0 : 0.0);
-        o[9 + 3 * i + j] = (pv < 0 || !ok) ? 0.0 : Inv[me + i][ot + j];
+    if (ok) {  // symmetrized: the partner stores the transpose of this cross block
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+          o[3 * i + j] = 0.5 * (Inv[me + i][me + j] + Inv[me + j][me + i]);
+          o[9 + 3 * i + j] = pv < 0 ? 0.0 : 0.5 * (Inv[me + i][ot + j] + Inv[ot + j][me + i]);
+        }
+    } else {  // own masked 3x3 block (k_block_jacobi)
+      double D[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      add_block(M, v, v, D);
+      D[0] += M.shift;
+      D[4] += M.shift;
+      D[8] += M.shift;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+          if (mask[3 * v + i] == 0 || mask[3 * v + j] == 0) D[3 * i + j] = (i == j) ? 1.0 : 0.0;
+      const double c00 = D[4] * D[8] - D[5] * D[7], c01 = D[2] * D[7] - D[1] * D[8], c02 = D[1] * D[5] - D[2] * D[4];
+      const double c10 = D[5] * D[6] - D[3] * D[8], c11 = D[0] * D[8] - D[2] * D[6], c12 = D[2] * D[3] - D[0] * D[5];
+      const double c20 = D[3] * D[7] - D[4] * D[6], c21 = D[1] * D[6] - D[0] * D[7], c22 = D[0] * D[4] - D[1] * D[3];
+      const double det = D[0] * c00 + D[1] * c10 + D[2] * c20;
+      for (int q = 0; q < 18; ++q) o[q] = 0;
+      if (det != 0 && isfinite(det)) {
+        const double id = 1.0 / det;
+        o[0] = c00 * id; o[1] = c01 * id; o[2] = c02 * id;
+        o[3] = c10 * id; o[4] = c11 * id; o[5] = c12 * id;
+        o[6] = c20 * id; o[7] = c21 * id; o[8] = c22 * id;
+      } else {
+        for (int q = 0; q < 3; ++q) o[4 * q] = D[4 * q] != 0 ? 1.0 / D[4 * q] : 1.0;
       }
+    }
   }
 }
 
@@ -351,6 +390,7 @@ __device__ __forceinline__ d3 pair_apply(const double* __restrict__ minv2, int v
 
 // K9b with the pair preconditioner: r ping-pongs (r_in -> r_out) so a thread
 // can form its partner's new residual r_p = r_in[p] - alpha q[p] itself.
+template <bool kCoarse>
 __global__ void __launch_bounds__(kThreads) k_update_cg_pair(int nv, const double* __restrict__ p,
                                                              const double* __restrict__ q, double* __restrict__ x,
                                                              const double* __restrict__ r_in,
@@ -398,14 +438,19 @@ __global__ void __launch_bounds__(kThreads) k_update_cg_pair(int nv, const doubl
   }
   double out[2];
   if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
-    const double rz_old = scal[0];
-    scal[3] = rz_old != 0 ? out[0] / rz_old : 0.0;  // beta
-    scal[0] = out[0];                                // rz
-    scal[4] = out[1];                                // rr
+    if (kCoarse) {  // r.z completed by the coarse solve (k_coarse_apply)
+      scal[6] = out[0];
+    } else {
+      const double rz_old = scal[0];
+      scal[3] = rz_old != 0 ? out[0] / rz_old : 0.0;  // beta
+      scal[0] = out[0];                                // rz
+    }
+    scal[4] = out[1];  // rr
   }
 }
 
 // PCG init with the pair preconditioner (z = M^-1 r, r = -mask .* grad)
+template <bool kCoarse>
 __global__ void __launch_bounds__(kThreads) k_pcg_init_pair(int nv, const double* __restrict__ grad,
                                                             const double* __restrict__ mask,
                                                             const double* __restrict__ minv2,
@@ -436,7 +481,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init_pair(int nv, const double
   }
   double out[2];
   if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
-    scal[0] = out[0];
+    scal[kCoarse ? 6 : 0] = out[0];
     scal[3] = 0;
     scal[4] = out[1];
     scal[5] = out[1];
@@ -444,6 +489,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init_pair(int nv, const double
 }
 
 // PCG init: x = p = 0, r = b = -mask.*grad, z = Minv r; rz, rr, bb; beta = 0.
+template <bool kCoarse>
 __global__ void __launch_bounds__(kThreads) k_pcg_init(int nv, const double* __restrict__ grad,
                                                        const double* __restrict__ mask, const double* __restrict__ minv,
                                                        double* __restrict__ x, double* __restrict__ r,
@@ -466,10 +512,277 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(int nv, const double* __r
   }
   double out[2];
   if (block_reduce_last<2>(dots, rs, out) && threadIdx.x == 0) {
-    scal[0] = out[0];  // rz
-    scal[3] = 0;       // beta: first direction p = z
+    scal[kCoarse ? 6 : 0] = out[0];  // rz (smoother part when the coarse solve completes it)
+    scal[3] = 0;                     // beta: first direction p = z
+    scal[4] = out[1];                // rr
+    scal[5] = out[1];                // bb
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Two-level PCG iteration kernels (coarse.cuh). With the coarse space on, one
+// PCG iteration is three kernels: the SpMV (k_spmv_cg), the update fused with
+// the restriction (k_update_agg), and the coarse solve fused with the
+// prolongation (k_coarse_prolong). Both fused kernels run one CTA per
+// aggregate over its vertex list, so the per-aggregate sums are CTA-local
+// fixed-order reductions (deterministic), and every z entry is completed by
+// the CTA that owns its vertex.
+
+// CTA sum of W values in warp order (thread 0 holds the result)
+template <int W, int NT>
+__device__ __forceinline__ void cta_sum(double (&v)[W], double (&sh)[NT / 32][W]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < W; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < W; ++q) sh[wid][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      double t = 0;
+      for (int w = 0; w < NT / 32; ++w) t += sh[w][q];
+      v[q] = t;
+    }
+}
+
+// x += alpha p, r = r_in - alpha q, z = M1^-1 r (pair or 3x3 block-Jacobi);
+// s_a = S P^T r over the aggregate; r.z (smoother part) and r.r by the last block.
+constexpr int kAggThreads = 1024;  // one CTA per aggregate: all of its vertices in flight at once
+template <bool kPair>
+__global__ void __launch_bounds__(kAggThreads) k_update_agg(
+    const int32_t* __restrict__ agg_off, const int32_t* __restrict__ agg_verts, const double* __restrict__ dvec,
+    const double* __restrict__ mask, const double* __restrict__ scale, const double* __restrict__ p,
+    const double* __restrict__ q, double* __restrict__ x, const double* r_in, double* r_out,
+    double* __restrict__ z, const double* __restrict__ minv, const int32_t* __restrict__ pair,
+    double* __restrict__ s, double* scal, RedSlot rs) {
+  __shared__ double sh[kAggThreads / 32][8];
+  const int a = blockIdx.x;
+  const double al = scal[2];
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // t(3), w(3), rz, rr
+  const int e1 = agg_off[a + 1];
+  for (int e = agg_off[a] + threadIdx.x; e < e1; e += kAggThreads) {
+    const int v = agg_verts[e];
+    const d3 xv = ld3nc(x, v) + al * ld3nc(p, v);
+    const d3 rv = ld3nc(r_in, v) - al * ld3nc(q, v);
+    d3 zv;
+    if (kPair) {
+      const int pp = pair[v];
+      const d3 rp = pp < 0 ? mk3(0, 0, 0) : ld3nc(r_in, pp) - al * ld3nc(q, pp);
+      zv = pair_apply(minv, v, rv, rp);
+    } else {
+      zv = bmv(minv + 9 * (int64_t)v, rv);
+    }
+    x[3 * v] = xv.x;
+    x[3 * v + 1] = xv.y;
+    x[3 * v + 2] = xv.z;
+    r_out[3 * v] = rv.x;
+    r_out[3 * v + 1] = rv.y;
+    r_out[3 * v + 2] = rv.z;
+    z[3 * v] = zv.x;
+    z[3 * v + 1] = zv.y;
+    z[3 * v + 2] = zv.z;
+    const d3 m = ld3(mask, v);
+    const d3 mr = mk3(m.x * rv.x, m.y * rv.y, m.z * rv.z);
+    const d3 w = cross(ld3(dvec, v), mr);
+    acc[0] += mr.x;
+    acc[1] += mr.y;
+    acc[2] += mr.z;
+    acc[3] += w.x;
+    acc[4] += w.y;
+    acc[5] += w.z;
+    acc[6] += dot(rv, zv);
+    acc[7] += dot(rv, rv);
+  }
+  cta_sum<8, kAggThreads>(acc, sh);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 6; ++k) s[6 * a + k] = acc[k] * scale[6 * a + k];
+  double d[2] = {threadIdx.x == 0 ? acc[6] : 0.0, threadIdx.x == 0 ? acc[7] : 0.0};
+  double out[2];
+  if (block_reduce_last<2, kAggThreads>(d, rs, out) && threadIdx.x == 0) {
+    scal[6] = out[0];  // r.z of the smoother; k_coarse_prolong completes it
     scal[4] = out[1];  // rr
-    scal[5] = out[1];  // bb
+  }
+}
+
+// y_a = S (Ainv s')_a for the CTA's aggregate (6 rows, one warp each, loads
+// unrolled), z_v += Phi_v y_a over its vertices, and s.y -> rz = r.M1^-1 r +
+// s.y, beta (last block). kInit: first direction (beta = 0).
+template <bool kInit>
+__global__ void __launch_bounds__(kAggThreads) k_coarse_prolong(
+    int n_pad, const double* __restrict__ Ainv, const double* __restrict__ scale, const double* __restrict__ s,
+    const int32_t* __restrict__ agg_off, const int32_t* __restrict__ agg_verts, const double* __restrict__ dvec,
+    const double* __restrict__ mask, double* __restrict__ z, double* scal, RedSlot rs) {
+  __shared__ double ya[6], sy[6];
+  const int a = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid < 6) {
+    const int i = 6 * a + wid;
+    const double* row = Ainv + (int64_t)i * n_pad;
+    double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    int j = lane;
+    for (; j + 96 < n_pad; j += 128) {
+      const double a0 = __ldg(row + j), a1 = __ldg(row + j + 32), a2 = __ldg(row + j + 64), a3 = __ldg(row + j + 96);
+      const double b0 = __ldg(s + j), b1 = __ldg(s + j + 32), b2 = __ldg(s + j + 64), b3 = __ldg(s + j + 96);
+      c0 += a0 * b0;
+      c1 += a1 * b1;
+      c2 += a2 * b2;
+      c3 += a3 * b3;
+    }
+    for (; j < n_pad; j += 32) c0 += __ldg(row + j) * __ldg(s + j);
+    const double acc = warp_sum((c0 + c1) + (c2 + c3));
+    if (lane == 0) {
+      ya[wid] = scale[i] * acc;
+      sy[wid] = s[i] * acc;
+    }
+  }
+  __syncthreads();
+  const d3 t = mk3(ya[0], ya[1], ya[2]), om = mk3(ya[3], ya[4], ya[5]);
+  const int e1 = agg_off[a + 1];
+  for (int e = agg_off[a] + threadIdx.x; e < e1; e += kAggThreads) {
+    const int v = agg_verts[e];
+    const d3 u = t + cross(om, ld3(dvec, v));
+    const d3 m = ld3(mask, v);
+    z[3 * v] += m.x * u.x;
+    z[3 * v + 1] += m.y * u.y;
+    z[3 * v + 2] += m.z * u.z;
+  }
+  double d[1] = {threadIdx.x == 0 ? ((sy[0] + sy[1]) + (sy[2] + sy[3])) + (sy[4] + sy[5]) : 0.0};
+  double out[1];
+  if (block_reduce_last<1, kAggThreads>(d, rs, out) && threadIdx.x == 0) {
+    const double rz = scal[6] + out[0];
+    if (kInit) {
+      scal[0] = rz;
+      scal[3] = 0;
+    } else {
+      const double rz_old = scal[0];
+      scal[3] = rz_old != 0 ? rz / rz_old : 0.0;
+      scal[0] = rz;
+    }
+  }
+}
+
+// Software grid barrier for a cooperatively launched (co-resident) grid:
+// bar[0] arrivals, bar[1] generation.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// k_update_agg and k_coarse_prolong<false> as ONE cooperative kernel (one CTA
+// per aggregate, all co-resident): update + restriction, grid barrier, coarse
+// rows + prolongation of the CTA's own aggregate; rz = r.M1^-1 r + s.y and rr
+// by the last block, in aggregate order.
+template <bool kPair>
+__global__ void __launch_bounds__(kAggThreads) k_update_coarse(
+    const int32_t* __restrict__ agg_off, const int32_t* __restrict__ agg_verts, const double* __restrict__ dvec,
+    const double* __restrict__ mask, const double* __restrict__ scale, const double* __restrict__ p,
+    const double* __restrict__ q, double* __restrict__ x, const double* r_in, double* r_out, double* z,
+    const double* __restrict__ minv, const int32_t* __restrict__ pair, double* s, int n_pad,
+    const double* __restrict__ Ainv, double* aparts, unsigned int* bar, double* scal, RedSlot rs) {
+  __shared__ double sh[kAggThreads / 32][8];
+  __shared__ double ya[6], sy[6];
+  const int a = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double al = scal[2];
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // t(3), w(3), rz, rr
+  const int e0 = agg_off[a], e1 = agg_off[a + 1];
+  for (int e = e0 + threadIdx.x; e < e1; e += kAggThreads) {
+    const int v = agg_verts[e];
+    const d3 xv = ld3nc(x, v) + al * ld3nc(p, v);
+    const d3 rv = ld3nc(r_in, v) - al * ld3nc(q, v);
+    d3 zv;
+    if (kPair) {
+      const int pp = pair[v];
+      const d3 rp = pp < 0 ? mk3(0, 0, 0) : ld3nc(r_in, pp) - al * ld3nc(q, pp);
+      zv = pair_apply(minv, v, rv, rp);
+    } else {
+      zv = bmv(minv + 9 * (int64_t)v, rv);
+    }
+    x[3 * v] = xv.x;
+    x[3 * v + 1] = xv.y;
+    x[3 * v + 2] = xv.z;
+    r_out[3 * v] = rv.x;
+    r_out[3 * v + 1] = rv.y;
+    r_out[3 * v + 2] = rv.z;
+    z[3 * v] = zv.x;
+    z[3 * v + 1] = zv.y;
+    z[3 * v + 2] = zv.z;
+    const d3 m = ld3(mask, v);
+    const d3 mr = mk3(m.x * rv.x, m.y * rv.y, m.z * rv.z);
+    const d3 w = cross(ld3(dvec, v), mr);
+    acc[0] += mr.x;
+    acc[1] += mr.y;
+    acc[2] += mr.z;
+    acc[3] += w.x;
+    acc[4] += w.y;
+    acc[5] += w.z;
+    acc[6] += dot(rv, zv);
+    acc[7] += dot(rv, rv);
+  }
+  cta_sum<8, kAggThreads>(acc, sh);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 6; ++k) s[6 * a + k] = acc[k] * scale[6 * a + k];
+    aparts[2 * a] = acc[6];
+    aparts[2 * a + 1] = acc[7];
+  }
+  grid_barrier(bar);
+  if (wid < 6) {  // coarse rows of this aggregate: s was written by every CTA (coherent loads)
+    const int i = 6 * a + wid;
+    const double* row = Ainv + (int64_t)i * n_pad;
+    double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    int j = lane;
+    for (; j + 96 < n_pad; j += 128) {
+      const double a0 = __ldg(row + j), a1 = __ldg(row + j + 32), a2 = __ldg(row + j + 64), a3 = __ldg(row + j + 96);
+      const double b0 = __ldcg(s + j), b1 = __ldcg(s + j + 32), b2 = __ldcg(s + j + 64), b3 = __ldcg(s + j + 96);
+      c0 += a0 * b0;
+      c1 += a1 * b1;
+      c2 += a2 * b2;
+      c3 += a3 * b3;
+    }
+    for (; j < n_pad; j += 32) c0 += __ldg(row + j) * __ldcg(s + j);
+    const double ac = warp_sum((c0 + c1) + (c2 + c3));
+    if (lane == 0) {
+      ya[wid] = scale[i] * ac;
+      sy[wid] = __ldcg(s + i) * ac;
+    }
+  }
+  __syncthreads();
+  const d3 t = mk3(ya[0], ya[1], ya[2]), om = mk3(ya[3], ya[4], ya[5]);
+  for (int e = e0 + threadIdx.x; e < e1; e += kAggThreads) {
+    const int v = agg_verts[e];
+    const d3 u = t + cross(om, ld3(dvec, v));
+    const d3 m = ld3(mask, v);
+    z[3 * v] += m.x * u.x;
+    z[3 * v + 1] += m.y * u.y;
+    z[3 * v + 2] += m.z * u.z;
+  }
+  double d[1] = {threadIdx.x == 0 ? ((sy[0] + sy[1]) + (sy[2] + sy[3])) + (sy[4] + sy[5]) : 0.0};
+  double out[1];
+  if (block_reduce_last<1, kAggThreads>(d, rs, out) && threadIdx.x == 0) {
+    double rzb = 0, rr = 0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      rzb += __ldcg(aparts + 2 * b);
+      rr += __ldcg(aparts + 2 * b + 1);
+    }
+    const double rz = rzb + out[0];
+    const double rz_old = scal[0];
+    scal[3] = rz_old != 0 ? rz / rz_old : 0.0;
+    scal[0] = rz;
+    scal[4] = rr;
   }
 }
 
@@ -765,6 +1078,15 @@ struct SystemImpl {
   DBuf<double> minv2, r2;   // vertex-pair block-Jacobi: [v][3x6] rows, r ping-pong
   DBuf<int32_t> pair_d;      // vertex-pair partner (-1: none), from the elastic matrix
   bool has_pairs = false;
+  // preconditioner of the single-system PCG (runtime: GMCP_PAIR_JACOBI, GMCP_COARSE, GMCP_COARSE_AGGS)
+  bool use_pair = true, use_coarse = true;
+  int coarse_aggs = 128;
+  CoarseSpace cs;            // two-level coarse space (coarse.cuh)
+  int coop_blocks = 0;       // co-resident CTAs of the fused cooperative kernel (0: not queried)
+  int64_t load_step = 0;     // current load step (coarse refresh policy)
+  bool coarse_refresh_always = false;  // GMCP_COARSE_REFRESH=1: new coarse inverse every solve
+  bool use_coop = false;     // GMCP_COOP=1: update + coarse as one cooperative kernel (measured slower)
+  int64_t u_gen = 0;         // union pattern generation (coarse pair lists follow it)
   DBuf<unsigned int> counter;
   DBuf<unsigned long long> redu;
   DBuf<int32_t> k_rowptr, k_cols;
@@ -811,7 +1133,7 @@ struct SystemImpl {
   struct PcgKey {
     MatSet M;
     int nv, lanes, gsp, gup;
-    const void* ptrs[11];
+    const void* ptrs[14];
   } pcg_key;
   cudaGraphExec_t pcg_exec = nullptr;
 
@@ -915,7 +1237,7 @@ void build_elastic(SystemImpl& S) {
   S.el_nnzb = (int64_t)cols.size();
 #if GMCP_PAIR_JACOBI
   S.has_pairs = false;
-  if (S.n_scenes <= 1) {  // vertex pairs (single systems; batched scenes use the per-scene CTA PCG) for the 6x6 block-Jacobi: greedy matching of the strongest
+  if (S.n_scenes <= 1 && S.use_pair) {  // vertex pairs (single systems; batched scenes use the per-scene CTA PCG) for the 6x6 block-Jacobi: greedy matching of the strongest
      // normalized elastic couplings |K_vw|_F^2 / (|K_vv|_F |K_ww|_F) (ties by index)
     std::vector<double> dn(nv, 0.0);
     for (int v = 0; v < nv; ++v)
@@ -1048,6 +1370,7 @@ void build_union(SystemImpl& S) {
   S.u_vals.resize(std::max<int64_t>(9 * S.u_nnzb, 1));
   S.sync();
   S.u_valid = true;
+  ++S.u_gen;
 }
 
 // solver.hpp:256-269
@@ -1145,6 +1468,200 @@ double assemble(SystemImpl& S, double lambda) {
   return from_ord_bits(u);
 }
 
+// Coarse space of the two-level preconditioner (coarse.cuh), host side, per
+// solve set-up: each body's rest bounding box is cut into a grid of roughly
+// cubic cells, ~coarse_aggs cells over the system in proportion to the bodies'
+// vertex counts (a thin body gets one cell through its thickness); the
+// vertices of one cell form an aggregate (empty cells form none).
+void build_coarse(SystemImpl& S, const std::vector<double>& mask) {
+  CoarseSpace& C = S.cs;
+  C.enabled = false;
+  if (!S.use_coarse || S.n_scenes > 1) return;
+  const int nv = S.nv();
+  std::vector<int32_t> agg(nv, -1);
+  int n_agg = 0;
+  for (const Body& b : S.bodies) {
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int v = 0; v < b.nv; ++v)
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = std::min(lo[k], b.verts[3 * v + k]);
+        hi[k] = std::max(hi[k], b.verts[3 * v + k]);
+      }
+    const double kb = std::max(1.0, (double)S.coarse_aggs * b.nv / std::max(1, nv));
+    double L[3];
+    for (int k = 0; k < 3; ++k) L[k] = std::max(hi[k] - lo[k], 1e-12 * std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-300}));
+    // cell size h with prod max(1, round(L/h)) ~ kb (bisection on log h)
+    auto cells = [&](double h, int* g) {
+      double p = 1;
+      for (int k = 0; k < 3; ++k) {
+        const double c = std::min(std::max(1.0, std::floor(L[k] / h + 0.5)), 4095.0);
+        g[k] = (int)c;
+        p *= c;
+      }
+      return p;
+    };
+    const double lmax = std::max({L[0], L[1], L[2]});
+    double hl = lmax * 1e-6, hh = lmax * 2;
+    int g[3];
+    for (int it = 0; it < 200; ++it) {
+      const double hm = std::sqrt(hl * hh);
+      if (cells(hm, g) > kb) hl = hm; else hh = hm;
+    }
+    cells(hh, g);
+    std::map<int64_t, int32_t> id;
+    for (int v = 0; v < b.nv; ++v) {
+      int64_t key = 0;
+      for (int k = 0; k < 3; ++k) {
+        const int c = std::min(g[k] - 1, std::max(0, (int)((b.verts[3 * v + k] - lo[k]) / L[k] * g[k])));
+        key = key * 4096 + c;
+      }
+      auto it = id.find(key);
+      if (it == id.end()) it = id.emplace(key, 0).first;
+      agg[b.offset + v] = (int32_t)key;  // replaced by a dense id below
+    }
+    int32_t next = n_agg;
+    for (auto& kv : id) kv.second = next++;  // cells in (x, y, z) order
+    for (int v = 0; v < b.nv; ++v) agg[b.offset + v] = id[agg[b.offset + v]];
+    n_agg = next;
+  }
+  for (int v = 0; v < nv; ++v)
+    if (agg[v] < 0) return;  // a vertex outside every body: no coarse space
+  std::vector<double> cen(3 * (size_t)n_agg, 0.0), dvec(3 * (size_t)nv), gram(36 * (size_t)n_agg, 0.0);
+  std::vector<int32_t> off(n_agg + 1, 0), verts(nv);
+  for (int v = 0; v < nv; ++v) ++off[agg[v] + 1];
+  for (int a = 0; a < n_agg; ++a) off[a + 1] += off[a];
+  {
+    std::vector<int32_t> fill(off.begin(), off.end() - 1);
+    for (int v = 0; v < nv; ++v) verts[fill[agg[v]]++] = v;  // ascending within an aggregate
+  }
+  for (int a = 0; a < n_agg; ++a) {
+    for (int e = off[a]; e < off[a + 1]; ++e)
+      for (int k = 0; k < 3; ++k) cen[3 * a + k] += S.rest[3 * (size_t)verts[e] + k];
+    for (int k = 0; k < 3; ++k) cen[3 * a + k] /= std::max(1, off[a + 1] - off[a]);
+  }
+  for (int v = 0; v < nv; ++v) {
+    const int a = agg[v];
+    const double d[3] = {S.rest[3 * (size_t)v] - cen[3 * a], S.rest[3 * (size_t)v + 1] - cen[3 * a + 1],
+                         S.rest[3 * (size_t)v + 2] - cen[3 * a + 2]};
+    for (int k = 0; k < 3; ++k) dvec[3 * (size_t)v + k] = d[k];
+    // Phi_v = M [I | -[d]x] (3 x 6)
+    const double cx[3][3] = {{0, -d[2], d[1]}, {d[2], 0, -d[0]}, {-d[1], d[0], 0}};
+    double Phi[3][6];
+    for (int i = 0; i < 3; ++i) {
+      const double m = mask[3 * (size_t)v + i];
+      for (int j = 0; j < 3; ++j) {
+        Phi[i][j] = m * (i == j ? 1.0 : 0.0);
+        Phi[i][3 + j] = -m * cx[i][j];
+      }
+    }
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j)
+        for (int q = 0; q < 3; ++q) gram[36 * (size_t)a + 6 * i + j] += Phi[q][i] * Phi[q][j];
+  }
+  C.n_agg = n_agg;
+  C.n_pad = ((6 * n_agg + kGJ - 1) / kGJ) * kGJ;
+  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+  if (trace) std::fprintf(stderr, "[gmcp] coarse space: %d aggregates, %d coarse dofs (padded)\n", n_agg, C.n_pad);
+  C.agg.upload(agg, S.stream);
+  C.dvec.upload(dvec, S.stream);
+  C.agg_off.upload(off, S.stream);
+  C.agg_verts.upload(verts, S.stream);
+  C.gram.upload(gram, S.stream);
+  const size_t n2 = (size_t)C.n_pad * C.n_pad;
+  C.A.resize(n2);
+  C.B.resize(n2);
+  C.scale.resize(C.n_pad);
+  C.s.resize(C.n_pad);
+  C.y.resize(C.n_pad);
+  C.s.zero(S.stream);
+  C.y.zero(S.stream);
+  C.pat_gen = -2;  // pair lists rebuilt at the first solve
+  C.enabled = true;
+}
+
+// Coarse operator of this solve's operand (single merged BCSR M.el) and its
+// scaled pseudo-inverse. Pair lists are rebuilt when the pattern changed.
+void coarse_setup_impl(SystemImpl& S, const MatSet& M);
+void coarse_setup(SystemImpl& S, const MatSet& M) {
+  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+  if (!trace) return coarse_setup_impl(S, M);
+  const auto t0 = std::chrono::steady_clock::now();
+  coarse_setup_impl(S, M);
+  S.sync();
+  std::fprintf(stderr, "[gmcp] coarse setup %.3f ms (%d aggregate pairs, %d coarse dofs)\n",
+               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), S.cs.n_pairs,
+               S.cs.n_pad);
+}
+void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
+  CoarseSpace& C = S.cs;
+  const int nv = S.nv();
+  const Bcsr& A = M.el;
+  int64_t nnzb = 0;
+  GMCP_CUDA(cudaMemcpyAsync(&nnzb, &A.rowptr[nv], sizeof(int32_t), cudaMemcpyDeviceToHost, S.stream));
+  S.sync();
+  nnzb = (int64_t)(int32_t)nnzb;
+  const int64_t gen = S.u_valid ? S.u_gen : -1;
+  if (C.pat_rowptr != A.rowptr || C.pat_cols != A.cols || C.pat_nnzb != nnzb || C.pat_gen != gen) {
+    const int64_t m = std::max<int64_t>(nnzb, 1);
+    C.u_row.resize(m);
+    C.blk.resize(m);
+    C.blk2.resize(m);
+    C.key.resize(m);
+    C.key2.resize(m);
+    C.ukey.resize(m);
+    C.pcnt.resize(m + 1);
+    C.poff.resize(m + 1);
+    C.npair.resize(1);
+    k_block_rows<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, A.rowptr, C.u_row.p);
+    k_pair_keys<<<grid_for(nnzb, 256), 256, 0, S.stream>>>(nnzb, C.u_row.p, A.cols, C.agg.p, C.n_agg, C.key.p,
+                                                           C.blk.p);
+    S.launches += 2;
+    int kb = 1;
+    while ((1ull << kb) <= (unsigned long long)C.n_agg * C.n_agg) ++kb;
+    sort_pairs(C.key.p, C.key2.p, C.blk.p, C.blk2.p, nnzb, S.stream, kb);
+    run_length_encode(C.key2.p, C.ukey.p, C.pcnt.p, C.npair.p, nnzb, S.stream);
+    int32_t np = 0;
+    unsigned long long last = 0;
+    GMCP_CUDA(cudaMemcpyAsync(&np, C.npair.p, sizeof np, cudaMemcpyDeviceToHost, S.stream));
+    S.sync();
+    if (np > 0) {
+      GMCP_CUDA(cudaMemcpyAsync(&last, C.ukey.p + np - 1, sizeof last, cudaMemcpyDeviceToHost, S.stream));
+      S.sync();
+      if (last == (unsigned long long)C.n_agg * C.n_agg) --np;  // lower-tile blocks (sentinel key)
+    }
+    GMCP_CUDA(cudaMemsetAsync(C.pcnt.p + np, 0, sizeof(int32_t), S.stream));
+    exclusive_scan(C.pcnt.p, C.poff.p, (int64_t)np + 1, S.stream);
+    C.n_pairs = np;
+    C.pat_rowptr = A.rowptr;
+    C.pat_cols = A.cols;
+    C.pat_nnzb = nnzb;
+    C.pat_gen = gen;
+  }
+  const int n_pad = C.n_pad;
+  GMCP_CUDA(cudaMemsetAsync(C.A.p, 0, (size_t)n_pad * n_pad * sizeof(double), S.stream));
+  if (C.n_pairs > 0)
+    k_coarse_assemble<<<C.n_pairs, 256, 0, S.stream>>>(
+        C.n_pairs, C.n_agg, n_pad, C.ukey.p, C.poff.p, C.pcnt.p, C.blk2.p, C.u_row.p, A.cols, A.vals, A.bs, A.cs,
+        S.mask_d.p, C.dvec.p, C.gram.p, M.shift, C.A.p);
+  k_coarse_scale<<<grid_for(n_pad, 256), 256, 0, S.stream>>>(n_pad, C.A.p, C.scale.p);
+  k_coarse_apply_scale<<<grid_for((int64_t)n_pad * n_pad, 256), 256, 0, S.stream>>>(n_pad, C.A.p, C.scale.p);
+  S.launches += 3;
+  const int nt = n_pad / kGJ;
+  double* X = C.A.p;
+  double* Y = C.B.p;
+  GMCP_CUDA(cudaMemsetAsync(S.redu.p + 4, 0, sizeof(unsigned long long), S.stream));
+  C.piv.resize(2 * kGJ * kGJ);
+  k_gj_pivot0<<<1, 32, 0, S.stream>>>(n_pad, X, C.piv.p, kCoarseDrop, S.redu.p + 4);
+  ++S.launches;
+  for (int k = 0; k < nt; ++k) {
+    k_gj_step<<<dim3(nt, nt), 256, 0, S.stream>>>(n_pad, k, X, Y, C.piv.p + (k & 1) * kGJ * kGJ,
+                                                  C.piv.p + ((k + 1) & 1) * kGJ * kGJ, kCoarseDrop, S.redu.p + 4);
+    ++S.launches;
+    std::swap(X, Y);
+  }
+  C.inv = X;
+}
+
 // ||H dx - rhs|| of the solve just finished (recomputed, not the recursive
 // residual PCG stops on); optionally copies the linear system to the host.
 void true_residual(SystemImpl& S, const MatSet& M) {
@@ -1212,18 +1729,71 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
   MatSet M = mats(S);
   M.shift = shift;
   const bool pairs = S.has_pairs && S.pair_d.n == nv;
+  const bool coarse = S.cs.enabled && M.np == 0;
+  CoarseSpace& C = S.cs;
+  if (coarse) {
+    const int64_t gen = S.u_valid ? S.u_gen : -1;
+    // reuse only once Newton is steady: the last two solves ran on fresh
+    // inverses with iteration counts within 15% (the contact Hessian settled)
+    const bool steady = C.prev_fresh_iters > 0 && C.ref_iters > 0 &&
+                        std::abs(C.ref_iters - C.prev_fresh_iters) <= 0.15 * C.prev_fresh_iters;
+    const bool stale = !C.have_inv || C.inv_step != S.load_step || C.inv_gen != gen || C.inv_shift != M.shift ||
+                       S.coarse_refresh_always || !steady ||
+                       (C.ref_iters > 0 && C.last_iters > kCoarseStale * C.ref_iters);
+    if (stale) {
+      const bool same_context = C.have_inv && C.inv_step == S.load_step && C.inv_gen == gen && C.inv_shift == M.shift;
+      C.prev_fresh_iters = same_context ? C.ref_iters : -1;
+    }
+    if (stale) {
+      coarse_setup(S, M);
+      C.have_inv = true;
+      C.inv_step = S.load_step;
+      C.inv_gen = gen;
+      C.inv_shift = M.shift;
+      C.ref_iters = -1;  // set by this solve
+    }
+  }
+  // the fused cooperative update + coarse kernel needs all aggregates co-resident
+  if (coarse && S.coop_blocks == 0) {
+    int occ = 0, sms = 0;
+    GMCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_coarse<true>, kAggThreads, 0));
+    int occ2 = 0;
+    GMCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_update_coarse<false>, kAggThreads, 0));
+    GMCP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, S.device));
+    S.coop_blocks = std::max(1, std::min(occ, occ2) * sms);
+  }
+  const bool coop = coarse && S.use_coop && C.n_agg <= S.coop_blocks;
+  if (coop) C.aparts.resize(2 * (int64_t)C.n_agg);
+  // two-level init: z += P Ac^+ P^T r, completing r.z (beta = 0)
+  auto coarse_init = [&]() {
+    k_restrict<<<C.n_agg, 256, 0, S.stream>>>(C.n_agg, C.agg_off.p, C.agg_verts.p, C.dvec.p, S.mask_d.p, S.r.p,
+                                            C.scale.p, C.s.p);
+    k_coarse_prolong<true><<<C.n_agg, kAggThreads, 0, S.stream>>>(C.n_pad, C.inv, C.scale.p, C.s.p, C.agg_off.p,
+                                                               C.agg_verts.p, C.dvec.p, S.mask_d.p, S.z.p, S.scal.p,
+                                                               S.slot(6));
+    S.launches += 2;
+  };
   if (pairs) {
     S.minv2.resize(18 * (int64_t)nv);
     S.r2.resize(3 * (int64_t)nv);
     k_pair_jacobi<<<grid_for(nv, 128), 128, 0, S.stream>>>(nv, M, S.mask_d.p, S.pair_d.p, S.minv2.p);
-    k_pcg_init_pair<<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv2.p, S.pair_d.p, S.dx.p,
+    if (coarse)
+      k_pcg_init_pair<true><<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv2.p, S.pair_d.p, S.dx.p,
+                                                                S.r.p, S.z.p, S.p.p, S.scal.p, S.slot(0));
+    else
+    k_pcg_init_pair<false><<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv2.p, S.pair_d.p, S.dx.p,
                                                         S.r.p, S.z.p, S.p.p, S.scal.p, S.slot(0));
   } else {
     k_block_jacobi<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, M, S.mask_d.p, S.minv.p);
-    k_pcg_init<<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p, S.p.p,
+    if (coarse)
+      k_pcg_init<true><<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p,
+                                                           S.p.p, S.scal.p, S.slot(0));
+    else
+    k_pcg_init<false><<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p, S.p.p,
                                                    S.scal.p, S.slot(0));
   }
   S.launches += 2;
+  if (coarse) coarse_init();
   double h[9];
   GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
   S.sync();
@@ -1248,9 +1818,12 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
   key.lanes = lanes;
   key.gsp = gsp;
   key.gup = gup;
-  const void* ptrs[11] = {S.mask_d.p, S.z.p, S.p.p, S.w.p, S.q.p, S.dx.p, S.r.p,
+  const void* ptrs[14] = {S.mask_d.p, S.z.p, S.p.p, S.w.p, S.q.p, S.dx.p, S.r.p,
                           pairs ? (const void*)S.minv2.p : (const void*)S.minv.p, S.scal.p,
-                          pairs ? (const void*)S.r2.p : (const void*)S.parts.p, S.counter.p};
+                          pairs ? (const void*)S.r2.p : (const void*)S.parts.p, S.counter.p,
+                          coarse ? (const void*)C.inv : nullptr, coarse ? (const void*)C.s.p : nullptr,
+                          coarse ? (coop ? (const void*)C.aparts.p : (const void*)C.agg.p) : nullptr};
+  static_assert(sizeof ptrs == sizeof key.ptrs, "PcgKey pointer list");
   std::memcpy(key.ptrs, ptrs, sizeof ptrs);
   auto same_bcsr = [](const Bcsr& a, const Bcsr& b) {
     return a.rowptr == b.rowptr && a.cols == b.cols && a.vals == b.vals && a.bs == b.bs && a.cs == b.cs;
@@ -1276,13 +1849,48 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
       else
         k_spmv_cg<4><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
                                                       S.slot(1));
-      if (pairs)  // r ping-pongs with p (chunk is even: r ends in S.r)
-        k_update_cg_pair<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, (k & 1) ? S.r2.p : S.r.p,
-                                                         (k & 1) ? S.r.p : S.r2.p, S.z.p, S.minv2.p, S.pair_d.p,
-                                                         S.scal.p, S.slot(2));
-      else
-        k_update_cg<<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p, S.scal.p,
-                                                    S.slot(2));
+      if (coarse) {  // update + restriction, then coarse solve + prolongation (per aggregate)
+        const double* rin = pairs ? ((k & 1) ? S.r2.p : S.r.p) : S.r.p;
+        double* rout = pairs ? ((k & 1) ? S.r.p : S.r2.p) : S.r.p;
+        if (coop) {  // one cooperative kernel (grid barrier between the two halves)
+          cudaLaunchConfig_t cfg{};
+          cfg.gridDim = dim3(C.n_agg);
+          cfg.blockDim = dim3(kAggThreads);
+          cfg.stream = S.stream;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeCooperative;
+          at[0].val.cooperative = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          const double* mi = pairs ? S.minv2.p : S.minv.p;
+          const int32_t* pd = pairs ? S.pair_d.p : nullptr;
+          GMCP_CUDA(cudaLaunchKernelEx(&cfg, pairs ? k_update_coarse<true> : k_update_coarse<false>,
+                                       (const int32_t*)C.agg_off.p, (const int32_t*)C.agg_verts.p,
+                                       (const double*)C.dvec.p, (const double*)S.mask_d.p, (const double*)C.scale.p,
+                                       (const double*)p_new, (const double*)S.q.p, S.dx.p, rin, rout, S.z.p, mi, pd,
+                                       C.s.p, C.n_pad, (const double*)C.inv, C.aparts.p, S.counter.p + 8, S.scal.p,
+                                       S.slot(2)));
+        } else {
+          if (pairs)
+            k_update_agg<true><<<C.n_agg, kAggThreads, 0, S.stream>>>(
+                C.agg_off.p, C.agg_verts.p, C.dvec.p, S.mask_d.p, C.scale.p, p_new, S.q.p, S.dx.p, rin, rout, S.z.p,
+                S.minv2.p, S.pair_d.p, C.s.p, S.scal.p, S.slot(2));
+          else
+            k_update_agg<false><<<C.n_agg, kAggThreads, 0, S.stream>>>(
+                C.agg_off.p, C.agg_verts.p, C.dvec.p, S.mask_d.p, C.scale.p, p_new, S.q.p, S.dx.p, rin, rout, S.z.p,
+                S.minv.p, nullptr, C.s.p, S.scal.p, S.slot(2));
+          k_coarse_prolong<false><<<C.n_agg, kAggThreads, 0, S.stream>>>(C.n_pad, C.inv, C.scale.p, C.s.p,
+                                                                      C.agg_off.p, C.agg_verts.p, C.dvec.p,
+                                                                      S.mask_d.p, S.z.p, S.scal.p, S.slot(6));
+        }
+      } else if (pairs) {  // r ping-pongs with p (chunk is even: r ends in S.r)
+        k_update_cg_pair<false><<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, (k & 1) ? S.r2.p : S.r.p,
+                                                                (k & 1) ? S.r.p : S.r2.p, S.z.p, S.minv2.p,
+                                                                S.pair_d.p, S.scal.p, S.slot(2));
+      } else {
+        k_update_cg<false><<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, S.r.p, S.z.p, S.minv.p,
+                                                           S.scal.p, S.slot(2));
+      }
     }
     GMCP_CUDA(cudaStreamEndCapture(S.stream, &graph));
     GMCP_CUDA(cudaGraphInstantiate(&S.pcg_exec, graph, 0));
@@ -1291,6 +1899,9 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
   }
   cudaGraphExec_t exec = S.pcg_exec;
   int it = 0;
+  // with the coarse space a converging solve gains orders of magnitude per
+  // 256 iterations, so a singular one is recognised four times sooner
+  const int stag = coarse ? kStagWindowCoarse : kStagWindow;
   double win_min = INFINITY, prev_min = INFINITY;  // stagnation windows
   if (!S.ev0) {
     GMCP_CUDA(cudaEventCreate(&S.ev0));
@@ -1300,7 +1911,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     GMCP_CUDA(cudaEventRecord(S.ev0, S.stream));
     GMCP_CUDA(cudaGraphLaunch(exec, S.stream));
     GMCP_CUDA(cudaEventRecord(S.ev1, S.stream));
-    S.launches += 2 * chunk;
+    S.launches += (coarse && !coop ? 3 : 2) * chunk;
     it += chunk;
     GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
     S.sync();
@@ -1311,8 +1922,8 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     if (!std::isfinite(h[4])) throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
     if (!(h[4] > target)) break;  // rr <= tol^2 bb
     win_min = std::min(win_min, h[4]);
-    if (it % kStagWindow == 0) {
-      if (it >= 2 * kStagWindow && !(win_min < 0.5 * prev_min) && h[4] > 1e-8 * bb) break;  // stagnated
+    if (it % stag == 0) {
+      if (it >= 2 * stag && !(win_min < 0.5 * prev_min) && h[4] > 1e-8 * bb) break;  // stagnated
       prev_min = std::min(prev_min, win_min);
       win_min = INFINITY;
     }
@@ -1333,6 +1944,10 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
 constexpr int kMaxRefine = 3;
 int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.0) {
   int it = pcg_core(S, tol, maxit, rel_out, shift, S.grad.p);
+  if (S.cs.enabled) {  // coarse refresh policy bookkeeping
+    S.cs.last_iters = it;
+    if (S.cs.ref_iters < 0) S.cs.ref_iters = it;
+  }
   MatSet M = mats(S);
   M.shift = shift;
   if (*rel_out == 0) {  // zero rhs: dx = 0 exactly
@@ -1385,9 +2000,9 @@ void setup_solve(SystemImpl& S, int64_t& n_free, DBuf<double>& eps_ref) {
   S.eel.resize(4);
   S.lsco.resize(4);
   S.parts.resize(kBlocks * 4);
-  S.counter.resize(8);
+  S.counter.resize(16);
   S.counter.zero(S.stream);
-  S.redu.resize(4);
+  S.redu.resize(8);
   S.x.upload(S.x_host, S.stream);
   S.dx.zero(S.stream);
   S.rest_d.upload(S.rest, S.stream);
@@ -1395,6 +2010,11 @@ void setup_solve(SystemImpl& S, int64_t& n_free, DBuf<double>& eps_ref) {
   std::vector<double> mask(n);
   for (int64_t d = 0; d < n; ++d) mask[d] = S.fixed[d] ? 0.0 : 1.0;
   S.mask_d.upload(mask, S.stream);
+  if (S.pcg_exec) {  // the coarse space (and its launch shapes) is rebuilt below
+    cudaGraphExecDestroy(S.pcg_exec);
+    S.pcg_exec = nullptr;
+  }
+  build_coarse(S, mask);
   eps_ref.resize(n);
   GMCP_CUDA(cudaMemcpyAsync(eps_ref.p, S.x.p, n * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
   for (auto& pr : S.pairs) {
@@ -2355,6 +2975,7 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
   out->newton_tol_used = tol;
   for (int step = 1; step <= st.load_steps; ++step) {
     const double lambda = (double)step / st.load_steps;
+    S.load_step = step;
     gmcp_step_stats ss{};
     ss.step = step;
     ss.min_gap = 1.7976931348623157e308;
@@ -2369,10 +2990,19 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
     double energy = e_el + ce.energy - lambda * work;
     ss.min_gap = std::min(ss.min_gap, ce.min_gap);
     bool converged = false;
+    static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+    auto tp = [&]() {
+      if (trace) S.sync();
+      return std::chrono::steady_clock::now();
+    };
+    auto dms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
     for (int it = 0; it < st.max_newton_iters; ++it) {
       const auto t_it = std::chrono::steady_clock::now();
       const int64_t pcg_before = ss.pcg_iters;
       if (it > 0) resid = assemble(S, lambda);
+      const auto t_as = tp();
       if (resid <= tol) {
         converged = true;
         break;
@@ -2402,6 +3032,7 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
       record_accepted_solve(S);
       ss.pcg_iters += pit;
       ss.newton_iters += 1;
+      const auto t_pcg = tp();
       double alpha = 1.0;
       for (auto& pr : S.pairs) {
         alpha = std::min(alpha, run_step_filter(*pr->c));
@@ -2463,6 +3094,11 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
         ce = contact_energy_at(S, S.x.p);
         if (!ce.feasible) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
         energy = e_el + ce.energy - lambda * work;
+      }
+      if (trace) {
+        const auto t_end = tp();
+        std::fprintf(stderr, "[gmcp] newton %d: assemble %.3f ms, linear solve %.3f ms (%d PCG), line search + "
+                             "rebuild %.3f ms\n", it, dms(t_it, t_as), dms(t_as, t_pcg), pit, dms(t_pcg, t_end));
       }
       if (S.iter_limit > 0) {  // timing mode (gmcp_system_time_newton)
         S.sync();
@@ -2555,6 +3191,11 @@ int gmcp_system_create(int device, gmcp_system** out) {
     s->s.device = device;
     const DeviceBind bind_(device, &s->s.cub);
     GMCP_CUDA(cudaStreamCreateWithFlags(&s->s.stream, cudaStreamNonBlocking));
+    if (const char* e = std::getenv("GMCP_PAIR_JACOBI")) s->s.use_pair = std::atoi(e) != 0;
+    if (const char* e = std::getenv("GMCP_COARSE")) s->s.use_coarse = std::atoi(e) != 0;
+    if (const char* e = std::getenv("GMCP_COARSE_AGGS")) s->s.coarse_aggs = std::min(512, std::max(1, std::atoi(e)));
+    if (const char* e = std::getenv("GMCP_COOP")) s->s.use_coop = std::atoi(e) != 0;
+    if (const char* e = std::getenv("GMCP_COARSE_REFRESH")) s->s.coarse_refresh_always = std::atoi(e) != 0;
     *out = s;
     return GMCP_OK;
   } catch (const StatusError& e) {
@@ -2610,6 +3251,7 @@ int gmcp_system_set_vertex_scenes(gmcp_system* sys, const int32_t* scene, int64_
   return sguard(const_cast<gmcp_system*>(sys), [&] {
     if (!sys) throw StatusError(GMCP_ERR_ARG, "null system");
     SystemImpl& S = sys->s;
+    S.el_built = false;  // the vertex pairing / coarse space depend on the scene layout
     if (!scene) {
       S.vscene.clear();
       S.scene_voff.clear();
