@@ -130,26 +130,57 @@ def profiled_traffic():
         return None
 
 
-def pcg_roofline(ps: dict) -> dict:
-    """HBM roofline of one PCG iteration (SpMV + update kernels), device time
-    from CUDA events around the chunk graphs of every PCG solve in the timed
-    Newton run. Algorithmic bytes per iteration:
-      SpMV   76 B per 3x3 block of the merged operand (72 B values + 4 B column)
-             + per row 4 B row pointer and 24 B each of z, p_old, mask read and
-             p_new, q written (124 B);
-      update 24 B each of p, q, x, r read, x, r, z written, the vertex-pair
-             block-Jacobi rows (3x6 = 144 B) and the partner's r and q (48 B):
-             360 B per row."""
+def pcg_roofline(ps: dict, pre: dict | None = None) -> dict:
+    """HBM roofline of one PCG iteration, device time from CUDA events around
+    the chunk graphs of every PCG solve in the timed Newton run. Algorithmic
+    bytes per iteration:
+      SpMV    76 B per 3x3 block of the merged operand (72 B values + 4 B column)
+              + per row 4 B row pointer and 24 B each of z, p_old, mask read and
+              p_new, q written (124 B);
+      update  24 B each of p, q, x, r read and x, r, z written (168 B), the
+              vertex-pair block-Jacobi rows (3x6 = 144 B) + 4 B pair index
+              (316 B/row; the partner's r and q rows are L2 hits of rows another
+              thread streams, not counted);
+      two-level (coarse space on): the restriction fused into the update reads
+              mask + aggregate offset + vertex id (52 B/row); the coarse solve +
+              prolongation reads the dense coarse inverse (8 n_pad^2 B) and per
+              row vertex id, offset, mask and z, writes z (100 B/row)."""
     if not ps["iters"]:
         return None
     peak, src = peaks()
-    per_iter = 76 * ps["nnzb"] + (124 + 360) * ps["rows"]
+    row = 124 + (316 if (pre is None or pre["pair_jacobi"]) else 168 + 72)
+    coarse = bool(pre and pre["coarse"])
+    if coarse:
+        row += 52 + 100
+    per_iter = 76 * ps["nnzb"] + row * ps["rows"] + (8 * pre["coarse_padded"] ** 2 if coarse else 0)
     ms = ps["ms"] / ps["iters"]
     achieved = per_iter / (ms / 1e3) / 1e9
-    return {"bound": "hbm", "kernels": "k_spmv_cg + k_update_cg (one PCG iteration)", "achieved": achieved,
+    kern = "k_spmv_cg + k_update_agg + k_coarse_prolong" if coarse else "k_spmv_cg + k_update_cg_pair"
+    return {"bound": "hbm", "kernels": kern + " (one PCG iteration)", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "algorithmic_bytes": per_iter,
             "us_per_iter": 1e3 * ms, "iters_timed": ps["iters"], "operand_blocks": ps["nnzb"], "rows": ps["rows"],
-            "peak_source": src, "clock": "CUDA events around each 16-iteration chunk graph on the solve stream"}
+            "preconditioner": pre, "peak_source": src,
+            "clock": "CUDA events around each 16-iteration chunk graph on the solve stream"}
+
+
+def cpu_newton_reference(refine: float = 0.7):
+    """The reference's own System::solve (solver.hpp:125-228) through run_hertz
+    (bench.hpp:210-303) on C1, compiled from the reference sources (oracle/_ref;
+    the Eigen shim's SimplicialLDLT stand-in with an RCM ordering), 1 thread:
+    Newton iterations per second of the whole 10-step solve."""
+    import ctypes as C
+    lib = os.path.join(ROOT, "oracle", "_ref", "libgmcp_ref.so")
+    if not os.path.exists(lib):
+        return None
+    L = C.CDLL(lib)
+    v = np.zeros(14)
+    rc = L.ref_run_hertz(C.c_double(refine), C.c_int32(10), C.c_void_p(v.ctypes.data))
+    if rc != 0:
+        return None
+    return {"newton_iters": int(v[8]), "wall_seconds": float(v[11]), "steps_per_s": float(v[8] / v[11]),
+            "peak": float(v[0]), "cores": 1, "kind": "reference",
+            "sample": f"C1 Hertz (refine {refine}) full 10-load-step solve, reference System::solve via run_hertz, "
+                      "oracle/_ref (shim SimplicialLDLT with RCM ordering), 1 thread"}
 
 
 def cpu_baseline(scene, samples: dict, x: np.ndarray, seconds_budget: float = 20.0, threads: int | None = None):
@@ -263,6 +294,7 @@ def main():
     ap.add_argument("--newton-iters", type=int, default=5)
     ap.add_argument("--no-batched", action="store_true")
     ap.add_argument("--batch-scenes", type=int, default=1024)
+    ap.add_argument("--no-job", action="store_true", help="skip the full C5 solve + result gather")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -352,6 +384,38 @@ def main():
         e2e_s = float(t[0])
     e2e = world * n * args.steps / e2e_s
 
+    # drop-in end to end: the reference's add_contact_gradient_hessian(state,
+    # params, x, grad, H) RETURNS H to the caller. Per step: the single-call
+    # assembly above plus the download of the Gauss-Newton Hessian (BCSR:
+    # row pointers, columns, 3x3 values) into host memory.
+    ctx.add_gradient(xh, gh, hessian=True)
+    rp_h, cl_h, vl_h = ctx.download_hessian()
+    hbytes = int(rp_h.nbytes + cl_h.nbytes + vl_h.nbytes)
+    pinned = (torch.empty(rp_h.size, dtype=torch.int32, pin_memory=True).numpy(),
+              torch.empty(cl_h.size, dtype=torch.int32, pin_memory=True).numpy(),
+              torch.empty(vl_h.size, dtype=torch.float64, pin_memory=True).numpy().reshape(-1, 3, 3))
+    nd = max(3, args.steps // 5)
+    for _ in range(2):
+        ctx.add_gradient(xh, gh, hessian=True)
+        ctx.download_hessian(pinned)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(nd):
+        ctx.add_gradient(xh, gh, hessian=True)
+        ctx.download_hessian(pinned)
+    e2e_dropin_s = (time.perf_counter() - t0) / nd
+    if dist:
+        t = torch.tensor([e2e_dropin_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_dropin_s = float(t[0])
+    e2e_dropin = {"value": world * n / e2e_dropin_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_dropin_s,
+                  "h2d_bytes_per_step": int(2 * scene.rest.size * 8),
+                  "d2h_bytes_per_step": int(scene.rest.size * 8 + 40 + hbytes),
+                  "path": "gmcp_add_gradient_hessian + gmcp_download_hessian into pinned host buffers: the Hessian "
+                          "returned to the host as BCSR (include/gmcp/b200.hpp then expands it into Eigen triplets, "
+                          "not timed here)"}
+
     # end-of-run result gather (NCCL): per-rank sample counts and energies
     if dist:
         from paper_2605_24339_b200 import dist as D
@@ -367,11 +431,13 @@ def main():
     if not args.no_newton:
         from paper_2605_24339_b200 import system as SY
         nsys = SY.build_slab_system(155, 124, texture_amp=2e-4, device=local)
-        settings = SY.SolverSettings(pcg_tol=1e-8, pcg_max_iters=50000)
+        settings = SY.SolverSettings(pcg_tol=1e-10, pcg_max_iters=50000)  # the product default
         if dist:
             dist.barrier()
         ms_it, pcg_it = nsys.time_newton(settings, args.newton_iters + 1)
         ps = nsys.pcg_stats()
+        pre = nsys.precond_info()
+        lin = nsys.linear_stats()
         steady = ms_it[1:] if ms_it.size > 1 else ms_it
         t = float(np.mean(steady))
         if dist:
@@ -383,18 +449,39 @@ def main():
                   "first_iter_includes": "load-step rebuild + one-time elastic BCSR build (excluded from the mean)",
                   "dofs": int(nsys.rest.size), "samples": int(nsys.num_samples(0)),
                   "clock": "host steady_clock around each iteration (device synchronized)",
-                  "pcg_roofline": pcg_roofline(ps)}
+                  "preconditioner": pre, "true_residual_max": lin["max_rel2"],
+                  "pcg_roofline": pcg_roofline(ps, pre)}
         del nsys
+        # C1 (the CPU reference's own scene): device Newton steps/s and the whole
+        # 10-step solve next to the reference System::solve on the host
+        from paper_2605_24339_b200 import scenes as S
+        c1cfg = S.HertzConfig(refine=0.7)  # C1: refine 0.7, the scene the CPU reference solves below
+        hs, _ = SY.build_hertz_system(c1cfg, device=local)
+        ms_h, pcg_h = hs.time_newton(SY.SolverSettings(), args.newton_iters + 3)
+        del hs
+        t0 = time.perf_counter()
+        hr = SY.run_hertz(c1cfg, device=local)
+        dev_solve = time.perf_counter() - t0
+        newton["c1"] = {"scene": "C1 Hertz (refine 0.7), 3,759 dofs",
+                        "steps_per_s": world * 1e3 / float(np.mean(ms_h[3:])),
+                        "per_iter_ms": [round(float(v), 3) for v in ms_h], "pcg_iters": [int(v) for v in pcg_h],
+                        "solve_seconds": dev_solve, "solve_newton_iters": int(hr.stats.total_newton_iters),
+                        "solve_steps_per_s": hr.stats.total_newton_iters / dev_solve, "peak": hr.peak}
+        del hr
 
-    # C5: the 1024-scene batched job (C1 Hertz scenes), scenes
-    # sharded across ranks as contiguous ranges and packed into one context per
-    # GPU (per-vertex scene ids); no collective on the hot path.
+    # C5: the 1024-scene batched job (C1 Hertz scenes) on the
+    # product path (paper_2605_24339_b200/batch.py): scenes sharded across
+    # ranks by sample-count prefix sums (dist.shard_scenes), each shard packed
+    # into one context / System per GPU; no collective on the hot path; one
+    # NCCL gather of the per-scene results at the end.
     batched = None
     if not args.no_batched:
+        from paper_2605_24339_b200 import batch as B
+        from paper_2605_24339_b200 import dist as D
         from paper_2605_24339_b200 import scenes as S
-        per, extra = divmod(args.batch_scenes, world)
-        first = rank * per + min(rank, extra)
-        count = per + (1 if rank < extra else 0)
+        counts = B.scene_sample_counts(args.batch_scenes, local)
+        first, last = D.shard_scenes(counts, world)[rank]
+        count = last - first
         b = S.c5_batch(args.batch_scenes, first, count)
         bctx = gm.Context(local)
         bctx.set_params(b.params)
@@ -420,10 +507,12 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dist.all_reduce(t2, op=dist.ReduceOp.SUM)
             ms_b, tot = float(t[0]), float(t2[1])
+        del bctx
         # batched Newton: the shard as one device System, every scene
         # with its own residual / step / line search / convergence; timed loop
         # passes 3..8 (pass 1-2: set-up and the singular first load-step solve)
         newton_b = None
+        job = None
         if not args.no_newton:
             from paper_2605_24339_b200 import system as SY
             bsys = SY.build_hertz_batch_system(b, device=local)
@@ -444,15 +533,42 @@ def main():
                         "definition": "scene-Newton-iterations (one scene's assemble + PCG + filter + line search) "
                                       "per second, all scenes of the shard in one batched device solve"}
             del bsys
+            # the whole job end to end: every scene's 10-step solve, then the
+            # per-scene results (final x, StepStats per load step, pressure
+            # records) gathered to rank 0 (one NCCL gather)
+            if not args.no_job:
+                if dist:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                tj = time.perf_counter()
+                res, info = B.run_batch(args.batch_scenes, SY.SolverSettings(), dist=dist, device=local,
+                                        counts=counts)
+                torch.cuda.synchronize()
+                wall = time.perf_counter() - tj
+                its = float(info["scene_newton_iters"])
+                if dist:
+                    t = torch.tensor([wall, info["wall_seconds"]], device="cuda", dtype=torch.float64)
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    wall, solve_s = float(t[0]), float(t[1])
+                    t2 = torch.tensor([its], device="cuda", dtype=torch.float64)
+                    dist.all_reduce(t2, op=dist.ReduceOp.SUM)
+                    its = float(t2[0])
+                else:
+                    solve_s = info["wall_seconds"]
+                job = {"what": f"{args.batch_scenes} scenes x 10 load steps, solved and gathered to rank 0",
+                       "wall_seconds": wall, "solve_seconds_max_rank": solve_s, "scene_newton_iters": int(its),
+                       "scene_newton_steps_per_s": its / wall,
+                       "gather_seconds": info.get("gather_seconds", 0.0), "gather_bytes": info.get("gather_bytes", 0),
+                       "scenes_gathered": len(res) if res is not None else None,
+                       "x_checksum": float(sum(float(r.x.sum()) for r in res)) if res else None}
         batched = {"workload": f"C5: {args.batch_scenes} independent C1 Hertz scenes (refine 0.7) sharded across "
-                               f"{world} GPU(s), packed per GPU with scene ids",
+                               f"{world} GPU(s) by sample-count prefix sums, packed per GPU with scene ids",
                    "samples_per_s": tot / (ms_b / 1e3), "ms_per_step": ms_b, "samples_total": int(tot),
                    "scenes_per_gpu": count, "samples_rank0": int(nb_s),
                    "scaling": "strong (fixed job, scenes sharded)",
                    "rebuild_seconds_rank0": t_brebuild,
                    "step": "energy + gradient + Gauss-Newton BCSR assembly over the packed batch, L2 flushed",
-                   "newton": newton_b}
-        del bctx
+                   "newton": newton_b, "job": job}
 
     peak, peak_src = peaks()
     achieved_k7 = ab["k7"] / (ms_k7 / 1e3) / 1e9
@@ -471,6 +587,19 @@ def main():
                                                    "iteration", "achieved": nb_ / (nms / 1e3) / 1e9, "peak": peak,
                            "unit": "GB/s", "frac": nb_ / (nms / 1e3) / 1e9 / peak, "algorithmic_bytes": nb_,
                            "ms": nms, "pcg_iters_mean": its}
+    e2e_solve = None
+    if rank == 0 and newton and not args.no_cpu_baseline:
+        ref = cpu_newton_reference()
+        if ref:
+            newton["cpu_baseline"] = {"value": ref["steps_per_s"], "unit": "Newton steps/s", "cores": 1,
+                                      "kind": ref["kind"], "sample": ref["sample"]}
+            c1 = newton["c1"]
+            e2e_solve = {"what": "C1 full load-stepped solve through the public API (host scene in, host x out): "
+                                 "device System::solve vs the reference System::solve on 1 host thread",
+                         "device_seconds": c1["solve_seconds"], "reference_seconds": ref["wall_seconds"],
+                         "speedup": ref["wall_seconds"] / c1["solve_seconds"],
+                         "device_newton_iters": c1["solve_newton_iters"], "reference_newton_iters": ref["newton_iters"],
+                         "device_peak": c1["peak"], "reference_peak": ref["peak"]}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -497,6 +626,8 @@ def main():
             "roofline_pass": {"achieved": achieved_pass, "peak": peak, "unit": "GB/s", "frac": achieved_pass / peak,
                               "algorithmic_bytes": ab["pass"], "ms": ms_pass},
             "roofline_newton": roofline_newton,
+            "e2e_dropin": e2e_dropin,
+            "e2e_solve": e2e_solve,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(2 * scene.rest.size * 8),
                     "d2h_bytes_per_step": int(scene.rest.size * 8 + 40),
                     "path": "gmcp.Context.add_gradient(x, grad, hessian=True) = one C-ABI call "

@@ -77,12 +77,28 @@ int gmcp_system_time_newton(gmcp_system* sys, const gmcp_solver_settings* settin
  * blocks). */
 int gmcp_system_pcg_stats(const gmcp_system* sys, double* ev_ms, int64_t* ev_iters, int64_t* n_rows,
                           int64_t* nnzb);
+/* Preconditioner of the single-system PCG after a solve: vertex-pair 6x6
+ * block-Jacobi on/off, two-level coarse space on/off, its aggregate count and
+ * padded coarse dimension (runtime switches GMCP_PAIR_JACOBI, GMCP_COARSE,
+ * GMCP_COARSE_AGGS; both default on). */
+int gmcp_system_precond_info(gmcp_system* sys, int32_t* pair_jacobi, int32_t* coarse, int32_t* n_aggregates,
+                             int32_t* n_coarse_padded);
 int gmcp_system_positions(gmcp_system* sys, double* x, int64_t n_dof);
 int gmcp_system_set_positions(gmcp_system* sys, const double* x, int64_t n_dof);
 int64_t gmcp_system_num_samples(gmcp_system* sys, int32_t pair);
 int gmcp_system_pair_force_summary(gmcp_system* sys, int32_t pair, double* out12);
 int gmcp_system_pair_pressure(gmcp_system* sys, int32_t pair, int64_t* n, gmcp_pressure_record* out);
 int64_t gmcp_system_launch_count(const gmcp_system* sys);
+/* Batched independent scenes (gmcp_system_set_vertex_scenes):
+ * the StepStats of every scene for every completed load step of the last
+ * solve, out[step * n_scenes + scene] (pass out = null to query n_steps);
+ * residual / energy / min_gap / backtracks / rebuilds / newton_iters are the
+ * scene's own (pcg_iters is 0: the per-scene CTA PCG runs all scenes at once). */
+int gmcp_system_scene_step_stats(gmcp_system* sys, int32_t* n_steps, gmcp_step_stats* out);
+/* Sample offsets of each scene inside a pair's packed sample set after the
+ * last batched solve ([n_scenes + 1]; the pressure records of scene s are the
+ * records whose sample index lies in [soff[s], soff[s+1])). */
+int gmcp_system_pair_scene_offsets(gmcp_system* sys, int32_t pair, int64_t* soff);
 /* Linear-solve parity (solver.hpp:349-356: the reference accepts a solve iff
  * ||M s - rhs||_inf <= 1e-6 ||rhs||_inf). After every PCG solve the residual
  * of the masked Newton system is RECOMPUTED (not PCG's recursive residual);

@@ -1056,6 +1056,7 @@ struct PairRt {
   gmcp_barrier_params params;
   DBuf<double> ref_pos;      // positions at sampling time
   DBuf<int32_t> motion_verts;  // slave.verts ++ master.verts
+  std::vector<int64_t> scene_soff;  // batched: sample offsets per scene after the last load step
 };
 
 struct SystemImpl {
@@ -1067,6 +1068,8 @@ struct SystemImpl {
   std::vector<int32_t> vscene;       // scene of each vertex (empty: one scene)
   std::vector<int64_t> scene_voff;   // [S+1] vertex offsets
   std::vector<int64_t> scene_iters;  // Newton iterations per scene (last solve)
+  std::vector<gmcp_step_stats> scene_stats;  // [load step][scene] StepStats of the last batched solve
+  int32_t scene_stats_steps = 0;              // load steps completed
   int64_t n_dof = 0;
   int64_t launches = 0;
   std::vector<Body> bodies;
@@ -2738,6 +2741,8 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
   };
   const int gn = grid_for(n, 256);
   S.scene_iters.assign(NS, 0);
+  S.scene_stats.assign((size_t)st.load_steps * NS, gmcp_step_stats{});
+  S.scene_stats_steps = 0;
   out->total_newton_iters = 0;
   out->total_rebuilds = 0;
   out->total_pcg_iters = 0;
@@ -2766,10 +2771,14 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
     assemble(S, lambda);
     scene_el();
     scene_contact(S.x.p, ce);
+    gmcp_step_stats* sst = S.scene_stats.data() + (size_t)(step - 1) * NS;  // this step, per scene
     for (int sc = 0; sc < NS; ++sc) {
       if (!feas[sc]) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
       energy[sc] = el[5 * sc + 3] + ce[sc] - lambda * el[5 * sc + 4];
       ss.min_gap = std::min(ss.min_gap, mg[sc]);
+      sst[sc].step = step;
+      sst[sc].min_gap = mg[sc];
+      sst[sc].energy_monotone = 1;
     }
     bool converged = false;
     for (int it = 0; it < st.max_newton_iters; ++it) {
@@ -2817,7 +2826,10 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
       }
       ss.pcg_iters += pit;
       ss.newton_iters += 1;
-      for (int sc = 0; sc < NS; ++sc) S.scene_iters[sc] += active[sc];
+      for (int sc = 0; sc < NS; ++sc) {
+        S.scene_iters[sc] += active[sc];
+        sst[sc].newton_iters += active[sc];
+      }
 
       const double ms_pcg = ms_since(t_pcg);
       const auto t_ls = tnow();
@@ -2852,8 +2864,10 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
             energy[sc] += dE;
             ce[sc] = ce_try[sc];
             ss.min_gap = std::min(ss.min_gap, mg[sc]);
+            sst[sc].min_gap = std::min(sst[sc].min_gap, mg[sc]);
           } else {
             ss.backtracks += 1;
+            sst[sc].backtracks += 1;
             alpha[sc] = 0.5 * a;
             all = false;
           }
@@ -2890,6 +2904,7 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
           flag[sc] = from_ord_bits(mu[sc]) > 0.5 * pr.params.eps_max;
           nflag += flag[sc];
         }
+        for (int sc = 0; sc < NS; ++sc) sst[sc].rebuilds += flag[sc];
         if (nflag) {
           rebuild_scenes(p, flag);
           rebuild = true;
@@ -2941,6 +2956,12 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
     }
     ss.residual = r_max;
     ss.energy = e_tot;
+    for (int sc = 0; sc < NS; ++sc) {
+      sst[sc].residual = resid[sc];
+      sst[sc].energy = el[5 * sc + 3] + ce[sc] - lambda * el[5 * sc + 4];
+    }
+    S.scene_stats_steps = step;
+    for (int p = 0; p < np; ++p) S.pairs[p]->scene_soff = soff_h[p];
     out->total_rebuilds += ss.rebuilds;
     out->total_pcg_iters += ss.pcg_iters;
     S.x.download(S.x_host.data(), n, s);
@@ -3479,6 +3500,39 @@ int gmcp_system_captured_linear_system(gmcp_system* sys, int64_t* nnzb, int32_t*
     if (grad) std::copy(S.cap_grad.begin(), S.cap_grad.end(), grad);
     if (dx) std::copy(S.cap_dx.begin(), S.cap_dx.end(), dx);
     if (shift) *shift = S.cap_shift;
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_precond_info(gmcp_system* sys, int32_t* pair_jacobi, int32_t* coarse, int32_t* n_aggregates,
+                             int32_t* n_coarse_padded) {
+  return sguard(sys, [&] {
+    const SystemImpl& S = sys->s;
+    *pair_jacobi = S.has_pairs ? 1 : 0;
+    *coarse = S.cs.enabled ? 1 : 0;
+    *n_aggregates = S.cs.enabled ? S.cs.n_agg : 0;
+    *n_coarse_padded = S.cs.enabled ? S.cs.n_pad : 0;
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_scene_step_stats(gmcp_system* sys, int32_t* n_steps, gmcp_step_stats* out) {
+  return sguard(sys, [&] {
+    const SystemImpl& S = sys->s;
+    *n_steps = S.scene_stats_steps;
+    if (out)
+      std::copy(S.scene_stats.begin(), S.scene_stats.begin() + (size_t)S.scene_stats_steps * S.n_scenes, out);
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_pair_scene_offsets(gmcp_system* sys, int32_t pair, int64_t* soff) {
+  return sguard(sys, [&] {
+    const SystemImpl& S = sys->s;
+    if (pair < 0 || pair >= (int)S.pairs.size()) throw StatusError(GMCP_ERR_ARG, "no such pair");
+    const auto& v = S.pairs[pair]->scene_soff;
+    if (v.size() != (size_t)S.n_scenes + 1) throw StatusError(GMCP_ERR_ARG, "no batched solve has completed");
+    std::copy(v.begin(), v.end(), soff);
     return GMCP_OK;
   });
 }

@@ -276,12 +276,18 @@ class Context:
         self.n_dof = x.size
         return e.value
 
-    def download_hessian(self):
+    def download_hessian(self, out=None):
+        """The assembled Gauss-Newton Hessian as BCSR (rowptr, cols, vals[nnzb,3,3]).
+        out: optional caller arrays (e.g. pinned host memory) of sufficient size."""
         nnzb = C.c_int64()
         _check(self.L.gmcp_download_hessian(self.h, C.byref(nnzb), None, None, None))
-        rowptr = np.zeros(self.n_dof // 3 + 1, np.int32)
-        cols = np.zeros(max(nnzb.value, 1), np.int32)
-        vals = np.zeros((max(nnzb.value, 1), 3, 3))
+        if out is not None:
+            rowptr, cols, vals = out
+            assert rowptr.size >= self.n_dof // 3 + 1 and cols.size >= nnzb.value and vals.shape[0] >= nnzb.value
+        else:
+            rowptr = np.zeros(self.n_dof // 3 + 1, np.int32)
+            cols = np.zeros(max(nnzb.value, 1), np.int32)
+            vals = np.zeros((max(nnzb.value, 1), 3, 3))
         _check(self.L.gmcp_download_hessian(self.h, C.byref(nnzb), _p(rowptr), _p(cols), _p(vals)))
         return rowptr, cols[:nnzb.value], vals[:nnzb.value]
 

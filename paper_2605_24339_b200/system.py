@@ -41,6 +41,13 @@ class _StepStats(C.Structure):
                 ("energy", C.c_double), ("min_gap", C.c_double), ("energy_monotone", C.c_int32)]
 
 
+# gmcp_step_stats as a numpy record (include/gmcp_solver.h; natural C alignment)
+SCENE_STEP_DTYPE = np.dtype([("step", np.int32), ("newton_iters", np.int32), ("rebuilds", np.int32),
+                             ("backtracks", np.int32), ("pcg_iters", np.int64), ("residual", np.float64),
+                             ("energy", np.float64), ("min_gap", np.float64), ("energy_monotone", np.int32),
+                             ("_pad", np.int32)])
+
+
 class _RunStats(C.Structure):
     _fields_ = [("total_newton_iters", C.c_int64), ("total_rebuilds", C.c_int64), ("total_pcg_iters", C.c_int64),
                 ("newton_tol_used", C.c_double), ("wall_seconds", C.c_double), ("residual", C.c_double)]
@@ -169,6 +176,25 @@ class System:
             self.L.gmcp_system_scene_newton_iters(self.h, _g._p(out))
         return out
 
+    def scene_step_stats(self) -> np.ndarray:
+        """Per-scene StepStats of the last batched solve: (load_steps, n_scenes)
+        structured array (step, newton_iters, rebuilds, backtracks, pcg_iters,
+        residual, energy, min_gap, energy_monotone)."""
+        n_steps = C.c_int32()
+        _check(self.L, self.L.gmcp_system_scene_step_stats(self.h, C.byref(n_steps), None))
+        ns = 0 if self._scenes is None else int(self._scenes.max()) + 1
+        out = np.zeros((n_steps.value, ns), dtype=SCENE_STEP_DTYPE)
+        if out.size:
+            _check(self.L, self.L.gmcp_system_scene_step_stats(self.h, C.byref(n_steps), _g._p(out)))
+        return out
+
+    def pair_scene_offsets(self, pair: int = 0) -> np.ndarray:
+        """Sample offsets of each scene in a pair's packed sample set (after a batched solve)."""
+        ns = 0 if self._scenes is None else int(self._scenes.max()) + 1
+        out = np.zeros(ns + 1, np.int64)
+        _check(self.L, self.L.gmcp_system_pair_scene_offsets(self.h, C.c_int32(pair), _g._p(out)))
+        return out
+
     def fix_dof(self, gv: int, axis: int, target: float):
         self.fixed[3 * gv + axis] = 1
         self.dirichlet[3 * gv + axis] = target
@@ -268,6 +294,11 @@ class System:
         it, rows, nnzb = C.c_int64(), C.c_int64(), C.c_int64()
         _check(self.L, self.L.gmcp_system_pcg_stats(self.h, C.byref(ms), C.byref(it), C.byref(rows), C.byref(nnzb)))
         return {"ms": ms.value, "iters": it.value, "rows": rows.value, "nnzb": nnzb.value}
+
+    def precond_info(self) -> dict:
+        a, b, c, d = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        _check(self.L, self.L.gmcp_system_precond_info(self.h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        return {"pair_jacobi": bool(a.value), "coarse": bool(b.value), "aggregates": c.value, "coarse_padded": d.value}
 
     def linear_stats(self, reset: bool = False) -> dict:
         """Recomputed true residuals of the linear solves since the last reset:
