@@ -141,6 +141,7 @@ constexpr int kStagWindow = 1024;
 constexpr int kStagWindowCoarse = 256;
 constexpr double kAcceptRelInf = 1e-6;  // solver.hpp:349-356 acceptance of a linear solve
 constexpr double kCoarseDrop = 1e-10;   // scaled coarse pivots below this drop their rigid mode
+constexpr double kSceneCoarseDrop = 1e-8;  // per-scene inverses: ill-conditioned rigid modes drop earlier
 constexpr double kCoarseStale = 1.25;   // refresh the coarse inverse when a solve needs 25% more iterations
 
 // A_vj x for block k, read through the read-only path (either layout)
@@ -1088,6 +1089,7 @@ struct SystemImpl {
   int coop_blocks = 0;       // co-resident CTAs of the fused cooperative kernel (0: not queried)
   int64_t load_step = 0;     // current load step (coarse refresh policy)
   bool coarse_refresh_always = false;  // GMCP_COARSE_REFRESH=1: new coarse inverse every solve
+  int coarse_scene_aggs = 24;          // batched scenes: aggregates per scene (GMCP_COARSE_SCENE_AGGS)
   bool use_coop = false;     // GMCP_COOP=1: update + coarse as one cooperative kernel (measured slower)
   int64_t u_gen = 0;         // union pattern generation (coarse pair lists follow it)
   DBuf<unsigned int> counter;
@@ -1116,6 +1118,7 @@ struct SystemImpl {
   // ||H dx - rhs||_2 / ||rhs||_2 and the inf-norm ratio the reference's acceptance test uses
   double last_true_rel2 = 0, last_true_relinf = 0, true_rel2_max = 0, true_relinf_max = 0;
   int64_t n_linear_solves = 0, refinements = 0;
+  int64_t coarse_fallbacks = 0;  // batched: scene solves re-run with block-Jacobi after a failed two-level solve
   DBuf<double> rt, xacc;  // true residual vector, accumulated solution (residual replacement)
   // optional host capture of the last linear system (gmcp_system_capture_linear_system)
   bool capture = false;
@@ -1479,18 +1482,27 @@ double assemble(SystemImpl& S, double lambda) {
 void build_coarse(SystemImpl& S, const std::vector<double>& mask) {
   CoarseSpace& C = S.cs;
   C.enabled = false;
-  if (!S.use_coarse || S.n_scenes > 1) return;
+  const bool scenes = S.n_scenes > 1;
+  if (!S.use_coarse) return;
   const int nv = S.nv();
   std::vector<int32_t> agg(nv, -1);
   int n_agg = 0;
+  // batched scenes: a per-scene coarse space of ~coarse_scene_aggs aggregates
+  // (each body lies in one scene; bodies come in scene order)
+  std::vector<int64_t> scene_nv(std::max(S.n_scenes, 1), 0);
+  if (scenes)
+    for (const Body& b : S.bodies) scene_nv[S.vscene[b.offset]] += b.nv;
+  std::vector<int32_t> body_first_agg;
   for (const Body& b : S.bodies) {
+    body_first_agg.push_back(n_agg);
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (int v = 0; v < b.nv; ++v)
       for (int k = 0; k < 3; ++k) {
         lo[k] = std::min(lo[k], b.verts[3 * v + k]);
         hi[k] = std::max(hi[k], b.verts[3 * v + k]);
       }
-    const double kb = std::max(1.0, (double)S.coarse_aggs * b.nv / std::max(1, nv));
+    const double kb = scenes ? std::max(1.0, (double)S.coarse_scene_aggs * b.nv / std::max<int64_t>(1, scene_nv[S.vscene[b.offset]]))
+                             : std::max(1.0, (double)S.coarse_aggs * b.nv / std::max(1, nv));
     double L[3];
     for (int k = 0; k < 3; ++k) L[k] = std::max(hi[k] - lo[k], 1e-12 * std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-300}));
     // cell size h with prod max(1, round(L/h)) ~ kb (bisection on log h)
@@ -1563,13 +1575,45 @@ void build_coarse(SystemImpl& S, const std::vector<double>& mask) {
   }
   C.n_agg = n_agg;
   C.n_pad = ((6 * n_agg + kGJ - 1) / kGJ) * kGJ;
-  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
-  if (trace) std::fprintf(stderr, "[gmcp] coarse space: %d aggregates, %d coarse dofs (padded)\n", n_agg, C.n_pad);
   C.agg.upload(agg, S.stream);
   C.dvec.upload(dvec, S.stream);
   C.agg_off.upload(off, S.stream);
   C.agg_verts.upload(verts, S.stream);
   C.gram.upload(gram, S.stream);
+  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+  if (scenes) {  // per-scene dense blocks: scene s owns aggregates [sa[s], sa[s+1]), its
+                 // (6 n_s)^2 coarse matrix at c_off[s]
+    const int NS = S.n_scenes;
+    std::vector<int32_t> sa(NS + 1, 0), agg_scene(n_agg);
+    for (size_t bi = 0; bi < S.bodies.size(); ++bi) {
+      const int sc = S.vscene[S.bodies[bi].offset];
+      const int a1 = bi + 1 < S.bodies.size() ? body_first_agg[bi + 1] : n_agg;
+      for (int a = body_first_agg[bi]; a < a1; ++a) agg_scene[a] = sc;
+      sa[sc + 1] = a1;
+    }
+    for (int sc = 0; sc < NS; ++sc) sa[sc + 1] = std::max(sa[sc + 1], sa[sc]);
+    std::vector<int64_t> coff(NS + 1, 0);
+    int max_c = 0;
+    for (int sc = 0; sc < NS; ++sc) {
+      const int64_t d = 6 * (int64_t)(sa[sc + 1] - sa[sc]);
+      coff[sc + 1] = coff[sc] + d * d;
+      max_c = std::max(max_c, (int)d);
+    }
+    if (max_c > kSceneCoarseMax) return;  // too large for the per-scene CTA kernel: no coarse space
+    C.scene_agg.upload(sa, S.stream);
+    C.agg_scene.upload(agg_scene, S.stream);
+    C.scene_coff.upload(coff, S.stream);
+    C.A.resize(std::max<int64_t>(coff[NS], 1));
+    C.scale.resize(6 * (size_t)n_agg);
+    C.n_scene_c = max_c;
+    C.pat_gen = -2;
+    C.enabled = true;
+    if (trace)
+      std::fprintf(stderr, "[gmcp] per-scene coarse spaces: %d aggregates over %d scenes (max %d coarse dofs/scene)\n",
+                   n_agg, NS, max_c);
+    return;
+  }
+  if (trace) std::fprintf(stderr, "[gmcp] coarse space: %d aggregates, %d coarse dofs (padded)\n", n_agg, C.n_pad);
   const size_t n2 = (size_t)C.n_pad * C.n_pad;
   C.A.resize(n2);
   C.B.resize(n2);
@@ -1595,7 +1639,8 @@ void coarse_setup(SystemImpl& S, const MatSet& M) {
                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), S.cs.n_pairs,
                S.cs.n_pad);
 }
-void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
+// aggregate-pair block lists of the operand's pattern (rebuilt when it changed)
+void coarse_pair_lists(SystemImpl& S, const MatSet& M) {
   CoarseSpace& C = S.cs;
   const int nv = S.nv();
   const Bcsr& A = M.el;
@@ -1640,6 +1685,12 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
     C.pat_nnzb = nnzb;
     C.pat_gen = gen;
   }
+}
+
+void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
+  CoarseSpace& C = S.cs;
+  const Bcsr& A = M.el;
+  coarse_pair_lists(S, M);
   const int n_pad = C.n_pad;
   GMCP_CUDA(cudaMemsetAsync(C.A.p, 0, (size_t)n_pad * n_pad * sizeof(double), S.stream));
   if (C.n_pairs > 0)
@@ -1663,6 +1714,22 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
     std::swap(X, Y);
   }
   C.inv = X;
+}
+
+// Batched scenes: every scene's coarse operator (its own shift) and its
+// scaled pseudo-inverse, per batched PCG call.
+void coarse_setup_scenes(SystemImpl& S, const MatSet& M, const double* shift_dev) {
+  CoarseSpace& C = S.cs;
+  const Bcsr& A = M.el;
+  coarse_pair_lists(S, M);
+  const int NS = S.n_scenes;
+  GMCP_CUDA(cudaMemsetAsync(C.A.p, 0, C.A.n * sizeof(double), S.stream));
+  if (C.n_pairs > 0)
+    k_coarse_assemble<<<C.n_pairs, 256, 0, S.stream>>>(
+        C.n_pairs, C.n_agg, 0, C.ukey.p, C.poff.p, C.pcnt.p, C.blk2.p, C.u_row.p, A.cols, A.vals, A.bs, A.cs,
+        S.mask_d.p, C.dvec.p, C.gram.p, 0.0, C.A.p, C.agg_scene.p, C.scene_agg.p, C.scene_coff.p, shift_dev);
+  k_scene_coarse_inv<<<NS, 256, 0, S.stream>>>(C.scene_agg.p, C.scene_coff.p, C.A.p, C.scale.p, kSceneCoarseDrop);
+  S.launches += 2;
 }
 
 // ||H dx - rhs|| of the solve just finished (recomputed, not the recursive
@@ -2336,6 +2403,7 @@ __global__ void __launch_bounds__(kSceneBlk) k_seg_diag(int nv, MatSet M, const 
 }  // namespace
 
 struct SegPcgTmp {
+  DBuf<unsigned long long> tr;  // per-scene true-residual maxima (k_scene_true_resid)
   DBuf<double> dv, st, shift;
   DBuf<int32_t> act, vscene;
   DBuf<int64_t> voff;
@@ -2371,17 +2439,92 @@ __device__ __forceinline__ void cta_sum2(double& a, double& b, double (*sh)[kCta
   b = s1;
 }
 
+// Per-scene two-level correction inside the CTA PCG (coarse.cuh): the scene's
+// own rigid-mode coarse space and dense pseudo-inverse.
+struct SceneCoarse {
+  const int32_t* agg;        // [nv] global aggregate id
+  const double* dvec;        // [nv][3]
+  const int32_t* agg_off;    // aggregate vertex lists (ascending ids)
+  const int32_t* agg_verts;
+  const int32_t* scene_agg;  // [NS+1] aggregate range of each scene
+  const int64_t* scene_coff; // [NS+1] offset of each scene's inverse
+  const double* inv;         // scaled pseudo-inverses
+  const double* scale;       // [6 n_agg]
+};
+
+// z += P Ac^+ P^T r over the CTA's scene (r, z written earlier in this
+// kernel: plain loads); returns s.y, identical in every thread. Restriction:
+// warp w sums aggregates w, w + 4, ... (lanes over the vertex list, fixed
+// butterfly); coarse rows: one warp per row; prolongation: the thread's own
+// vertices (the update loop's assignment).
+__device__ double scene_coarse(int sc, int v0, int v1, const double* r, double* z, const double* __restrict__ mask,
+                               const SceneCoarse& C, double* s_sm, double* y_sm,
+                               double (*sh)[kCtaThreads / 32]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int a0 = C.scene_agg[sc], na = C.scene_agg[sc + 1] - a0, dim = 6 * na;
+  const double* Ai = C.inv + C.scene_coff[sc];
+  const double* scl = C.scale + 6 * (int64_t)a0;
+  for (int la = wid; la < na; la += kCtaThreads / 32) {
+    const int a = a0 + la;
+    double t[6] = {0, 0, 0, 0, 0, 0};
+    for (int e = __ldg(C.agg_off + a) + lane; e < __ldg(C.agg_off + a + 1); e += 32) {
+      const int v = __ldg(C.agg_verts + e);
+      const d3 m = ld3(mask, v), rv = ld3nc(r, v);
+      const d3 q = mk3(m.x * rv.x, m.y * rv.y, m.z * rv.z);
+      const d3 w = cross(ld3(C.dvec, v), q);
+      t[0] += q.x;
+      t[1] += q.y;
+      t[2] += q.z;
+      t[3] += w.x;
+      t[4] += w.y;
+      t[5] += w.z;
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) t[k] = warp_sum(t[k]);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s_sm[6 * la + k] = t[k] * __ldg(scl + 6 * la + k);
+  }
+  __syncthreads();
+  double sy = 0;
+  for (int i = wid; i < dim; i += kCtaThreads / 32) {
+    const double* row = Ai + (int64_t)i * dim;
+    double acc = 0;
+    for (int j = lane; j < dim; j += 32) acc += __ldg(row + j) * s_sm[j];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      y_sm[i] = __ldg(scl + i) * acc;
+      sy += s_sm[i] * acc;
+    }
+  }
+  __syncthreads();
+  for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
+    const int la = __ldg(C.agg + v) - a0;
+    const double* ya = y_sm + 6 * la;
+    const d3 u = mk3(ya[0], ya[1], ya[2]) + cross(mk3(ya[3], ya[4], ya[5]), ld3(C.dvec, v));
+    const d3 m = ld3(mask, v);
+    z[3 * v] += m.x * u.x;
+    z[3 * v + 1] += m.y * u.y;
+    z[3 * v + 2] += m.z * u.z;
+  }
+  double unused = 0;
+  cta_sum2(sy, unused, sh);  // lane-0 partials of each warp, summed in warp order
+  return sy;
+}
+
 // st[8 s + 0] rz, [1] pq, [2] alpha, [3] beta, [4] rr, [5] bb, [6] iterations
+template <bool kCoarse>
 __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const double* __restrict__ mask,
                                                           const int64_t* __restrict__ voff,
                                                           const int32_t* __restrict__ act,
                                                           const double* __restrict__ shift_s,
                                                           const double* __restrict__ minv,
                                                           const double* __restrict__ grad, double* __restrict__ x,
-                                                          double* __restrict__ r, double* __restrict__ z,
-                                                          double* __restrict__ p, double* __restrict__ q,
-                                                          double tol2, int maxit, double* __restrict__ st) {
+                                                          double* r, double* z, double* __restrict__ p,
+                                                          double* __restrict__ q, double tol2, int maxit,
+                                                          double* __restrict__ st, SceneCoarse CS) {
   __shared__ double sh[2][kCtaThreads / 32];
+  __shared__ double s_sm[kCoarse ? kSceneCoarseMax : 1], y_sm[kCoarse ? kSceneCoarseMax : 1];
   const int sc = blockIdx.x;
   if (!act[sc]) return;  // scenes not being solved keep their x (dx)
   const int v0 = (int)voff[sc], v1 = (int)voff[sc + 1];
@@ -2397,18 +2540,25 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
       x[3 * v + k] = 0;
       r[3 * v + k] = ra[k];
       z[3 * v + k] = za[k];
-      p[3 * v + k] = za[k];
+      if (!kCoarse) p[3 * v + k] = za[k];
     }
     rz += dot(rv, zv);
     rr += dot(rv, rv);
   }
   cta_sum2(rz, rr, sh);
+  bool indefinite = false;  // two-level M^-1 lost positivity (r.z <= 0 with r != 0)
+  if (kCoarse) {  // z += P Ac^+ P^T r, then p = z (own rows)
+    rz += scene_coarse(sc, v0, v1, r, z, mask, CS, s_sm, y_sm, sh);
+    indefinite = !(rz > 0) && rr > 0;
+    for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads)
+      for (int k = 0; k < 3; ++k) p[3 * v + k] = z[3 * v + k];
+  }
   const double bb = rr;
   int it = 0;
   double pq = 0, alpha = 0, beta = 0;
   double win_min = INFINITY, prev_min = INFINITY;  // stagnation windows (kStagWindow)
   const int lane = threadIdx.x & 31, sub = lane & 7;
-  while (rr > tol2 * bb && it < maxit) {
+  while (rr > tol2 * bb && it < maxit && !indefinite) {
     __syncthreads();  // p complete
     // q = mask .* ((H + shift I) p); pq
     double pqa = 0, unused = 0;
@@ -2423,7 +2573,7 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
         acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
       }
       if (sub == 0 && v < v1) {
-        const d3 m = ld3(mask, v), pv = ld3(p, v);
+        const d3 m = ld3(mask, v), pv = ld3nc(p, v);
         if (shift != 0) acc = acc + shift * pv;
         const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
         q[3 * v] = y.x;
@@ -2438,8 +2588,8 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
     // x += alpha p, r -= alpha q, z = Minv r; (r.z, r.r)
     double rzn = 0, rrn = 0;
     for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
-      const d3 xv = ld3(x, v) + alpha * ld3(p, v);
-      const d3 rv = ld3(r, v) - alpha * ld3(q, v);
+      const d3 xv = ld3nc(x, v) + alpha * ld3nc(p, v);
+      const d3 rv = ld3nc(r, v) - alpha * ld3nc(q, v);
       const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
       const double xa[3] = {xv.x, xv.y, xv.z}, ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
 #pragma unroll
@@ -2452,20 +2602,29 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
       rrn += dot(rv, rv);
     }
     cta_sum2(rzn, rrn, sh);
+    if (kCoarse) {
+      rzn += scene_coarse(sc, v0, v1, r, z, mask, CS, s_sm, y_sm, sh);
+      if (!(rzn > 0) && rrn > 0) {
+        indefinite = true;
+        rr = rrn;
+        break;
+      }
+    }
     beta = rz != 0 ? rzn / rz : 0.0;
     rz = rzn;
     rr = rrn;
     ++it;
     if (!isfinite(rr)) break;
     win_min = fmin(win_min, rr);
-    if (it % kStagWindow == 0) {
-      if (it >= 2 * kStagWindow && !(win_min < 0.5 * prev_min) && rr > 1e-8 * bb) break;  // stagnated
+    constexpr int stag = kCoarse ? kStagWindowCoarse : kStagWindow;
+    if (it % stag == 0) {
+      if (it >= 2 * stag && !(win_min < 0.5 * prev_min) && rr > 1e-8 * bb) break;  // stagnated
       prev_min = fmin(prev_min, win_min);
       win_min = INFINITY;
     }
     // p = z + beta p (own rows; the barrier at the loop head publishes it)
     for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
-      const d3 pv = ld3(z, v) + beta * ld3(p, v);
+      const d3 pv = ld3nc(z, v) + beta * ld3nc(p, v);
       p[3 * v] = pv.x;
       p[3 * v + 1] = pv.y;
       p[3 * v + 2] = pv.z;
@@ -2480,13 +2639,64 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
     o[4] = rr;
     o[5] = bb;
     o[6] = (double)it;
+    o[7] = indefinite ? 1.0 : 0.0;
+  }
+}
+
+// Per scene (one CTA): max |mask .* ((H + shift I) dx) + mask .* grad| and
+// max |mask .* grad| (the reference's inf-norm acceptance test,
+// solver.hpp:349-356), as ordered bits (max is order-free).
+__global__ void __launch_bounds__(kSceneBlk) k_scene_true_resid(MatSet M, const double* __restrict__ mask,
+                                                                const int64_t* __restrict__ voff,
+                                                                const int32_t* __restrict__ act,
+                                                                const double* __restrict__ shift_s,
+                                                                const double* __restrict__ dx,
+                                                                const double* __restrict__ grad,
+                                                                unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long sm[2][kSceneBlk / 32];
+  const int sc = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long mr = 0, mb = 0;
+  if (act[sc]) {
+    for (int64_t v = voff[sc] + wid; v < voff[sc + 1]; v += kSceneBlk / 32) {
+      d3 acc = mk3(0, 0, 0);
+      for (int k = M.el.rowptr[v] + lane; k < M.el.rowptr[v + 1]; k += 32)
+        acc = acc + bmv_ro(M.el, k, ld3(dx, M.el.cols[k]));
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+      acc.z = warp_sum(acc.z);
+      if (lane == 0) {
+        const d3 m = ld3(mask, (int)v), g = ld3(grad, (int)v), d = ld3(dx, (int)v);
+        const double sh = shift_s[sc];
+        const double y[3] = {acc.x + sh * d.x, acc.y + sh * d.y, acc.z + sh * d.z};
+        const double ma[3] = {m.x, m.y, m.z}, ga[3] = {g.x, g.y, g.z};
+        for (int a = 0; a < 3; ++a) {
+          const unsigned long long br = ord_bits(fabs(ma[a] * y[a] + ma[a] * ga[a])), bb = ord_bits(fabs(ma[a] * ga[a]));
+          mr = br > mr ? br : mr;
+          mb = bb > mb ? bb : mb;
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    sm[0][wid] = mr;
+    sm[1][wid] = mb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kSceneBlk / 32; ++w) {
+      mr = max(mr, sm[0][w]);
+      mb = max(mb, sm[1][w]);
+    }
+    out[2 * sc] = max(mr, sm[0][0]);
+    out[2 * sc + 1] = max(mb, sm[1][0]);
   }
 }
 
 // Runs the segmented PCG for the scenes with active[s]; returns iterations of
 // the slowest scene; rel[s] = sqrt(rr_s / bb_s) at exit (0 when bb_s = 0).
 int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::vector<int32_t>& active,
-                const std::vector<double>& shift, std::vector<double>& rel) {
+                const std::vector<double>& shift, std::vector<double>& rel, bool allow_coarse = false,
+                std::vector<int32_t>* bad = nullptr) {
   const int nv = S.nv(), NS = S.n_scenes;
   cudaStream_t s = S.stream;
   MatSet M = mats(S);
@@ -2500,11 +2710,39 @@ int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::v
   int64_t max_rows = 0;
   for (int sc = 0; sc < NS; ++sc) max_rows = std::max(max_rows, S.scene_voff[sc + 1] - S.scene_voff[sc]);
   if (max_rows <= kCtaSceneRows && !std::getenv("GMCP_SEG_PCG")) {  // one CTA per scene
-    k_pcg_scene<<<NS, kCtaThreads, 0, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.minv.p, S.grad.p, S.dx.p,
-                                           S.r.p, S.z.p, S.p.p, S.q.p, tol * tol, maxit, T.st.p);
+    CoarseSpace& C = S.cs;
+    const bool coarse = allow_coarse && C.enabled && M.np == 0;
+    SceneCoarse CS{};
+    if (coarse) {
+      coarse_setup_scenes(S, M, T.shift.p);
+      CS = SceneCoarse{C.agg.p, C.dvec.p, C.agg_off.p, C.agg_verts.p, C.scene_agg.p, C.scene_coff.p, C.A.p,
+                       C.scale.p};
+      k_pcg_scene<true><<<NS, kCtaThreads, 0, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.minv.p, S.grad.p,
+                                                   S.dx.p, S.r.p, S.z.p, S.p.p, S.q.p, tol * tol, maxit, T.st.p, CS);
+    } else {
+      k_pcg_scene<false><<<NS, kCtaThreads, 0, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.minv.p,
+                                                    S.grad.p, S.dx.p, S.r.p, S.z.p, S.p.p, S.q.p, tol * tol, maxit,
+                                                    T.st.p, CS);
+    }
     ++S.launches;
     std::vector<double> st = T.st.to_host(s);
     rel.resize(NS, 0.0);
+    if (bad) bad->assign(NS, 0);
+    if (coarse && bad) {  // two-level solves: reference acceptance on the recomputed residual
+      T.tr.resize(2 * NS);
+      k_scene_true_resid<<<NS, kSceneBlk, 0, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.dx.p, S.grad.p,
+                                                   T.tr.p);
+      ++S.launches;
+      std::vector<unsigned long long> tr = T.tr.to_host(s);
+      for (int sc = 0; sc < NS; ++sc) {
+        if (!active[sc]) continue;
+        const double rmax = from_ord_bits(tr[2 * sc]), bmax = from_ord_bits(tr[2 * sc + 1]);
+        // indefinite, or converged on the recursive residual but not on the true one
+        // (scenes that simply did not converge go to the regularized retry)
+        const bool conv = st[8 * sc + 5] > 0 ? st[8 * sc + 4] <= tol * tol * st[8 * sc + 5] : true;
+        (*bad)[sc] = st[8 * sc + 7] != 0 || (conv && !(rmax <= kAcceptRelInf * bmax)) ? 1 : 0;
+      }
+    }
     int it_max = 0;
     for (int sc = 0; sc < NS; ++sc) {
       if (!active[sc]) continue;
@@ -2801,7 +3039,14 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
       const double ms_asm = ms_since(t_it);
       S.dx.zero(s);
       std::vector<double> rel, shift(NS, 0.0);
-      int pit = pcg_batched(S, segT, st.pcg_tol, st.pcg_max_iters, active, shift, rel);
+      // two-level PCG first; a scene whose solve did not converge, lost
+      // positivity, or fails the reference's acceptance test on the recomputed
+      // residual (solver.hpp:349-356) retries regularized (solver.hpp:352-361):
+      // two-level, then block-Jacobi alone
+      std::vector<int32_t> bad;
+      int pit = pcg_batched(S, segT, st.pcg_tol, st.pcg_max_iters, active, shift, rel, true, &bad);
+      for (int sc = 0; sc < NS; ++sc)
+        if (active[sc] && bad[sc]) rel[sc] = INFINITY;  // -> regularized retry
       std::vector<int32_t> retry(NS, 0);
       bool any_retry = false;
       for (int sc = 0; sc < NS; ++sc)
@@ -2817,7 +3062,22 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
         std::vector<double> dsum = dsum_d.to_host(s);
         for (int sc = 0; sc < NS; ++sc)
           if (retry[sc]) shift[sc] = kRegularization * dsum[sc] / (double)std::max<int64_t>(n_free_s[sc], 1);
-        pit += pcg_batched(S, segT, st.pcg_tol, st.pcg_max_iters, retry, shift, rel);
+        std::vector<int32_t> bad2;
+        pit += pcg_batched(S, segT, st.pcg_tol, st.pcg_max_iters, retry, shift, rel, true, &bad2);
+        std::vector<int32_t> retry2(NS, 0);
+        bool any2 = false;
+        for (int sc = 0; sc < NS; ++sc)
+          if (retry[sc] && (bad2[sc] || !(rel[sc] <= st.pcg_tol))) {
+            retry2[sc] = 1;
+            any2 = true;
+          }
+        if (any2) {
+          std::vector<double> rel3;
+          pit += pcg_batched(S, segT, st.pcg_tol, st.pcg_max_iters, retry2, shift, rel3, false);
+          for (int sc = 0; sc < NS; ++sc)
+            if (retry2[sc]) rel[sc] = rel3[sc];
+          S.coarse_fallbacks += std::count(retry2.begin(), retry2.end(), 1);
+        }
         for (int sc = 0; sc < NS; ++sc)
           if (retry[sc] && !(rel[sc] <= st.pcg_tol))
             throw StatusError(GMCP_ERR_SOLVER, "scene " + std::to_string(sc) +
@@ -3217,6 +3477,8 @@ int gmcp_system_create(int device, gmcp_system** out) {
     if (const char* e = std::getenv("GMCP_COARSE_AGGS")) s->s.coarse_aggs = std::min(512, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("GMCP_COOP")) s->s.use_coop = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE_REFRESH")) s->s.coarse_refresh_always = std::atoi(e) != 0;
+    if (const char* e = std::getenv("GMCP_COARSE_SCENE_AGGS"))
+      s->s.coarse_scene_aggs = std::min(32, std::max(1, std::atoi(e)));
     *out = s;
     return GMCP_OK;
   } catch (const StatusError& e) {
