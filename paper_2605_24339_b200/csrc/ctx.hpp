@@ -56,6 +56,7 @@ struct Ctx {
   int device = 0;
   CubScratch cub;        // CUB temp storage (bound per C-ABI call)
   int k7_resident = 0;   // K7 persistent grid size on this context's device
+  bool thread_query = std::getenv("GMCP_THREAD_QUERY") != nullptr;  // broadphase: per-thread traversal
   std::unique_ptr<TmpBase> rebuild_tmp;  // broadphase + sampler scratch (sampler.cu)
   std::unique_ptr<TmpBase> embed_tmp;    // dual-mesh embedding scratch (sampler.cu)
   std::unique_ptr<TmpBase> scene_tmp;    // scene-segmented reductions scratch (exact.cu)

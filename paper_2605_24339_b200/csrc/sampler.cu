@@ -5,12 +5,15 @@
 //
 //  K1 lbvh_build   Morton codes of master-triangle AABB centroids, CUB radix
 //                  sort, Karras (2012) hierarchy, bottom-up AABB refit.
-//  K2 lbvh_query   one thread per slave triangle, stack traversal with the
-//                  inflated query box; count pass -> scan -> emit pass, then a
-//                  per-triangle sort (the reference sorts, so traversal order
-//                  is irrelevant).                  contact_sampling.hpp:296-326
-//  K3 features     per slave triangle sorted-unique candidate edges / vertex
-//                  features.                        contact_sampling.hpp:328-337
+//  K2 lbvh_query   one WARP per slave triangle: breadth-first traversal with
+//                  the inflated query box, lanes test one frontier node each,
+//                  ballot compaction of hits / children in shared memory;
+//                  count pass -> scan -> emit pass with a warp bitonic sort
+//                  (the reference sorts, so traversal order is irrelevant).
+//                  Per-thread stack traversal as the capacity fallback.
+//                                                    contact_sampling.hpp:296-326
+//  K3 features     per slave triangle (one warp) sorted-unique candidate edges /
+//                  vertex features.                 contact_sampling.hpp:328-337
 //  K4 point_owner  master vertex -> owning slave triangles (interior: all,
 //                  else the first boundary one).     contact_sampling.hpp:403-436
 //  K5 sample       one thread per (slave tri, feature) task in reference
@@ -279,6 +282,190 @@ __global__ void k_query(int32_t nst, const int32_t* __restrict__ stris, const do
     }
     if (Mode) isort(out + base, (int)c);
     else cnt[st] = c;
+  }
+}
+
+// K2 (default): warp-cooperative traversal, one warp per slave triangle.
+// The warp walks the LBVH breadth-first: each lane tests one node of the
+// current frontier (scene range + Aabb::overlaps against the inflated query
+// box), and ballot / popcount compaction appends the leaves hit to the warp's
+// hit list and the children of the internal nodes hit to the next frontier,
+// all in shared memory. The hits are then sorted by a warp bitonic sort
+// (the reference sorts, contact_sampling.hpp:296-326, so the traversal order
+// is irrelevant). A frontier or hit list beyond the warp's capacity raises
+// *wovf and the host re-runs the per-thread kernels (k_query).
+constexpr int kQW = 4;          // warps per block
+constexpr int kFront = 256;     // frontier capacity per warp
+constexpr int kHitCap = 512;    // hits per warp
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ascending bitonic sort of a[0, n) (n a power of two, <= kHitCap) by one warp
+__device__ __forceinline__ void warp_bitonic(int32_t* a, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 2; k <= n; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < n; i += 32) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int32_t x0 = a[i], x1 = a[l];
+          if ((x0 > x1) == ((i & k) == 0)) {
+            a[i] = x1;
+            a[l] = x0;
+          }
+        }
+      }
+      __syncwarp();
+    }
+}
+
+__device__ __forceinline__ int pow2_at_least(int n) {
+  int p = 32;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+template <int Mode>
+__global__ void __launch_bounds__(32 * kQW) k_query_warp(
+    int32_t nst, const int32_t* __restrict__ stris, const double* __restrict__ x, double r, int n_leaf,
+    const Box* __restrict__ nodes, const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+    const int32_t* __restrict__ sorted_idx, int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
+    int32_t* __restrict__ out, int* wovf, const int32_t* __restrict__ vscene, const int2* __restrict__ srange,
+    const uint8_t* __restrict__ scene_mask) {
+  __shared__ int32_t fr[kQW][2][kFront];
+  __shared__ int32_t hits[kQW][kHitCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t* H = hits[w];
+  const unsigned lt = lanemask_lt();
+  for (int64_t st = blockIdx.x * (int64_t)kQW + w; st < nst; st += (int64_t)gridDim.x * kQW) {
+    const int qs = vscene ? vscene[stris[3 * st]] : -1;  // batched scenes: own scene only
+    if (scene_mask && !scene_mask[qs]) {  // scene not being re-sampled
+      if (!Mode && lane == 0) cnt[st] = 0;
+      continue;
+    }
+    Box q = tri_box(x, stris + 3 * st);
+    for (int k = 0; k < 3; ++k) {  // Aabb::inflated, core.hpp:77-82
+      q.lo[k] = q.lo[k] - r;
+      q.hi[k] = q.hi[k] + r;
+    }
+    int32_t* F0 = fr[w][0];
+    int32_t* F1 = fr[w][1];
+    if (lane == 0) F0[0] = 0;  // root (the single leaf when n_leaf == 1)
+    __syncwarp();
+    int nf = 1, nh = 0;
+    bool ovf = false;
+    while (nf > 0 && !ovf) {
+      int nn = 0;
+      for (int b0 = 0; b0 < nf; b0 += 32) {
+        const int i = b0 + lane;
+        int node = -1;
+        bool hit = false, push = false;
+        if (i < nf) {
+          node = F0[i];
+          bool ok = true;
+          if (qs >= 0) {
+            const int2 sr = srange[node];
+            ok = !(qs < sr.x || qs > sr.y);
+          }
+          if (ok && overlaps(nodes[node], q)) {
+            if (node >= n_leaf - 1) hit = true;
+            else push = true;
+          }
+        }
+        const unsigned hb = __ballot_sync(0xffffffffu, hit), pb = __ballot_sync(0xffffffffu, push);
+        const int hpos = nh + __popc(hb & lt), ppos = nn + 2 * __popc(pb & lt);
+        if (hit && hpos < kHitCap) H[hpos] = sorted_idx[node - (n_leaf - 1)];
+        if (push && ppos + 1 < kFront) {
+          F1[ppos] = left[node];
+          F1[ppos + 1] = right[node];
+        }
+        nh += __popc(hb);
+        nn += 2 * __popc(pb);
+      }
+      if (nn > kFront || nh > kHitCap) ovf = true;
+      __syncwarp();
+      int32_t* t = F0;
+      F0 = F1;
+      F1 = t;
+      nf = nn;
+    }
+    if (ovf) {
+      if (lane == 0) atomicExch(wovf, 1);
+      continue;
+    }
+    if (!Mode) {
+      if (lane == 0) cnt[st] = nh;
+      continue;
+    }
+    const int n2 = pow2_at_least(nh);
+    for (int i = nh + lane; i < n2; i += 32) H[i] = 0x7fffffff;
+    __syncwarp();
+    warp_bitonic(H, n2);
+    const int64_t base = off[st];
+    for (int i = lane; i < nh; i += 32) out[base + i] = H[i];
+    __syncwarp();
+  }
+}
+
+// K3 (default): the same per warp. A warp gathers its slave triangle's
+// candidate edges and vertex features (lower_bound into master.verts) into
+// shared memory, bitonic-sorts both lists, and keeps the first of each run of
+// equal ids (ballot compaction). Over kHitCap raw ids raises *wovf.
+__global__ void __launch_bounds__(32 * kQW) k_features_warp(
+    int32_t nst, const int64_t* __restrict__ tri_off, const int32_t* __restrict__ tri_ids,
+    const int32_t* __restrict__ mtris, const int32_t* __restrict__ mtri_edges, const int32_t* __restrict__ mverts,
+    int32_t n_mverts, int32_t* __restrict__ tmp_e, int32_t* __restrict__ tmp_v, int64_t* __restrict__ ecnt,
+    int64_t* __restrict__ vcnt, int* wovf) {
+  __shared__ int32_t bufE[kQW][kHitCap], bufV[kQW][kHitCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t* E = bufE[w];
+  int32_t* V = bufV[w];
+  const unsigned lt = lanemask_lt();
+  for (int64_t st = blockIdx.x * (int64_t)kQW + w; st < nst; st += (int64_t)gridDim.x * kQW) {
+    const int64_t a = tri_off[st], b = tri_off[st + 1];
+    const int k = (int)(3 * (b - a));
+    if (k > kHitCap) {
+      if (lane == 0) atomicExch(wovf, 1);
+      continue;
+    }
+    for (int j = lane; j < k; j += 32) {
+      const int mt = tri_ids[a + j / 3], e = j % 3;
+      E[j] = mtri_edges[3 * mt + e];
+      const int gv = mtris[3 * mt + e];
+      int lo = 0, hi = n_mverts;  // lower_bound into master.verts
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (mverts[mid] < gv) lo = mid + 1; else hi = mid;
+      }
+      V[j] = lo;
+    }
+    const int n2 = pow2_at_least(k);
+    for (int j = k + lane; j < n2; j += 32) E[j] = V[j] = 0x7fffffff;
+    __syncwarp();
+    warp_bitonic(E, n2);
+    warp_bitonic(V, n2);
+    int32_t* oe = tmp_e + 3 * a;
+    int32_t* ov = tmp_v + 3 * a;
+    int ue = 0, uv = 0;
+    for (int b0 = 0; b0 < k; b0 += 32) {
+      const int j = b0 + lane;
+      const bool fe = j < k && (j == 0 || E[j] != E[j - 1]);
+      const bool fv = j < k && (j == 0 || V[j] != V[j - 1]);
+      const unsigned be = __ballot_sync(0xffffffffu, fe), bv = __ballot_sync(0xffffffffu, fv);
+      if (fe) oe[ue + __popc(be & lt)] = E[j];
+      if (fv) ov[uv + __popc(bv & lt)] = V[j];
+      ue += __popc(be);
+      uv += __popc(bv);
+    }
+    if (lane == 0) {
+      ecnt[st] = ue;
+      vcnt[st] = uv;
+    }
+    __syncwarp();
   }
 }
 
@@ -987,7 +1174,7 @@ int lbvh_build(Lbvh& B, int32_t n, const int32_t* tris, const double* x, const i
 struct RebuildTmp : TmpBase {
   Lbvh bvh;
   DBuf<int64_t> cnt;
-  DBuf<int> ovf;
+  DBuf<int> ovf, wovf;
   DBuf<int32_t> tmp_e, tmp_v;
   DBuf<int64_t> ecnt, vcnt;
   DBuf<unsigned long long> err;
@@ -1047,35 +1234,68 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   auto& srange = B.srange;
   // K2: count, scan, emit+sort
   const uint8_t* smask = vsc && c.use_scene_mask ? c.scene_mask.p : nullptr;
+  auto& tmp_e = RT.tmp_e;
+  auto& tmp_v = RT.tmp_v;
+  auto& ecnt = RT.ecnt;
+  auto& vcnt = RT.vcnt;
   auto& cnt = RT.cnt;
   auto& ovf = RT.ovf;
   cnt.resize(nst + 1);
   cnt.zero(s);
   ovf.resize(1);
   ovf.zero(s);
-  k_query<0><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
-                                                 idx_sorted.p, cnt.p, nullptr, nullptr, ovf.p, vsc, srange.p, smask);
-  exclusive_scan(cnt.p, c.pair_off[0].p, nst + 1, s);
-  const int64_t ntri = last_of(c.pair_off[0], nst, s);
-  c.pair_ids[0].resize(std::max<int64_t>(ntri, 1));
-  k_query<1><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
-                                                 idx_sorted.p, nullptr, c.pair_off[0].p, c.pair_ids[0].p, ovf.p, vsc,
-                                                 srange.p, smask);
-  c.pair_ids[0].n = ntri;
-  // K3: candidate edges / verts
-  auto& tmp_e = RT.tmp_e;
-  auto& tmp_v = RT.tmp_v;
-  auto& ecnt = RT.ecnt;
-  auto& vcnt = RT.vcnt;
-  tmp_e.resize(std::max<int64_t>(3 * ntri, 1));
-  tmp_v.resize(std::max<int64_t>(3 * ntri, 1));
-  ecnt.resize(nst + 1);
-  vcnt.resize(nst + 1);
-  ecnt.zero(s);
-  vcnt.zero(s);
-  k_features<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.master.tris.p,
-                                                 c.master.tri_edges.p, c.master.verts.p, c.master.n_verts, tmp_e.p,
-                                                 tmp_v.p, ecnt.p, vcnt.p);
+  auto& wovf = RT.wovf;
+  wovf.resize(1);
+  // batched scenes keep the per-thread traversal: a scene-pruned query descends
+  // a 1-2 node frontier through the packed tree's upper levels, where 32
+  // independent queries per warp beat one query per warp
+  bool warp_path = !c.thread_query && vsc == nullptr;
+  for (;;) {  // the warp-cooperative kernels; the per-thread ones if a warp ran out of shared memory
+    cnt.zero(s);
+    wovf.zero(s);
+    const int gq = (int)std::min<int64_t>((nst + kQW - 1) / kQW, 148 * 64);
+    if (warp_path)
+      k_query_warp<0><<<gq, 32 * kQW, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
+                                              idx_sorted.p, cnt.p, nullptr, nullptr, wovf.p, vsc, srange.p, smask);
+    else
+      k_query<0><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
+                                                     idx_sorted.p, cnt.p, nullptr, nullptr, ovf.p, vsc, srange.p,
+                                                     smask);
+    exclusive_scan(cnt.p, c.pair_off[0].p, nst + 1, s);
+    const int64_t ntri = last_of(c.pair_off[0], nst, s);
+    c.pair_ids[0].resize(std::max<int64_t>(ntri, 1));
+    if (warp_path)
+      k_query_warp<1><<<gq, 32 * kQW, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
+                                              idx_sorted.p, nullptr, c.pair_off[0].p, c.pair_ids[0].p, wovf.p, vsc,
+                                              srange.p, smask);
+    else
+      k_query<1><<<grid_for(nst, 128), 128, 0, s>>>(nst, c.slave.tris.p, c.X(), r, nmt, nodes.p, left.p, right.p,
+                                                     idx_sorted.p, nullptr, c.pair_off[0].p, c.pair_ids[0].p, ovf.p,
+                                                     vsc, srange.p, smask);
+    c.pair_ids[0].n = ntri;
+    // K3: candidate edges / verts
+    tmp_e.resize(std::max<int64_t>(3 * ntri, 1));
+    tmp_v.resize(std::max<int64_t>(3 * ntri, 1));
+    ecnt.resize(nst + 1);
+    vcnt.resize(nst + 1);
+    ecnt.zero(s);
+    vcnt.zero(s);
+    if (warp_path)
+      k_features_warp<<<gq, 32 * kQW, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.master.tris.p,
+                                              c.master.tri_edges.p, c.master.verts.p, c.master.n_verts, tmp_e.p,
+                                              tmp_v.p, ecnt.p, vcnt.p, wovf.p);
+    else
+      k_features<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.master.tris.p,
+                                                     c.master.tri_edges.p, c.master.verts.p, c.master.n_verts,
+                                                     tmp_e.p, tmp_v.p, ecnt.p, vcnt.p);
+    c.launches += 3;
+    if (!warp_path) break;
+    int wo = 0;
+    GMCP_CUDA(cudaMemcpyAsync(&wo, wovf.p, sizeof wo, cudaMemcpyDeviceToHost, s));
+    c.sync();
+    if (!wo) break;
+    warp_path = false;
+  }
   exclusive_scan(ecnt.p, c.pair_off[1].p, nst + 1, s);
   exclusive_scan(vcnt.p, c.pair_off[2].p, nst + 1, s);
   const int64_t ne = last_of(c.pair_off[1], nst, s), nv = last_of(c.pair_off[2], nst, s);
@@ -1085,7 +1305,8 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
   k_compact<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, tmp_v.p, c.pair_off[2].p, c.pair_ids[2].p);
   c.pair_ids[1].n = ne;
   c.pair_ids[2].n = nv;
-  c.launches += 5;
+  c.launches += 2;
+  const int64_t ntri = c.pair_ids[0].n;
   GMCP_CUDA(cudaGetLastError());
   int of = 0;
   GMCP_CUDA(cudaMemcpyAsync(&of, ovf.p, sizeof of, cudaMemcpyDeviceToHost, s));
