@@ -14,11 +14,11 @@ ncu --set full --clock-control none --import-source on -k regex:k_run_partials -
 ncu --set full --clock-control none --import-source on -k regex:k_gather -s 2 -c 1 -o $O/k8 \
     python tools/k7_time.py > /dev/null 2>&1
 # the PCG kernels inside the C3 Newton solve (steady iteration: skip the first solves)
-ncu --set full --clock-control none --import-source on -k regex:k_spmv_cg -s 3000 -c 1 -o $O/spmv \
+ncu --set full --clock-control none --import-source on -k regex:k_spmv_cg -s 2600 -c 1 -o $O/spmv \
     python tools/newton_c3.py 3 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_update_agg -s 3000 -c 1 -o $O/update_agg \
+ncu --set full --clock-control none --import-source on -k regex:k_update_agg -s 2600 -c 1 -o $O/update_agg \
     python tools/newton_c3.py 3 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_coarse_prolong -s 3000 -c 1 -o $O/coarse_prolong \
+ncu --set full --clock-control none --import-source on -k regex:k_coarse_prolong -s 2600 -c 1 -o $O/coarse_prolong \
     python tools/newton_c3.py 3 > /dev/null 2>&1
 # per-launch durations of one steady PCG stretch
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
