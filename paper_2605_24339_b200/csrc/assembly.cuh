@@ -81,9 +81,15 @@ constexpr int kUC = 16;               // U' / V columns
 
 constexpr int kRunWarps = 4;          // warps (= runs in flight) per K7 block
 #ifndef K7_MINB
-#define K7_MINB 4
+#define K7_MINB 5  // 96 registers, no spills: 20 warps/SM (4: 128 registers, 16 warps/SM, K7 +4%)
 #endif
-constexpr int kStage = 16;            // sample rows staged per tensor-core pass
+#ifndef K7_PREFETCH
+#define K7_PREFETCH 0  // next-run metadata prefetch: costs the registers of minB 5 (1: spills)
+#endif
+#ifndef K7_STAGE
+#define K7_STAGE 16
+#endif
+constexpr int kStage = K7_STAGE;      // sample rows staged per tensor-core pass
 constexpr int kLDS = kStage + 4;      // column stride (doubles): conflict-free fragment loads
 
 // Per-warp shared memory: staged U' / V rows (column-major); after the last
@@ -137,6 +143,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     unsigned long long* __restrict__ red, double* __restrict__ warp_energy) {
   __shared__ RunSmem wsm[kRunWarps];
   __shared__ unsigned char pair_tab[kRunMasters + 1][kRunMasters * (kRunMasters + 1) / 2];  // t -> m | l << 4
+  __shared__ uint64_t ss_tab[2][32];  // per lane: SS slot offsets / mirror offsets (kept out of registers)
   pdl_trigger();  // K8 may take SM slots as K7's persistent blocks retire (it waits for K7's results)
   for (int q = threadIdx.x; q < (kRunMasters + 1) * kRunMasters; q += blockDim.x) {
     const int Mq = q / kRunMasters, m = q % kRunMasters;
@@ -153,6 +160,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
   // fragments F[8 mt + g][4 ks + t4]. SS output slot (mt, nt, e) is
   // SS[8 mt + g][8 nt + 2 t4 + e]: its partial offset (upper entries of the
   // six stored blocks, 0xff = not stored) and mirror offset (diagonal blocks).
+  {
   uint64_t ss_off = ~0ull, ss_mir = ~0ull;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -171,6 +179,13 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
           }
         }
       }
+  if (threadIdx.x < 32) {
+    ss_tab[0][lane] = ss_off;
+    ss_tab[1][lane] = ss_mir;
+  }
+  }
+  __syncthreads();
+
   double e_warp = 0;  // this warp's run energies, summed in its run order
   // persistent warps; the next run's metadata loads during this run
   struct Meta {
@@ -190,11 +205,18 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
   };
   const int64_t stride = (int64_t)gridDim.x * kRunWarps;
   int64_t r = blockIdx.x * (int64_t)kRunWarps + (threadIdx.x >> 5);
+#if K7_PREFETCH
   Meta nxt;
   if (r < n_runs) load_meta(r, nxt);
+#endif
   for (; r < n_runs; r += stride) {
+#if K7_PREFETCH
     const Meta cur = nxt;
     if (r + stride < n_runs) load_meta(r + stride, nxt);
+#else
+    Meta cur;
+    load_meta(r, cur);
+#endif
     const int64_t s0 = cur.s0, s1 = cur.s1, pb = cur.pb;
     const int M = cur.M, sid0 = cur.sid0, sid1 = cur.sid1, sid2 = cur.sid2, my_lm = cur.my_lm;
     {
@@ -382,7 +404,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int slot = 4 * mt + 2 * nt + e;
-            const int o = (int)((ss_off >> (8 * slot)) & 0xff), om = (int)((ss_mir >> (8 * slot)) & 0xff);
+            const int o = (int)((ss_tab[0][lane] >> (8 * slot)) & 0xff), om = (int)((ss_tab[1][lane] >> (8 * slot)) & 0xff);
             if (o != 0xff) P[kSSBase + o] = sv[mt][nt][e];
             if (om != 0xff) P[kSSBase + om] = sv[mt][nt][e];
           }
