@@ -140,7 +140,9 @@ constexpr double kRegularization = 1e-8;  // SolverSettings::regularization (sol
 constexpr int kStagWindow = 1024;
 constexpr int kStagWindowCoarse = 256;
 constexpr double kAcceptRelInf = 1e-6;  // solver.hpp:349-356 acceptance of a linear solve
-constexpr double kCoarseDrop = 1e-10;   // scaled coarse pivots below this drop their rigid mode
+// scaled coarse pivots below this drop their rigid mode: low enough to keep a
+// floating body's regularized rigid mode (pivot ~ shift / aggregate stiffness)
+constexpr double kCoarseDropDefault = 1e-13;
 constexpr double kSceneCoarseDrop = 1e-8;  // per-scene inverses: ill-conditioned rigid modes drop earlier
 constexpr double kCoarseStale = 1.25;   // refresh the coarse inverse when a solve needs 25% more iterations
 
@@ -1089,6 +1091,7 @@ struct SystemImpl {
   int coop_blocks = 0;       // co-resident CTAs of the fused cooperative kernel (0: not queried)
   int64_t load_step = 0;     // current load step (coarse refresh policy)
   bool coarse_refresh_always = false;  // GMCP_COARSE_REFRESH=1: new coarse inverse every solve
+  double coarse_drop = kCoarseDropDefault;  // GMCP_COARSE_DROP
   int coarse_scene_aggs = 24;          // batched scenes: aggregates per scene (GMCP_COARSE_SCENE_AGGS)
   bool use_coop = false;     // GMCP_COOP=1: update + coarse as one cooperative kernel (measured slower)
   int64_t u_gen = 0;         // union pattern generation (coarse pair lists follow it)
@@ -1705,11 +1708,11 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
   double* Y = C.B.p;
   GMCP_CUDA(cudaMemsetAsync(S.redu.p + 4, 0, sizeof(unsigned long long), S.stream));
   C.piv.resize(2 * kGJ * kGJ);
-  k_gj_pivot0<<<1, 32, 0, S.stream>>>(n_pad, X, C.piv.p, kCoarseDrop, S.redu.p + 4);
+  k_gj_pivot0<<<1, 32, 0, S.stream>>>(n_pad, X, C.piv.p, S.coarse_drop, S.redu.p + 4);
   ++S.launches;
   for (int k = 0; k < nt; ++k) {
     k_gj_step<<<dim3(nt, nt), 256, 0, S.stream>>>(n_pad, k, X, Y, C.piv.p + (k & 1) * kGJ * kGJ,
-                                                  C.piv.p + ((k + 1) & 1) * kGJ * kGJ, kCoarseDrop, S.redu.p + 4);
+                                                  C.piv.p + ((k + 1) & 1) * kGJ * kGJ, S.coarse_drop, S.redu.p + 4);
     ++S.launches;
     std::swap(X, Y);
   }
@@ -1972,6 +1975,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
   // with the coarse space a converging solve gains orders of magnitude per
   // 256 iterations, so a singular one is recognised four times sooner
   const int stag = coarse ? kStagWindowCoarse : kStagWindow;
+  bool failed = false;
   double win_min = INFINITY, prev_min = INFINITY;  // stagnation windows
   if (!S.ev0) {
     GMCP_CUDA(cudaEventCreate(&S.ev0));
@@ -1989,8 +1993,13 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     GMCP_CUDA(cudaEventElapsedTime(&ems, S.ev0, S.ev1));
     S.pcg_ev_ms += ems;
     S.pcg_ev_iters += chunk;
-    if (!std::isfinite(h[4])) throw StatusError(GMCP_ERR_SOLVER, "PCG diverged (non-finite residual)");
     if (!(h[4] > target)) break;  // rr <= tol^2 bb
+    // a non-finite residual or r.z <= 0 (the preconditioner lost positivity):
+    // the solve failed -> the caller retries regularized, as after a failed LDL^T
+    if (!std::isfinite(h[4]) || !(h[0] > 0)) {
+      failed = true;
+      break;
+    }
     win_min = std::min(win_min, h[4]);
     if (it % stag == 0) {
       if (it >= 2 * stag && !(win_min < 0.5 * prev_min) && h[4] > 1e-8 * bb) break;  // stagnated
@@ -1998,7 +2007,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
       win_min = INFINITY;
     }
   }
-  *rel_out = std::sqrt(h[4] / bb);
+  *rel_out = failed ? INFINITY : std::sqrt(h[4] / bb);
   GMCP_CUDA(cudaGetLastError());
   return it;
 }
@@ -2012,6 +2021,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
 // LAPACK solve of the same system sits at the same floor,
 // tests/test_gpu_linear_solve.py). Returns the total PCG iterations.
 constexpr int kMaxRefine = 3;
+constexpr double kRefineMaxDrift = 1e4;  // true / tolerance ratio beyond which the solve counts as failed
 int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.0) {
   int it = pcg_core(S, tol, maxit, rel_out, shift, S.grad.p);
   if (S.cs.enabled) {  // coarse refresh policy bookkeeping
@@ -2025,8 +2035,16 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
     return it;
   }
   true_residual(S, M);
+  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+  if (trace)
+    std::fprintf(stderr, "[gmcp] pcg shift %.3e: %d iterations, recursive %.3e, true %.3e (inf %.3e)\n", shift, it,
+                 *rel_out, S.last_true_rel2, S.last_true_relinf);
   const int n = (int)S.n_dof;
-  for (int k = 0; k < kMaxRefine && *rel_out <= tol && S.last_true_rel2 > tol && it < maxit; ++k) {
+  // refine a drifted residual only; a true residual orders of magnitude above the
+  // recursive one means a failed (e.g. singular) solve -> regularized retry
+  for (int k = 0; k < kMaxRefine && *rel_out <= tol && S.last_true_rel2 > tol &&
+                  S.last_true_rel2 < kRefineMaxDrift * tol && it < maxit;
+       ++k) {
     GMCP_CUDA(cudaMemcpyAsync(S.xacc.p, S.dx.p, n * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
     double rel_c;
     const double tc = std::min(0.5, 0.5 * tol / S.last_true_rel2);
@@ -3303,6 +3321,18 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
         S.sync();
         const double shift = kRegularization * dsum / (double)n_free;
         pit += pcg(S, st.pcg_tol, st.pcg_max_iters, &rel, shift);
+        if ((!(rel <= st.pcg_tol) || !(S.last_true_relinf <= kAcceptRelInf)) && S.cs.enabled) {
+          // last resort: the regularized solve with the smoother alone
+          S.cs.enabled = false;
+          try {
+            pit += pcg(S, st.pcg_tol, st.pcg_max_iters, &rel, shift);
+          } catch (...) {
+            S.cs.enabled = true;
+            throw;
+          }
+          S.cs.enabled = true;
+          ++S.coarse_fallbacks;
+        }
         if (!(rel <= st.pcg_tol) || !(S.last_true_relinf <= kAcceptRelInf)) {
           out->residual = resid;
           throw StatusError(GMCP_ERR_SOLVER,
@@ -3477,6 +3507,7 @@ int gmcp_system_create(int device, gmcp_system** out) {
     if (const char* e = std::getenv("GMCP_COARSE_AGGS")) s->s.coarse_aggs = std::min(512, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("GMCP_COOP")) s->s.use_coop = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE_REFRESH")) s->s.coarse_refresh_always = std::atoi(e) != 0;
+    if (const char* e = std::getenv("GMCP_COARSE_DROP")) s->s.coarse_drop = std::atof(e);
     if (const char* e = std::getenv("GMCP_COARSE_SCENE_AGGS"))
       s->s.coarse_scene_aggs = std::min(32, std::max(1, std::atoi(e)));
     *out = s;
