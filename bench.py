@@ -163,6 +163,26 @@ def pcg_roofline(ps: dict, pre: dict | None = None) -> dict:
             "clock": "CUDA events around each 16-iteration chunk graph on the solve stream"}
 
 
+def cpu_scene_reference(name: str):
+    """The reference's parse_scene + build_scene + System::solve (scene.hpp,
+    solver.hpp) on one of the repo's scene files, oracle/_ref, 1 thread."""
+    import ctypes as C
+    lib = os.path.join(ROOT, "oracle", "_ref", "libgmcp_ref.so")
+    if not os.path.exists(lib):
+        return None
+    L = C.CDLL(lib)
+    path = os.path.join(ROOT, "scenes", name + ".scene").encode()
+    n = C.c_int64()
+    if L.ref_run_scene(C.c_char_p(path), C.byref(n), None, None, None, C.c_int32(0)) != 0:
+        return None
+    x, st, fo = np.zeros(n.value), np.zeros(6), np.zeros(24)
+    if L.ref_run_scene(C.c_char_p(path), C.byref(n), C.c_void_p(x.ctypes.data), C.c_void_p(st.ctypes.data),
+                       C.c_void_p(fo.ctypes.data), C.c_int32(8)) != 0:
+        return None
+    return {"newton_iters": int(st[0]), "rebuilds": int(st[1]), "wall_seconds": float(st[3]),
+            "steps_per_s": float(st[0] / st[3]), "x": x}
+
+
 def cpu_newton_reference(refine: float = 0.7):
     """The reference's own System::solve (solver.hpp:125-228) through run_hertz
     (bench.hpp:210-303) on C1, compiled from the reference sources (oracle/_ref;
@@ -468,6 +488,17 @@ def main():
                         "solve_seconds": dev_solve, "solve_newton_iters": int(hr.stats.total_newton_iters),
                         "solve_steps_per_s": hr.stats.total_newton_iters / dev_solve, "peak": hr.peak}
         del hr
+        # C4 (scenes/fingertip.scene: two pads squeeze a clamped object, 2 contact
+        # pairs, 20 load steps, rebuilds): parse_scene + build_scene + solve
+        from paper_2605_24339_b200 import scene as SC
+        t0 = time.perf_counter()
+        c4_sys, c4_st = SC.run_scene(os.path.join(ROOT, "scenes", "fingertip.scene"), device=local)
+        c4_s = time.perf_counter() - t0
+        newton["c4"] = {"scene": "C4 fingertip (scenes/fingertip.scene), 2 contact pairs, 20 load steps",
+                        "solve_seconds": c4_s, "solve_newton_iters": int(c4_st.total_newton_iters),
+                        "solve_rebuilds": int(c4_st.total_rebuilds), "solve_steps_per_s": c4_st.total_newton_iters / c4_s,
+                        "x": c4_sys.x.copy()}
+        del c4_sys
 
     # C5: the 1024-scene batched job (C1 Hertz scenes) on the
     # product path (paper_2605_24339_b200/batch.py): scenes sharded across
@@ -594,12 +625,29 @@ def main():
             newton["cpu_baseline"] = {"value": ref["steps_per_s"], "unit": "Newton steps/s", "cores": 1,
                                       "kind": ref["kind"], "sample": ref["sample"]}
             c1 = newton["c1"]
-            e2e_solve = {"what": "C1 full load-stepped solve through the public API (host scene in, host x out): "
+            e2e_solve = {"what": "full load-stepped solves through the public API (host scene in, host x out): "
                                  "device System::solve vs the reference System::solve on 1 host thread",
-                         "device_seconds": c1["solve_seconds"], "reference_seconds": ref["wall_seconds"],
-                         "speedup": ref["wall_seconds"] / c1["solve_seconds"],
-                         "device_newton_iters": c1["solve_newton_iters"], "reference_newton_iters": ref["newton_iters"],
-                         "device_peak": c1["peak"], "reference_peak": ref["peak"]}
+                         "c1": {"device_seconds": c1["solve_seconds"], "reference_seconds": ref["wall_seconds"],
+                                "speedup": ref["wall_seconds"] / c1["solve_seconds"],
+                                "device_newton_iters": c1["solve_newton_iters"],
+                                "reference_newton_iters": ref["newton_iters"], "device_peak": c1["peak"],
+                                "reference_peak": ref["peak"]}}
+        c4 = newton.get("c4")
+        r4 = cpu_scene_reference("fingertip") if c4 else None
+        if r4:
+            x4 = c4.pop("x")
+            newton["cpu_baseline_c4"] = {"value": r4["steps_per_s"], "unit": "Newton steps/s", "cores": 1,
+                                         "kind": "reference", "sample": "C4 fingertip full 20-load-step solve, "
+                                         "reference parse_scene + build_scene + System::solve (oracle/_ref), 1 thread"}
+            e2e_solve = e2e_solve or {"what": "full load-stepped solves, device vs reference"}
+            e2e_solve["c4"] = {"device_seconds": c4["solve_seconds"], "reference_seconds": r4["wall_seconds"],
+                               "speedup": r4["wall_seconds"] / c4["solve_seconds"],
+                               "device_newton_iters": c4["solve_newton_iters"],
+                               "reference_newton_iters": r4["newton_iters"],
+                               "device_rebuilds": c4["solve_rebuilds"], "reference_rebuilds": r4["rebuilds"],
+                               "max_abs_x_diff": float(np.abs(x4 - r4["x"]).max())}
+    if newton and "c4" in newton:
+        newton["c4"].pop("x", None)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:

@@ -665,130 +665,6 @@ __global__ void __launch_bounds__(kAggThreads) k_coarse_prolong(
   }
 }
 
-// Software grid barrier for a cooperatively launched (co-resident) grid:
-// bar[0] arrivals, bar[1] generation.
-__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* gen = bar + 1;
-    const unsigned int g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// k_update_agg and k_coarse_prolong<false> as ONE cooperative kernel (one CTA
-// per aggregate, all co-resident): update + restriction, grid barrier, coarse
-// rows + prolongation of the CTA's own aggregate; rz = r.M1^-1 r + s.y and rr
-// by the last block, in aggregate order.
-template <bool kPair>
-__global__ void __launch_bounds__(kAggThreads) k_update_coarse(
-    const int32_t* __restrict__ agg_off, const int32_t* __restrict__ agg_verts, const double* __restrict__ dvec,
-    const double* __restrict__ mask, const double* __restrict__ scale, const double* __restrict__ p,
-    const double* __restrict__ q, double* __restrict__ x, const double* r_in, double* r_out, double* z,
-    const double* __restrict__ minv, const int32_t* __restrict__ pair, double* s, int n_pad,
-    const double* __restrict__ Ainv, double* aparts, unsigned int* bar, double* scal, RedSlot rs) {
-  __shared__ double sh[kAggThreads / 32][8];
-  __shared__ double ya[6], sy[6];
-  const int a = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const double al = scal[2];
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // t(3), w(3), rz, rr
-  const int e0 = agg_off[a], e1 = agg_off[a + 1];
-  for (int e = e0 + threadIdx.x; e < e1; e += kAggThreads) {
-    const int v = agg_verts[e];
-    const d3 xv = ld3nc(x, v) + al * ld3nc(p, v);
-    const d3 rv = ld3nc(r_in, v) - al * ld3nc(q, v);
-    d3 zv;
-    if (kPair) {
-      const int pp = pair[v];
-      const d3 rp = pp < 0 ? mk3(0, 0, 0) : ld3nc(r_in, pp) - al * ld3nc(q, pp);
-      zv = pair_apply(minv, v, rv, rp);
-    } else {
-      zv = bmv(minv + 9 * (int64_t)v, rv);
-    }
-    x[3 * v] = xv.x;
-    x[3 * v + 1] = xv.y;
-    x[3 * v + 2] = xv.z;
-    r_out[3 * v] = rv.x;
-    r_out[3 * v + 1] = rv.y;
-    r_out[3 * v + 2] = rv.z;
-    z[3 * v] = zv.x;
-    z[3 * v + 1] = zv.y;
-    z[3 * v + 2] = zv.z;
-    const d3 m = ld3(mask, v);
-    const d3 mr = mk3(m.x * rv.x, m.y * rv.y, m.z * rv.z);
-    const d3 w = cross(ld3(dvec, v), mr);
-    acc[0] += mr.x;
-    acc[1] += mr.y;
-    acc[2] += mr.z;
-    acc[3] += w.x;
-    acc[4] += w.y;
-    acc[5] += w.z;
-    acc[6] += dot(rv, zv);
-    acc[7] += dot(rv, rv);
-  }
-  cta_sum<8, kAggThreads>(acc, sh);
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < 6; ++k) s[6 * a + k] = acc[k] * scale[6 * a + k];
-    aparts[2 * a] = acc[6];
-    aparts[2 * a + 1] = acc[7];
-  }
-  grid_barrier(bar);
-  if (wid < 6) {  // coarse rows of this aggregate: s was written by every CTA (coherent loads)
-    const int i = 6 * a + wid;
-    const double* row = Ainv + (int64_t)i * n_pad;
-    double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-    int j = lane;
-    for (; j + 96 < n_pad; j += 128) {
-      const double a0 = __ldg(row + j), a1 = __ldg(row + j + 32), a2 = __ldg(row + j + 64), a3 = __ldg(row + j + 96);
-      const double b0 = __ldcg(s + j), b1 = __ldcg(s + j + 32), b2 = __ldcg(s + j + 64), b3 = __ldcg(s + j + 96);
-      c0 += a0 * b0;
-      c1 += a1 * b1;
-      c2 += a2 * b2;
-      c3 += a3 * b3;
-    }
-    for (; j < n_pad; j += 32) c0 += __ldg(row + j) * __ldcg(s + j);
-    const double ac = warp_sum((c0 + c1) + (c2 + c3));
-    if (lane == 0) {
-      ya[wid] = scale[i] * ac;
-      sy[wid] = __ldcg(s + i) * ac;
-    }
-  }
-  __syncthreads();
-  const d3 t = mk3(ya[0], ya[1], ya[2]), om = mk3(ya[3], ya[4], ya[5]);
-  for (int e = e0 + threadIdx.x; e < e1; e += kAggThreads) {
-    const int v = agg_verts[e];
-    const d3 u = t + cross(om, ld3(dvec, v));
-    const d3 m = ld3(mask, v);
-    z[3 * v] += m.x * u.x;
-    z[3 * v + 1] += m.y * u.y;
-    z[3 * v + 2] += m.z * u.z;
-  }
-  double d[1] = {threadIdx.x == 0 ? ((sy[0] + sy[1]) + (sy[2] + sy[3])) + (sy[4] + sy[5]) : 0.0};
-  double out[1];
-  if (block_reduce_last<1, kAggThreads>(d, rs, out) && threadIdx.x == 0) {
-    double rzb = 0, rr = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-      rzb += __ldcg(aparts + 2 * b);
-      rr += __ldcg(aparts + 2 * b + 1);
-    }
-    const double rz = rzb + out[0];
-    const double rz_old = scal[0];
-    scal[3] = rz_old != 0 ? rz / rz_old : 0.0;
-    scal[0] = rz;
-    scal[4] = rr;
-  }
-}
-
 // Block-Jacobi: Minv_v = inverse of the masked 3x3 diagonal block.
 // diagonal block of row v copied to d[9] (either layout); false if absent
 __device__ __forceinline__ bool get_diag(const Bcsr& A, int v, double* d) {
@@ -1088,12 +964,10 @@ struct SystemImpl {
   bool use_pair = true, use_coarse = true;
   int coarse_aggs = 128;
   CoarseSpace cs;            // two-level coarse space (coarse.cuh)
-  int coop_blocks = 0;       // co-resident CTAs of the fused cooperative kernel (0: not queried)
   int64_t load_step = 0;     // current load step (coarse refresh policy)
   bool coarse_refresh_always = false;  // GMCP_COARSE_REFRESH=1: new coarse inverse every solve
   double coarse_drop = kCoarseDropDefault;  // GMCP_COARSE_DROP
   int coarse_scene_aggs = 24;          // batched scenes: aggregates per scene (GMCP_COARSE_SCENE_AGGS)
-  bool use_coop = false;     // GMCP_COOP=1: update + coarse as one cooperative kernel (measured slower)
   int64_t u_gen = 0;         // union pattern generation (coarse pair lists follow it)
   DBuf<unsigned int> counter;
   DBuf<unsigned long long> redu;
@@ -1826,17 +1700,6 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
       C.ref_iters = -1;  // set by this solve
     }
   }
-  // the fused cooperative update + coarse kernel needs all aggregates co-resident
-  if (coarse && S.coop_blocks == 0) {
-    int occ = 0, sms = 0;
-    GMCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_coarse<true>, kAggThreads, 0));
-    int occ2 = 0;
-    GMCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_update_coarse<false>, kAggThreads, 0));
-    GMCP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, S.device));
-    S.coop_blocks = std::max(1, std::min(occ, occ2) * sms);
-  }
-  const bool coop = coarse && S.use_coop && C.n_agg <= S.coop_blocks;
-  if (coop) C.aparts.resize(2 * (int64_t)C.n_agg);
   // two-level init: z += P Ac^+ P^T r, completing r.z (beta = 0)
   auto coarse_init = [&]() {
     k_restrict<<<C.n_agg, 256, 0, S.stream>>>(C.n_agg, C.agg_off.p, C.agg_verts.p, C.dvec.p, S.mask_d.p, S.r.p,
@@ -1895,7 +1758,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
                           pairs ? (const void*)S.minv2.p : (const void*)S.minv.p, S.scal.p,
                           pairs ? (const void*)S.r2.p : (const void*)S.parts.p, S.counter.p,
                           coarse ? (const void*)C.inv : nullptr, coarse ? (const void*)C.s.p : nullptr,
-                          coarse ? (coop ? (const void*)C.aparts.p : (const void*)C.agg.p) : nullptr};
+                          coarse ? (const void*)C.agg.p : nullptr};
   static_assert(sizeof ptrs == sizeof key.ptrs, "PcgKey pointer list");
   std::memcpy(key.ptrs, ptrs, sizeof ptrs);
   auto same_bcsr = [](const Bcsr& a, const Bcsr& b) {
@@ -1925,37 +1788,17 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
       if (coarse) {  // update + restriction, then coarse solve + prolongation (per aggregate)
         const double* rin = pairs ? ((k & 1) ? S.r2.p : S.r.p) : S.r.p;
         double* rout = pairs ? ((k & 1) ? S.r.p : S.r2.p) : S.r.p;
-        if (coop) {  // one cooperative kernel (grid barrier between the two halves)
-          cudaLaunchConfig_t cfg{};
-          cfg.gridDim = dim3(C.n_agg);
-          cfg.blockDim = dim3(kAggThreads);
-          cfg.stream = S.stream;
-          cudaLaunchAttribute at[1];
-          at[0].id = cudaLaunchAttributeCooperative;
-          at[0].val.cooperative = 1;
-          cfg.attrs = at;
-          cfg.numAttrs = 1;
-          const double* mi = pairs ? S.minv2.p : S.minv.p;
-          const int32_t* pd = pairs ? S.pair_d.p : nullptr;
-          GMCP_CUDA(cudaLaunchKernelEx(&cfg, pairs ? k_update_coarse<true> : k_update_coarse<false>,
-                                       (const int32_t*)C.agg_off.p, (const int32_t*)C.agg_verts.p,
-                                       (const double*)C.dvec.p, (const double*)S.mask_d.p, (const double*)C.scale.p,
-                                       (const double*)p_new, (const double*)S.q.p, S.dx.p, rin, rout, S.z.p, mi, pd,
-                                       C.s.p, C.n_pad, (const double*)C.inv, C.aparts.p, S.counter.p + 8, S.scal.p,
-                                       S.slot(2)));
-        } else {
-          if (pairs)
-            k_update_agg<true><<<C.n_agg, kAggThreads, 0, S.stream>>>(
-                C.agg_off.p, C.agg_verts.p, C.dvec.p, S.mask_d.p, C.scale.p, p_new, S.q.p, S.dx.p, rin, rout, S.z.p,
-                S.minv2.p, S.pair_d.p, C.s.p, S.scal.p, S.slot(2));
-          else
-            k_update_agg<false><<<C.n_agg, kAggThreads, 0, S.stream>>>(
-                C.agg_off.p, C.agg_verts.p, C.dvec.p, S.mask_d.p, C.scale.p, p_new, S.q.p, S.dx.p, rin, rout, S.z.p,
-                S.minv.p, nullptr, C.s.p, S.scal.p, S.slot(2));
-          k_coarse_prolong<false><<<C.n_agg, kAggThreads, 0, S.stream>>>(C.n_pad, C.inv, C.scale.p, C.s.p,
-                                                                      C.agg_off.p, C.agg_verts.p, C.dvec.p,
-                                                                      S.mask_d.p, S.z.p, S.scal.p, S.slot(6));
-        }
+        if (pairs)
+          k_update_agg<true><<<C.n_agg, kAggThreads, 0, S.stream>>>(
+              C.agg_off.p, C.agg_verts.p, C.dvec.p, S.mask_d.p, C.scale.p, p_new, S.q.p, S.dx.p, rin, rout, S.z.p,
+              S.minv2.p, S.pair_d.p, C.s.p, S.scal.p, S.slot(2));
+        else
+          k_update_agg<false><<<C.n_agg, kAggThreads, 0, S.stream>>>(
+              C.agg_off.p, C.agg_verts.p, C.dvec.p, S.mask_d.p, C.scale.p, p_new, S.q.p, S.dx.p, rin, rout, S.z.p,
+              S.minv.p, nullptr, C.s.p, S.scal.p, S.slot(2));
+        k_coarse_prolong<false><<<C.n_agg, kAggThreads, 0, S.stream>>>(C.n_pad, C.inv, C.scale.p, C.s.p,
+                                                                    C.agg_off.p, C.agg_verts.p, C.dvec.p,
+                                                                    S.mask_d.p, S.z.p, S.scal.p, S.slot(6));
       } else if (pairs) {  // r ping-pongs with p (chunk is even: r ends in S.r)
         k_update_cg_pair<false><<<gup, kThreads, 0, S.stream>>>(nv, p_new, S.q.p, S.dx.p, (k & 1) ? S.r2.p : S.r.p,
                                                                 (k & 1) ? S.r.p : S.r2.p, S.z.p, S.minv2.p,
@@ -1985,7 +1828,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     GMCP_CUDA(cudaEventRecord(S.ev0, S.stream));
     GMCP_CUDA(cudaGraphLaunch(exec, S.stream));
     GMCP_CUDA(cudaEventRecord(S.ev1, S.stream));
-    S.launches += (coarse && !coop ? 3 : 2) * chunk;
+    S.launches += (coarse ? 3 : 2) * chunk;
     it += chunk;
     GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
     S.sync();
@@ -3505,7 +3348,6 @@ int gmcp_system_create(int device, gmcp_system** out) {
     if (const char* e = std::getenv("GMCP_PAIR_JACOBI")) s->s.use_pair = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE")) s->s.use_coarse = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE_AGGS")) s->s.coarse_aggs = std::min(512, std::max(1, std::atoi(e)));
-    if (const char* e = std::getenv("GMCP_COOP")) s->s.use_coop = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE_REFRESH")) s->s.coarse_refresh_always = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE_DROP")) s->s.coarse_drop = std::atof(e);
     if (const char* e = std::getenv("GMCP_COARSE_SCENE_AGGS"))
