@@ -693,6 +693,11 @@ struct Out {
   int8_t* type;
   int32_t *slave, *master;
   double *beta_s, *beta_m, *eta, *weight, *gamma, *eps, *g_ref;
+  // single-pass mode (k_sample<2>): records land unordered at warp-aggregated
+  // slots of a staging buffer, keyed (task << 5 | k) for the ordering sort
+  uint32_t* key = nullptr;
+  unsigned int* ctr = nullptr;
+  int64_t cap = 0;
 };
 
 struct SampleRec {
@@ -738,7 +743,24 @@ __device__ __forceinline__ void put(const SamplerArgs& A, const int32_t* sid, co
   double g_ref, eps;
   if (!freeze(A, sid, r, g_ref, eps, err)) return;
   if (Mode) {
-    const int64_t i = base + c;
+    int64_t i;
+    if (Mode == 2) {  // base = task index; one atomic per group of lanes emitting together
+      const unsigned am = __activemask();
+      const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+      unsigned lt;
+      asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+      unsigned b0 = 0;
+      if (lane == leader) b0 = atomicAdd(O.ctr, (unsigned)__popc(am));
+      b0 = __shfl_sync(am, b0, leader);
+      i = (int64_t)b0 + __popc(am & lt);
+      if (i >= O.cap) {  // staging full: counted, not stored (the host re-runs with room)
+        ++c;
+        return;
+      }
+      O.key[i] = ((uint32_t)base << 5) | (uint32_t)c;
+    } else {
+      i = base + c;
+    }
     O.type[i] = r.type;
     for (int k = 0; k < 3; ++k) {
       O.slave[3 * i + k] = sid[k];
@@ -809,7 +831,7 @@ __global__ void __launch_bounds__(128) k_sample(SamplerArgs A, int64_t ntask, co
     const int32_t* sid = A.stris + 3 * st;
     const d3 s[3] = {ld3(A.x, sid[0]), ld3(A.x, sid[1]), ld3(A.x, sid[2])};
     int64_t c = 0;
-    const int64_t base = Mode ? off[t] : 0;
+    const int64_t base = Mode == 1 ? off[t] : (Mode == 2 ? t : 0);
     bool bad = false, ferr = false;
     Frame f;
     if (!tangent_frame(s[0], s[1], s[2], f)) {
@@ -970,6 +992,29 @@ __global__ void k_tasks(int32_t nst, const int64_t* __restrict__ toff, const int
       task_feat[o] = pids[i];
       task_kind[o] = kPoint;
     }
+  }
+}
+
+__global__ void k_iota(int64_t n, uint32_t* __restrict__ v) {
+  GRID_LOOP(i, n) v[i] = (uint32_t)i;
+}
+
+// single-pass sampler: staged records -> reference order (sorted keys)
+__global__ void k_unstage(int64_t n, const uint32_t* __restrict__ src_of, Out S, Out O) {
+  GRID_LOOP(i, n) {
+    const int64_t j = src_of[i];
+    O.type[i] = S.type[j];
+    for (int k = 0; k < 3; ++k) {
+      O.slave[3 * i + k] = S.slave[3 * j + k];
+      O.master[3 * i + k] = S.master[3 * j + k];
+      O.beta_s[3 * i + k] = S.beta_s[3 * j + k];
+      O.beta_m[3 * i + k] = S.beta_m[3 * j + k];
+    }
+    O.eta[i] = S.eta[j];
+    O.weight[i] = S.weight[j];
+    O.gamma[i] = S.gamma[j];
+    O.eps[i] = S.eps[j];
+    O.g_ref[i] = S.g_ref[j];
   }
 }
 
@@ -1184,6 +1229,14 @@ struct RebuildTmp : TmpBase {
   DBuf<int32_t> task_st, task_feat;
   DBuf<int8_t> task_kind;
   DBuf<int64_t> tcnt, toff;
+  struct Stage {
+    DBuf<int8_t> type;
+    DBuf<int32_t> slave, master;
+    DBuf<double> beta_s, beta_m, eta, weight, gamma, eps, gref;
+  } stage;                        // single-pass sampler staging (unordered)
+  int64_t stage_cap = 0;
+  DBuf<uint32_t> skey, skey2, sidx, sidx2;
+  DBuf<unsigned int> sctr;
 };
 RebuildTmp& rebuild_tmp(Ctx& c) {
   if (!c.rebuild_tmp) c.rebuild_tmp = std::make_unique<RebuildTmp>();
@@ -1390,20 +1443,55 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
   task_st.resize(std::max<int64_t>(ntask, 1));
   task_feat.resize(std::max<int64_t>(ntask, 1));
   task_kind.resize(std::max<int64_t>(ntask, 1));
-  tcnt.resize(ntask + 1);
-  tcnt.zero(s);
-  toff.resize(ntask + 1);
   Out O{};
   if (ntask) {
     k_tasks<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.pair_off[1].p,
                                                 c.pair_ids[1].p, pt_off.p, pt_ids.p, task_st.p, task_feat.p,
                                                 task_kind.p);
-    k_sample<0><<<grid_for(ntask, 128), 128, 0, s>>>(A, ntask, task_st.p, task_feat.p, task_kind.p, tcnt.p, nullptr,
-                                                      O, err.p);
-    c.launches += 2;
+    ++c.launches;
   }
-  exclusive_scan(tcnt.p, toff.p, ntask + 1, s);
-  const int64_t n = last_of(toff, ntask, s);
+  if (ntask >= (int64_t)1 << 27) throw StatusError(GMCP_ERR_CONFIG, "sampler: too many (slave tri, feature) tasks");
+  // one pass over the tasks: every accepted sample goes to a staging slot
+  // (warp-aggregated atomics) keyed by (task, index in task); a radix sort of
+  // the keys then restores the reference order (contact_sampling.hpp:438-468)
+  auto& st_ = RT.stage;
+  auto& skey = RT.skey;
+  auto& skey2 = RT.skey2;
+  auto& sidx = RT.sidx;
+  auto& sidx2 = RT.sidx2;
+  auto& sctr = RT.sctr;
+  sctr.resize(1);
+  int64_t cap = std::max<int64_t>({RT.stage_cap, ntask, c.ns + c.ns / 4, 1});
+  unsigned int cnt_h = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (cap > RT.stage_cap) {
+      st_.type.resize(cap);
+      st_.slave.resize(3 * cap);
+      st_.master.resize(3 * cap);
+      st_.beta_s.resize(3 * cap);
+      st_.beta_m.resize(3 * cap);
+      st_.eta.resize(cap);
+      st_.weight.resize(cap);
+      st_.gamma.resize(cap);
+      st_.eps.resize(cap);
+      st_.gref.resize(cap);
+      skey.resize(cap);
+      RT.stage_cap = cap;
+    }
+    Out SO{st_.type.p, st_.slave.p, st_.master.p, st_.beta_s.p, st_.beta_m.p, st_.eta.p,
+           st_.weight.p, st_.gamma.p, st_.eps.p, st_.gref.p, skey.p, sctr.p, cap};
+    sctr.zero(s);
+    if (ntask) {
+      k_sample<2><<<grid_for(ntask, 128), 128, 0, s>>>(A, ntask, task_st.p, task_feat.p, task_kind.p, nullptr,
+                                                        nullptr, SO, err.p);
+      ++c.launches;
+    }
+    GMCP_CUDA(cudaMemcpyAsync(&cnt_h, sctr.p, sizeof cnt_h, cudaMemcpyDeviceToHost, s));
+    c.sync();
+    if ((int64_t)cnt_h <= cap) break;
+    cap = (int64_t)cnt_h;  // staging was too small: every record counted, re-run with room
+  }
+  const int64_t n = cnt_h;
   unsigned long long e = 0;
   GMCP_CUDA(cudaMemcpyAsync(&e, err.p, sizeof e, cudaMemcpyDeviceToHost, s));
   c.sync();
@@ -1422,9 +1510,17 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
   O = Out{c.s_type.p, c.s_slave.p, c.s_master.p, c.s_beta_s.p, c.s_beta_m.p, c.s_eta.p,
           c.s_weight.p, c.s_gamma.p, c.s_eps.p, c.s_gref.p};
   if (n) {
-    k_sample<1><<<grid_for(ntask, 128), 128, 0, s>>>(A, ntask, task_st.p, task_feat.p, task_kind.p, nullptr, toff.p,
-                                                      O, err.p);
-    ++c.launches;
+    skey2.resize(n);
+    sidx.resize(n);
+    sidx2.resize(n);
+    k_iota<<<grid_for(n, 256), 256, 0, s>>>(n, sidx.p);
+    int kb = 5;
+    while (((int64_t)1 << kb) < (ntask << 5)) ++kb;
+    sort_pairs(skey.p, skey2.p, sidx.p, sidx2.p, n, s, kb);
+    Out SO{st_.type.p, st_.slave.p, st_.master.p, st_.beta_s.p, st_.beta_m.p, st_.eta.p,
+           st_.weight.p, st_.gamma.p, st_.eps.p, st_.gref.p};
+    k_unstage<<<grid_for(n, 256), 256, 0, s>>>(n, sidx2.p, SO, O);
+    c.launches += 2;
   }
   GMCP_CUDA(cudaGetLastError());
   derive_sample_fields(c);

@@ -3351,7 +3351,7 @@ int gmcp_system_create(int device, gmcp_system** out) {
     if (const char* e = std::getenv("GMCP_COARSE_REFRESH")) s->s.coarse_refresh_always = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE_DROP")) s->s.coarse_drop = std::atof(e);
     if (const char* e = std::getenv("GMCP_COARSE_SCENE_AGGS"))
-      s->s.coarse_scene_aggs = std::min(32, std::max(1, std::atoi(e)));
+      s->s.coarse_scene_aggs = std::min(64, std::max(1, std::atoi(e)));
     *out = s;
     return GMCP_OK;
   } catch (const StatusError& e) {
