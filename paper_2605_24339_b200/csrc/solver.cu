@@ -304,8 +304,10 @@ __device__ __forceinline__ void add_block(const MatSet& M, int v, int w, double*
       for (int q = 0; q < 9; ++q) d[q] += t[q];
 }
 __global__ void k_pair_jacobi(int nv, MatSet M, const double* __restrict__ mask, const int32_t* __restrict__ pair,
-                              double* __restrict__ minv2) {
+                              double* __restrict__ minv2, const int32_t* __restrict__ vscene = nullptr,
+                              const double* __restrict__ shift_s = nullptr) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    if (shift_s) M.shift = shift_s[vscene[v]];  // batched scenes: the scene's own shift (pairs lie in one scene)
     const int pv = pair[v];
     const int a = pv < 0 ? v : min(v, pv), b = pv < 0 ? v : max(v, pv);
     const int n = pv < 0 ? 3 : 6;
@@ -1120,7 +1122,7 @@ void build_elastic(SystemImpl& S) {
   S.el_nnzb = (int64_t)cols.size();
 #if GMCP_PAIR_JACOBI
   S.has_pairs = false;
-  if (S.n_scenes <= 1 && S.use_pair) {  // vertex pairs (single systems; batched scenes use the per-scene CTA PCG) for the 6x6 block-Jacobi: greedy matching of the strongest
+  if (S.use_pair) {  // vertex pairs for the 6x6 block-Jacobi (single systems and the per-scene CTA PCG): greedy matching of the strongest
      // normalized elastic couplings |K_vw|_F^2 / (|K_vv|_F |K_ww|_F) (ties by index)
     std::vector<double> dn(nv, 0.0);
     for (int v = 0; v < nv; ++v)
@@ -2383,7 +2385,9 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
                                                           const double* __restrict__ grad, double* __restrict__ x,
                                                           double* r, double* z, double* __restrict__ p,
                                                           double* __restrict__ q, double tol2, int maxit,
-                                                          double* __restrict__ st, SceneCoarse CS) {
+                                                          double* __restrict__ st, SceneCoarse CS,
+                                                          const int32_t* __restrict__ pair,
+                                                          const double* __restrict__ minv2) {
   __shared__ double sh[2][kCtaThreads / 32];
   __shared__ double s_sm[kCoarse ? kSceneCoarseMax : 1], y_sm[kCoarse ? kSceneCoarseMax : 1];
   const int sc = blockIdx.x;
@@ -2392,10 +2396,27 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
   const double shift = shift_s[sc];
   // init: x = 0, r = -mask .* grad, z = Minv r, p = z
   double rz = 0, rr = 0;
+  // vertex-pair smoother (pair != null): z_v = Minv2_v [r_v; r_partner] needs
+  // the partner's residual, so r is written in its own loop and published first
+  if (pair) {
+    for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
+      const d3 m = ld3(mask, v), g = ld3(grad, v);
+      r[3 * v] = -m.x * g.x;
+      r[3 * v + 1] = -m.y * g.y;
+      r[3 * v + 2] = -m.z * g.z;
+    }
+    __syncthreads();
+  }
   for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
     const d3 m = ld3(mask, v), g = ld3(grad, v);
     const d3 rv = mk3(-m.x * g.x, -m.y * g.y, -m.z * g.z);
-    const d3 zv = bmv(minv + 9 * (int64_t)v, rv);
+    d3 zv;
+    if (pair) {
+      const int pp = pair[v];
+      zv = pair_apply(minv2, v, rv, pp < 0 ? mk3(0, 0, 0) : ld3nc(r, pp));
+    } else {
+      zv = bmv(minv + 9 * (int64_t)v, rv);
+    }
     const double ra[3] = {rv.x, rv.y, rv.z}, za[3] = {zv.x, zv.y, zv.z};
     for (int k = 0; k < 3; ++k) {
       x[3 * v + k] = 0;
@@ -2448,6 +2469,29 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
     alpha = pq != 0 ? rz / pq : 0.0;
     // x += alpha p, r -= alpha q, z = Minv r; (r.z, r.r)
     double rzn = 0, rrn = 0;
+    if (pair) {  // r first (published), then z from the vertex and its partner
+      for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
+        const d3 xv = ld3nc(x, v) + alpha * ld3nc(p, v);
+        const d3 rv = ld3nc(r, v) - alpha * ld3nc(q, v);
+        x[3 * v] = xv.x;
+        x[3 * v + 1] = xv.y;
+        x[3 * v + 2] = xv.z;
+        r[3 * v] = rv.x;
+        r[3 * v + 1] = rv.y;
+        r[3 * v + 2] = rv.z;
+      }
+      __syncthreads();
+      for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
+        const d3 rv = ld3nc(r, v);
+        const int pp = pair[v];
+        const d3 zv = pair_apply(minv2, v, rv, pp < 0 ? mk3(0, 0, 0) : ld3nc(r, pp));
+        z[3 * v] = zv.x;
+        z[3 * v + 1] = zv.y;
+        z[3 * v + 2] = zv.z;
+        rzn += dot(rv, zv);
+        rrn += dot(rv, rv);
+      }
+    } else {
     for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
       const d3 xv = ld3nc(x, v) + alpha * ld3nc(p, v);
       const d3 rv = ld3nc(r, v) - alpha * ld3nc(q, v);
@@ -2461,6 +2505,7 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
       }
       rzn += dot(rv, zv);
       rrn += dot(rv, rv);
+    }
     }
     cta_sum2(rzn, rrn, sh);
     if (kCoarse) {
@@ -2568,6 +2613,14 @@ int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::v
   T.shift.upload(shift, s);
   k_block_jacobi_seg<<<grid_for(nv, 256), 256, 0, s>>>(nv, M, S.mask_d.p, T.vscene.p, T.shift.p, S.minv.p);
   ++S.launches;
+  // the per-scene CTA PCG smooths with the vertex-pair 6x6 block-Jacobi when
+  // the system has a pairing (every pair lies in one body, so in one scene)
+  const bool pair_smoother = S.has_pairs && S.pair_d.n == (size_t)nv;
+  if (pair_smoother) {
+    S.minv2.resize(18 * (int64_t)nv);
+    k_pair_jacobi<<<grid_for(nv, 128), 128, 0, s>>>(nv, M, S.mask_d.p, S.pair_d.p, S.minv2.p, T.vscene.p, T.shift.p);
+    ++S.launches;
+  }
   int64_t max_rows = 0;
   for (int sc = 0; sc < NS; ++sc) max_rows = std::max(max_rows, S.scene_voff[sc + 1] - S.scene_voff[sc]);
   if (max_rows <= kCtaSceneRows && !std::getenv("GMCP_SEG_PCG")) {  // one CTA per scene
@@ -2579,11 +2632,12 @@ int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::v
       CS = SceneCoarse{C.agg.p, C.dvec.p, C.agg_off.p, C.agg_verts.p, C.scene_agg.p, C.scene_coff.p, C.A.p,
                        C.scale.p};
       k_pcg_scene<true><<<NS, kCtaThreads, 0, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.minv.p, S.grad.p,
-                                                   S.dx.p, S.r.p, S.z.p, S.p.p, S.q.p, tol * tol, maxit, T.st.p, CS);
+                                                   S.dx.p, S.r.p, S.z.p, S.p.p, S.q.p, tol * tol, maxit, T.st.p, CS,
+                                                   pair_smoother ? S.pair_d.p : nullptr, S.minv2.p);
     } else {
       k_pcg_scene<false><<<NS, kCtaThreads, 0, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.minv.p,
                                                     S.grad.p, S.dx.p, S.r.p, S.z.p, S.p.p, S.q.p, tol * tol, maxit,
-                                                    T.st.p, CS);
+                                                    T.st.p, CS, pair_smoother ? S.pair_d.p : nullptr, S.minv2.p);
     }
     ++S.launches;
     std::vector<double> st = T.st.to_host(s);
