@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/gmcp_types.h"
 
 namespace gmcp_b200 {
@@ -117,6 +119,15 @@ struct DBuf {
     std::swap(n, o.n);
     std::swap(cap, o.cap);
   }
+};
+
+// NVTX range over a host stage (K-stages of the pipeline, the solver phases):
+// visible in Nsight Systems / ncu --nvtx; no cost without an attached tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 // ---------------------------------------------------------------------------

@@ -240,6 +240,7 @@ void splice_samples(Ctx& c, const std::vector<int64_t>& soff_old, const std::vec
 }
 
 double run_assembly(Ctx& c, int mode, int64_t* bad) {
+  const NvtxRange nvtx_("gmcp:K6-K8 assembly");
   if (!c.plan.valid) build_assembly_plan(c);
   c.grad.resize(std::max<int64_t>(c.n_dof, 1));
   c.red_d.resize(kRedBlocks + 8);
@@ -275,6 +276,7 @@ __global__ void k_add3(int64_t n, double* __restrict__ dst, const double* __rest
 }
 
 double run_assembly_host(Ctx& c, int mode, const double* x, double* grad, int64_t* bad) {
+  const NvtxRange nvtx_("gmcp:K6-K8 assembly (host buffers)");
   *bad = -1;
   const int64_t n = c.n_dof;
   c.ensure_aux();

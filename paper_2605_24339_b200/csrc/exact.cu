@@ -305,6 +305,7 @@ int grid_for(int64_t n, int threads) {
 }  // namespace
 
 EnergyOut run_energy(Ctx& c, bool need_prefix_min) {
+  const NvtxRange nvtx_("gmcp:K6 energy");
   EnergyOut o{0, 1.7976931348623157e308, 1.7976931348623157e308, -1, -1};
   reset_red(c);
   c.red_d.resize(kRedBlocks + 8);
@@ -342,6 +343,7 @@ EnergyOut run_energy(Ctx& c, bool need_prefix_min) {
 }
 
 void run_pressure(Ctx& c, gmcp_pressure_record* out_host) {
+  const NvtxRange nvtx_("gmcp:pressure field");
   const int64_t nf = (int64_t)c.face_idx.n;
   if (nf == 0) return;
   DBuf<gmcp_pressure_record> out;
@@ -407,6 +409,7 @@ void run_kinematics(Ctx& c, double* g, int32_t* nv, int32_t* ids, double* dg) {
 
 
 double run_step_filter(Ctx& c) {
+  const NvtxRange nvtx_("gmcp:K10 step filter");
   if (c.ns == 0) return 1.0;
   c.red_u.resize(4);
   const unsigned long long init[4] = {ord_bits_host(1.0), ~0ull, ~0ull, 0ull};
@@ -422,6 +425,7 @@ double run_step_filter(Ctx& c) {
 }
 
 double run_displacement_cap(Ctx& c) {
+  const NvtxRange nvtx_("gmcp:K10 displacement cap");
   c.red_u.resize(4);
   const unsigned long long init[4] = {0ull, ~0ull, ~0ull, ord_bits_host(0.0)};
   GMCP_CUDA(cudaMemcpyAsync(c.red_u.p, init, sizeof init, cudaMemcpyHostToDevice, c.stream));

@@ -231,6 +231,7 @@ T last_value(const DBuf<T>& b, int64_t idx, cudaStream_t s) {
 }  // namespace
 
 void build_assembly_plan(Ctx& c) {
+  const NvtxRange nvtx_("gmcp:assembly plan");
   AssemblyPlan& P = c.plan;
   AssemblyPlan::Tmp& T = P.tmp;
   cudaStream_t s = c.stream;

@@ -1248,6 +1248,7 @@ RebuildTmp& rebuild_tmp(Ctx& c) {
 // ===========================================================================
 
 void run_broadphase(Ctx& c, double r, int64_t* counts) {
+  const NvtxRange nvtx_("gmcp:K1-K3 broadphase");
   RebuildTmp& RT = rebuild_tmp(c);
   cudaStream_t s = c.stream;
   // self-contact check (contact_sampling.hpp:286-294), host mirrors are sorted
@@ -1372,6 +1373,7 @@ void run_broadphase(Ctx& c, double r, int64_t* counts) {
 }
 
 int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
+  const NvtxRange nvtx_("gmcp:K4-K5 sampler");
   RebuildTmp& RT = rebuild_tmp(c);
   cudaStream_t s = c.stream;
   const int32_t nst = c.slave.n_tris, nmv = c.master.n_verts;

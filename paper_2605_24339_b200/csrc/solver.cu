@@ -1275,6 +1275,7 @@ double derived_newton_tol(const SystemImpl& S) {
 }
 
 void rebuild_pair(SystemImpl& S, PairRt& pr, const double* eps_ref_dev) {
+  const NvtxRange nvtx_("gmcp:rebuild pair");
   Ctx& c = *pr.c;
   S.u_valid = false;
   int64_t counts[3];
@@ -1324,6 +1325,7 @@ void elastic_terms(SystemImpl& S, double& e_el, double& work) {
 
 // grad = K u + sum contact grads - lambda f ; returns residual (max |grad| free)
 double assemble(SystemImpl& S, double lambda) {
+  const NvtxRange nvtx_("gmcp:assemble");
   std::vector<const double*> gp;
   for (auto& pr : S.pairs) {
     int64_t bad = -1;
@@ -1509,6 +1511,7 @@ void build_coarse(SystemImpl& S, const std::vector<double>& mask) {
 // scaled pseudo-inverse. Pair lists are rebuilt when the pattern changed.
 void coarse_setup_impl(SystemImpl& S, const MatSet& M);
 void coarse_setup(SystemImpl& S, const MatSet& M) {
+  const NvtxRange nvtx_("gmcp:coarse setup");
   static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
   if (!trace) return coarse_setup_impl(S, M);
   const auto t0 = std::chrono::steady_clock::now();
@@ -1582,6 +1585,12 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
   const int nt = n_pad / kGJ;
   double* X = C.A.p;
   double* Y = C.B.p;
+  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+  cudaEvent_t te[3];
+  if (trace) {
+    for (auto& e : te) GMCP_CUDA(cudaEventCreate(&e));
+    GMCP_CUDA(cudaEventRecord(te[0], S.stream));
+  }
   GMCP_CUDA(cudaMemsetAsync(S.redu.p + 4, 0, sizeof(unsigned long long), S.stream));
   C.piv.resize(2 * kGJ * kGJ);
   k_gj_pivot0<<<1, 32, 0, S.stream>>>(n_pad, X, C.piv.p, S.coarse_drop, S.redu.p + 4);
@@ -1591,13 +1600,24 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
                                                   C.piv.p + ((k + 1) & 1) * kGJ * kGJ, S.coarse_drop, S.redu.p + 4);
     ++S.launches;
     std::swap(X, Y);
+    if (trace && k == 0) GMCP_CUDA(cudaEventRecord(te[1], S.stream));
   }
   C.inv = X;
+  if (trace) {
+    GMCP_CUDA(cudaEventRecord(te[2], S.stream));
+    GMCP_CUDA(cudaEventSynchronize(te[2]));
+    float a = 0, b = 0;
+    GMCP_CUDA(cudaEventElapsedTime(&a, te[0], te[1]));
+    GMCP_CUDA(cudaEventElapsedTime(&b, te[1], te[2]));
+    std::fprintf(stderr, "[gmcp] Gauss-Jordan: pivot 0 + step 0 %.3f ms, steps 1..%d %.3f ms\n", a, nt - 1, b);
+    for (auto& e : te) cudaEventDestroy(e);
+  }
 }
 
 // Batched scenes: every scene's coarse operator (its own shift) and its
 // scaled pseudo-inverse, per batched PCG call.
 void coarse_setup_scenes(SystemImpl& S, const MatSet& M, const double* shift_dev) {
+  const NvtxRange nvtx_("gmcp:coarse setup (scenes)");
   CoarseSpace& C = S.cs;
   const Bcsr& A = M.el;
   coarse_pair_lists(S, M);
@@ -1868,6 +1888,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
 constexpr int kMaxRefine = 3;
 constexpr double kRefineMaxDrift = 1e4;  // true / tolerance ratio beyond which the solve counts as failed
 int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.0) {
+  const NvtxRange nvtx_("gmcp:K9 PCG");
   int it = pcg_core(S, tol, maxit, rel_out, shift, S.grad.p);
   if (S.cs.enabled) {  // coarse refresh policy bookkeeping
     S.cs.last_iters = it;
@@ -2603,6 +2624,7 @@ __global__ void __launch_bounds__(kSceneBlk) k_scene_true_resid(MatSet M, const 
 int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::vector<int32_t>& active,
                 const std::vector<double>& shift, std::vector<double>& rel, bool allow_coarse = false,
                 std::vector<int32_t>* bad = nullptr) {
+  const NvtxRange nvtx_("gmcp:K9 PCG (scenes)");
   const int nv = S.nv(), NS = S.n_scenes;
   cudaStream_t s = S.stream;
   MatSet M = mats(S);
