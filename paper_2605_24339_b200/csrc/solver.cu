@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const do
   if (block_reduce_last<1>(dots, rs, out) && threadIdx.x == 0) {
     scal[1] = out[0];                                // pq
     scal[2] = out[0] != 0 ? scal[0] / out[0] : 0.0;  // alpha = rz / pq
+    if (!(out[0] > 0)) scal[8] += 1.0;               // p.Hp <= 0: H not positive definite on p
   }
 }
 
@@ -490,6 +491,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init_pair(int nv, const double
     scal[3] = 0;
     scal[4] = out[1];
     scal[5] = out[1];
+    scal[8] = 0;
   }
 }
 
@@ -521,6 +523,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(int nv, const double* __r
     scal[3] = 0;                     // beta: first direction p = z
     scal[4] = out[1];                // rr
     scal[5] = out[1];                // bb
+    scal[8] = 0;                     // non-positive curvature count
   }
 }
 
@@ -997,6 +1000,7 @@ struct SystemImpl {
   // ||H dx - rhs||_2 / ||rhs||_2 and the inf-norm ratio the reference's acceptance test uses
   double last_true_rel2 = 0, last_true_relinf = 0, true_rel2_max = 0, true_relinf_max = 0;
   int64_t n_linear_solves = 0, refinements = 0;
+  int64_t drift_fails = 0;       // PCG solves failed early on a true/recursive residual gap (pcg_core)
   int64_t coarse_fallbacks = 0;  // batched: scene solves re-run with block-Jacobi after a failed two-level solve
   DBuf<double> rt, xacc;  // true residual vector, accumulated solution (residual replacement)
   // optional host capture of the last linear system (gmcp_system_capture_linear_system)
@@ -1693,6 +1697,9 @@ void true_residual(SystemImpl& S, const MatSet& M) {
 
 // Block-Jacobi PCG on the masked system (chunks of iterations replayed as one
 // CUDA graph) for rhs = -mask .* gsrc. Returns iterations; solution in S.dx.
+constexpr int kDriftWindow = 256;
+constexpr double kDriftFail = 1e6;  // 100x the largest true/tolerance ratio refinement accepts (kRefineMaxDrift)
+
 int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift, const double* gsrc) {
   const int nv = S.nv();
   MatSet M = mats(S);
@@ -1865,6 +1872,22 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
       failed = true;
       break;
     }
+    // a singular system with an inconsistent rhs (a rigid mode before contact
+    // engages) keeps shrinking its recursive residual while the true one
+    // stalls: every kDriftWindow iterations the true residual is recomputed, and a
+    // gap between the two that no refinement can close fails the solve now
+    // (the regularized retry follows) instead of after thousands of iterations
+    if (gsrc == S.grad.p && it % kDriftWindow == 0) {
+      const bool cap = S.capture;
+      S.capture = false;
+      true_residual(S, M);
+      S.capture = cap;
+      if (S.last_true_rel2 - std::sqrt(h[4] / bb) > kDriftFail * tol) {
+        failed = true;
+        ++S.drift_fails;
+        break;
+      }
+    }
     win_min = std::min(win_min, h[4]);
     if (it % stag == 0) {
       if (it >= 2 * stag && !(win_min < 0.5 * prev_min) && h[4] > 1e-8 * bb) break;  // stagnated
@@ -1903,8 +1926,13 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   true_residual(S, M);
   static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
   if (trace)
-    std::fprintf(stderr, "[gmcp] pcg shift %.3e: %d iterations, recursive %.3e, true %.3e (inf %.3e)\n", shift, it,
-                 *rel_out, S.last_true_rel2, S.last_true_relinf);
+  {
+    double npc = 0;
+    GMCP_CUDA(cudaMemcpyAsync(&npc, S.scal.p + 8, sizeof npc, cudaMemcpyDeviceToHost, S.stream));
+    S.sync();
+    std::fprintf(stderr, "[gmcp] pcg shift %.3e: %d iterations, recursive %.3e, true %.3e (inf %.3e), p.Hp<=0 %g, drift fails %lld\n",
+                 shift, it, *rel_out, S.last_true_rel2, S.last_true_relinf, npc, (long long)S.drift_fails);
+  }
   const int n = (int)S.n_dof;
   // refine a drifted residual only; a true residual orders of magnitude above the
   // recursive one means a failed (e.g. singular) solve -> regularized retry
@@ -2396,7 +2424,8 @@ __device__ double scene_coarse(int sc, int v0, int v1, const double* r, double* 
   return sy;
 }
 
-// st[8 s + 0] rz, [1] pq, [2] alpha, [3] beta, [4] rr, [5] bb, [6] iterations
+// st[8 s + 0] rz, [1] pq, [2] alpha, [3] beta, [4] rr, [5] bb, [6] iterations,
+// [7] 1 indefinite / 2 drifted (two-level only; the caller retries regularized)
 template <bool kCoarse>
 __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const double* __restrict__ mask,
                                                           const int64_t* __restrict__ voff,
@@ -2450,6 +2479,7 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
   }
   cta_sum2(rz, rr, sh);
   bool indefinite = false;  // two-level M^-1 lost positivity (r.z <= 0 with r != 0)
+  bool drifted = false;     // true residual stalled far above the recursive one
   if (kCoarse) {  // z += P Ac^+ P^T r, then p = z (own rows)
     rz += scene_coarse(sc, v0, v1, r, z, mask, CS, s_sm, y_sm, sh);
     indefinite = !(rz > 0) && rr > 0;
@@ -2542,6 +2572,34 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
     rr = rrn;
     ++it;
     if (!isfinite(rr)) break;
+    if (kCoarse && it % kDriftWindow == 0) {
+      // true residual ||mask .* (grad + (H + shift) x)|| (x complete: the
+      // update's reductions ended in barriers); a gap to the recursive one that
+      // no refinement closes (a singular scene) fails the solve now -> retry
+      double tr = 0, unused2 = 0;
+      for (int vb = v0 + (threadIdx.x >> 3); vb - (lane >> 3) < v1; vb += kCtaThreads / 8) {
+        const int v = vb;
+        d3 acc = mk3(0, 0, 0);
+        if (v < v1) acc = row_mv8<8>(M.el, v, x, x, 0.0, sub);
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+          acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        }
+        if (sub == 0 && v < v1) {
+          const d3 m = ld3(mask, v), g = ld3(grad, v), xv = ld3nc(x, v);
+          if (shift != 0) acc = acc + shift * xv;
+          const d3 e = mk3(m.x * (acc.x + g.x), m.y * (acc.y + g.y), m.z * (acc.z + g.z));
+          tr += dot(e, e);
+        }
+      }
+      cta_sum2(tr, unused2, sh);
+      if (sqrt(tr / bb) - sqrt(rr / bb) > kDriftFail * sqrt(tol2)) {
+        drifted = true;
+        break;
+      }
+    }
     win_min = fmin(win_min, rr);
     constexpr int stag = kCoarse ? kStagWindowCoarse : kStagWindow;
     if (it % stag == 0) {
@@ -2566,7 +2624,7 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
     o[4] = rr;
     o[5] = bb;
     o[6] = (double)it;
-    o[7] = indefinite ? 1.0 : 0.0;
+    o[7] = indefinite ? 1.0 : drifted ? 2.0 : 0.0;
   }
 }
 
