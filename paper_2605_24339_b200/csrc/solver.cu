@@ -100,6 +100,15 @@ struct MatSet {
   Bcsr c[kMaxPairs];
   int np = 0;
   double shift = 0;  // regularization added to every diagonal entry (solver.hpp:352-356)
+  // symmetric-half copy of el for the PCG SpMV (single systems): the nh
+  // blocks on and above the diagonal, compacted: entries 0-7 of stored block i
+  // at hv[8 i] (two 32-byte loads), entry 8 at hv[8 nh + i]. hix[k] (union
+  // block k) = i of the stored block on/above the diagonal, ~i of the stored
+  // block whose transpose it is (below the diagonal); nh = hn. The SpMV reads
+  // (column, hix) pairs interleaved: hix[2 k] = column, hix[2 k + 1] = index.
+  const int32_t* hix = nullptr;
+  int64_t hn = 0;
+  const double* hv = nullptr;
 };
 
 __device__ __forceinline__ d3 bmv(const double* b, d3 p) {
@@ -157,6 +166,47 @@ __device__ __forceinline__ d3 bmv_ro(const Bcsr& A, int64_t k, d3 p) {
 
 // y_v = sum_j A_vj (z_j + beta p_j) over one row by kRowLanes lanes, two
 // blocks in flight per lane (fixed order: deterministic)
+// block k of the symmetric-half operand times p: H_vj for j >= v, else the
+// transpose of the stored block (j, v)
+__device__ __forceinline__ void ldg4(const double* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ d3 half_bmv(int raw, const double* __restrict__ hv, int64_t nh, d3 p) {
+  const bool lower = raw < 0;
+  const int64_t idx = lower ? ~raw : raw;
+  double b0, u1, u2, u3, b4, u5, u6, u7;
+  ldg4(hv + 8 * idx, b0, u1, u2, u3);
+  ldg4(hv + 8 * idx + 4, b4, u5, u6, u7);
+  const double b8 = __ldg(hv + 8 * nh + idx);
+  const double b1 = lower ? u3 : u1, b3 = lower ? u1 : u3, b2 = lower ? u6 : u2, b6 = lower ? u2 : u6;
+  const double b5 = lower ? u7 : u5, b7 = lower ? u5 : u7;
+  return d3{b0 * p.x + b1 * p.y + b2 * p.z, b3 * p.x + b4 * p.y + b5 * p.z, b6 * p.x + b7 * p.y + b8 * p.z};
+}
+
+// row_mv8 over the symmetric-half operand (MatSet::hv / hix)
+template <int kRowLanes>
+__device__ __forceinline__ d3 row_mv8_half(const Bcsr& A, const int32_t* __restrict__ hix,
+                                           const double* __restrict__ hv, int64_t nh, int v,
+                                           const double* __restrict__ z, const double* __restrict__ p, double beta,
+                                           int sub) {
+  d3 acc0 = mk3(0, 0, 0), acc1 = mk3(0, 0, 0);
+  const int a = __ldg(A.rowptr + v), b = __ldg(A.rowptr + v + 1);
+  const int2* ch = reinterpret_cast<const int2*>(hix);
+  int k = a + sub;
+  for (; k + kRowLanes < b; k += 2 * kRowLanes) {
+    const int2 c0 = __ldg(ch + k), c1 = __ldg(ch + k + kRowLanes);
+    const d3 x0 = ld3(z, c0.x) + beta * ld3(p, c0.x);
+    const d3 x1 = ld3(z, c1.x) + beta * ld3(p, c1.x);
+    acc0 = acc0 + half_bmv(c0.y, hv, nh, x0);
+    acc1 = acc1 + half_bmv(c1.y, hv, nh, x1);
+  }
+  if (k < b) {
+    const int2 c0 = __ldg(ch + k);
+    acc0 = acc0 + half_bmv(c0.y, hv, nh, ld3(z, c0.x) + beta * ld3(p, c0.x));
+  }
+  return acc0 + acc1;
+}
+
 template <int kRowLanes>
 __device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __restrict__ z,
                                       const double* __restrict__ p, double beta, int sub) {
@@ -178,7 +228,7 @@ __device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __rest
 }
 
 // K9a: p_new = z + beta p_old (own rows), q = mask .* (H p_new), pq -> alpha (last block).
-template <int kRowLanes>
+template <int kRowLanes, bool kHalf = false>
 __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const double* __restrict__ mask,
                                                       const double* __restrict__ z, const double* __restrict__ p_old,
                                                       double* __restrict__ p_new, double* __restrict__ q,
@@ -193,8 +243,12 @@ __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const do
     const int v = v0 + (lane / kRowLanes);
     d3 acc = mk3(0, 0, 0);
     if (v < nv) {
-      acc = row_mv8<kRowLanes>(M.el, v, z, p_old, beta, sub);
-      for (int k = 0; k < M.np; ++k) acc = acc + row_mv8<kRowLanes>(M.c[k], v, z, p_old, beta, sub);
+      if (kHalf) {
+        acc = row_mv8_half<kRowLanes>(M.el, M.hix, M.hv, M.hn, v, z, p_old, beta, sub);
+      } else {
+        acc = row_mv8<kRowLanes>(M.el, v, z, p_old, beta, sub);
+        for (int k = 0; k < M.np; ++k) acc = acc + row_mv8<kRowLanes>(M.c[k], v, z, p_old, beta, sub);
+      }
     }
 #pragma unroll
     for (int o = kRowLanes / 2; o > 0; o >>= 1) {
@@ -899,7 +953,8 @@ __global__ void k_motion(int64_t n, const int32_t* __restrict__ verts, const dou
 struct ValPtrs {
   const double* v[1 + kMaxPairs];
 };
-__global__ void k_merge(int64_t nnzb, int ns, const int32_t* __restrict__ src, ValPtrs V, double* __restrict__ out) {
+__global__ void k_merge(int64_t nnzb, int ns, const int32_t* __restrict__ src, ValPtrs V, double* __restrict__ out,
+                        const int32_t* __restrict__ hix, double* __restrict__ hv, int64_t nh) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnzb; k += (int64_t)gridDim.x * blockDim.x) {
     double acc[9];
 #pragma unroll
@@ -914,6 +969,54 @@ __global__ void k_merge(int64_t nnzb, int ns, const int32_t* __restrict__ src, V
     }
 #pragma unroll
     for (int q = 0; q < 9; ++q) out[q * nnzb + k] = acc[q];  // component-major (coalesced SpMV loads)
+    if (hv && hix[2 * k + 1] >= 0) {  // on/above the diagonal: the compact symmetric-half copy
+      const int64_t i = hix[2 * k + 1];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) hv[8 * i + q] = acc[q];
+      hv[8 * nh + i] = acc[8];
+    }
+  }
+}
+
+// Symmetric-half numbering (MatSet::hix). k_half_count: per row, the blocks on
+// and above the diagonal (columns are sorted); after the scan hoff[v] is the
+// compact index of row v's first such block. k_half_index: (column, hix) of
+// every union block; block (v, c), c < v, points at the stored (c, v), found by binary
+// search in row c. A missing mirror (non-symmetric pattern) sets *bad.
+__global__ void k_half_count(int nv, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                             int32_t* __restrict__ cnt) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) c += cols[k] >= v;
+    cnt[v] = c;
+  }
+}
+__global__ void k_half_index(int nv, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                             const int32_t* __restrict__ hoff, int32_t* __restrict__ hix, int* bad) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    int up = hoff[v];
+    for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
+      const int c = cols[k];
+      hix[2 * k] = c;
+      if (c >= v) {
+        hix[2 * k + 1] = up++;
+        continue;
+      }
+      int lo = rowptr[c], hi = rowptr[c + 1];
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cols[mid] < v) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < rowptr[c + 1] && cols[lo] == v) {
+        int before = 0;  // blocks of row c below its diagonal precede the stored ones
+        for (int t = rowptr[c]; t < lo; ++t) before += cols[t] >= c;
+        hix[2 * k + 1] = ~(hoff[c] + before);
+      } else {
+        hix[2 * k + 1] = 0;
+        atomicExch(bad, 1);
+      }
+    }
   }
 }
 
@@ -983,12 +1086,18 @@ struct SystemImpl {
   // pair s-1 matrix, or -1. Pattern rebuilt when a pair is re-sampled.
   DBuf<int32_t> u_rowptr, u_cols, u_src;
   DBuf<double> u_vals;
+  DBuf<int32_t> u_hix, u_hoff;  // symmetric-half PCG operand (MatSet::hix / hv): single systems
+  int64_t u_hn = 0;
+  DBuf<double> u_half;
+  bool u_half_ok = false;
+  bool use_half = true;      // GMCP_HALF_SPMV=0 turns it off
   int64_t u_nnzb = 0;
   bool u_valid = false;
   struct UnionTmp {  // build_union scratch, reused across rebuilds
     DBuf<unsigned long long> keys, keys2, ukeys;
     DBuf<int64_t> vals, vals2;
     DBuf<int32_t> ucnt, uoff, nuniq, rowcnt;
+    DBuf<int> bad;
   } utmp;
   DBuf<const double*> gc_ptrs;
   bool el_built = false;
@@ -1171,6 +1280,11 @@ MatSet mats(SystemImpl& S) {
   }
   M.el = Bcsr{S.u_rowptr.p, S.u_cols.p, S.u_vals.p, 1, S.u_nnzb};
   M.np = 0;
+  if (S.u_half_ok) {
+    M.hix = S.u_hix.p;
+    M.hv = S.u_half.p;
+    M.hn = S.u_hn;
+  }
   return M;
 }
 
@@ -1257,6 +1371,27 @@ void build_union(SystemImpl& S) {
   S.u_rowptr.resize(nv + 1);
   exclusive_scan(rowcnt.p, S.u_rowptr.p, (int64_t)nv + 1, S.stream);
   S.u_vals.resize(std::max<int64_t>(9 * S.u_nnzb, 1));
+  S.u_half_ok = false;
+  if (S.use_half && S.n_scenes == 1 && nu > 0) {
+    S.u_hix.resize(2 * (int64_t)nu);
+    S.u_hoff.resize(nv + 1);
+    DBuf<int>& bad = T.bad;
+    bad.resize(1);
+    bad.zero(S.stream);
+    rowcnt.zero(S.stream);
+    k_half_count<<<grid_for(nv, 128), 128, 0, S.stream>>>(nv, S.u_rowptr.p, S.u_cols.p, rowcnt.p);
+    exclusive_scan(rowcnt.p, S.u_hoff.p, (int64_t)nv + 1, S.stream);
+    k_half_index<<<grid_for(nv, 128), 128, 0, S.stream>>>(nv, S.u_rowptr.p, S.u_cols.p, S.u_hoff.p, S.u_hix.p,
+                                                         bad.p);
+    S.launches += 2;
+    int hb = 0, hn = 0;
+    GMCP_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof hb, cudaMemcpyDeviceToHost, S.stream));
+    GMCP_CUDA(cudaMemcpyAsync(&hn, S.u_hoff.p + nv, sizeof hn, cudaMemcpyDeviceToHost, S.stream));
+    S.sync();
+    S.u_hn = hn;
+    S.u_half.resize(9 * (int64_t)hn);
+    S.u_half_ok = hb == 0;
+  }
   S.sync();
   S.u_valid = true;
   ++S.u_gen;
@@ -1342,7 +1477,8 @@ double assemble(SystemImpl& S, double lambda) {
     V.v[0] = S.k_vals.p;
     for (size_t p = 0; p < S.pairs.size(); ++p) V.v[1 + p] = S.pairs[p]->c->plan.vals.p;
     k_merge<<<grid_for(S.u_nnzb, 256), 256, 0, S.stream>>>(S.u_nnzb, 1 + (int)S.pairs.size(), S.u_src.p, V,
-                                                            S.u_vals.p);
+                                                            S.u_vals.p, S.u_half_ok ? S.u_hix.p : nullptr,
+                                                            S.u_half_ok ? S.u_half.p : nullptr, S.u_hn);
     ++S.launches;
   }
   S.gc_ptrs.resize(std::max<size_t>(gp.size(), 1));
@@ -1794,7 +1930,9 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     return a.rowptr == b.rowptr && a.cols == b.cols && a.vals == b.vals && a.bs == b.bs && a.cs == b.cs;
   };
   auto same_key = [&](const SystemImpl::PcgKey& a, const SystemImpl::PcgKey& b) {
-    if (!same_bcsr(a.M.el, b.M.el) || a.M.np != b.M.np || a.M.shift != b.M.shift) return false;
+    if (!same_bcsr(a.M.el, b.M.el) || a.M.np != b.M.np || a.M.shift != b.M.shift || a.M.hix != b.M.hix ||
+        a.M.hv != b.M.hv || a.M.hn != b.M.hn)
+      return false;
     for (int k = 0; k < a.M.np; ++k)
       if (!same_bcsr(a.M.c[k], b.M.c[k])) return false;
     return a.nv == b.nv && a.lanes == b.lanes && a.gsp == b.gsp && a.gup == b.gup &&
@@ -1808,9 +1946,16 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     for (int k = 0; k < chunk; ++k) {  // p ping-pongs between S.p and S.w (chunk is even)
       double* p_old = (k & 1) ? S.w.p : S.p.p;
       double* p_new = (k & 1) ? S.p.p : S.w.p;
-      if (lanes == 8)
+      const bool half = M.hv != nullptr && M.np == 0;
+      if (lanes == 8 && half)
+        k_spmv_cg<8, true><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
+                                                            S.slot(1));
+      else if (lanes == 8)
         k_spmv_cg<8><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
                                                       S.slot(1));
+      else if (half)
+        k_spmv_cg<4, true><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
+                                                            S.slot(1));
       else
         k_spmv_cg<4><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
                                                       S.slot(1));
@@ -3480,6 +3625,7 @@ int gmcp_system_create(int device, gmcp_system** out) {
     const DeviceBind bind_(device, &s->s.cub);
     GMCP_CUDA(cudaStreamCreateWithFlags(&s->s.stream, cudaStreamNonBlocking));
     if (const char* e = std::getenv("GMCP_PAIR_JACOBI")) s->s.use_pair = std::atoi(e) != 0;
+    if (const char* e = std::getenv("GMCP_HALF_SPMV")) s->s.use_half = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE")) s->s.use_coarse = std::atoi(e) != 0;
     if (const char* e = std::getenv("GMCP_COARSE_AGGS")) s->s.coarse_aggs = std::min(512, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("GMCP_COARSE_REFRESH")) s->s.coarse_refresh_always = std::atoi(e) != 0;
