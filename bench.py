@@ -134,9 +134,11 @@ def pcg_roofline(ps: dict, pre: dict | None = None) -> dict:
     """HBM roofline of one PCG iteration, device time from CUDA events around
     the chunk graphs of every PCG solve in the timed Newton run. Algorithmic
     bytes per iteration:
-      SpMV    76 B per 3x3 block of the merged operand (72 B values + 4 B column)
-              + per row 4 B row pointer and 24 B each of z, p_old, mask read and
-              p_new, q written (124 B);
+      SpMV    the symmetric-half operand: 72 B per stored block (on or above
+              the diagonal) + 8 B (column, stored index) per block of the merged
+              pattern (76 B per block when the full BCSR is read) + per row 4 B
+              row pointer and 24 B each of z, p_old, mask read and p_new, q
+              written (124 B);
       update  24 B each of p, q, x, r read and x, r, z written (168 B), the
               vertex-pair block-Jacobi rows (3x6 = 144 B) + 4 B pair index
               (316 B/row; the partner's r and q rows are L2 hits of rows another
@@ -149,16 +151,19 @@ def pcg_roofline(ps: dict, pre: dict | None = None) -> dict:
         return None
     peak, src = peaks()
     row = 124 + (316 if (pre is None or pre["pair_jacobi"]) else 168 + 72)
+    half = ps.get("stored_blocks", 0) > 0
     coarse = bool(pre and pre["coarse"])
     if coarse:
         row += 52 + 100
-    per_iter = 76 * ps["nnzb"] + row * ps["rows"] + (8 * pre["coarse_padded"] ** 2 if coarse else 0)
+    mat = 72 * ps["stored_blocks"] + 8 * ps["nnzb"] if half else 76 * ps["nnzb"]
+    per_iter = mat + row * ps["rows"] + (8 * pre["coarse_padded"] ** 2 if coarse else 0)
     ms = ps["ms"] / ps["iters"]
     achieved = per_iter / (ms / 1e3) / 1e9
     kern = "k_spmv_cg + k_update_agg + k_coarse_prolong" if coarse else "k_spmv_cg + k_update_cg_pair"
     return {"bound": "hbm", "kernels": kern + " (one PCG iteration)", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "algorithmic_bytes": per_iter,
             "us_per_iter": 1e3 * ms, "iters_timed": ps["iters"], "operand_blocks": ps["nnzb"], "rows": ps["rows"],
+            "stored_blocks": ps.get("stored_blocks", 0),
             "preconditioner": pre, "peak_source": src,
             "clock": "CUDA events around each 16-iteration chunk graph on the solve stream"}
 
@@ -456,6 +461,7 @@ def main():
             dist.barrier()
         ms_it, pcg_it = nsys.time_newton(settings, args.newton_iters + 1)
         ps = nsys.pcg_stats()
+        ps.update(nsys.operand_info())
         pre = nsys.precond_info()
         lin = nsys.linear_stats()
         steady = ms_it[1:] if ms_it.size > 1 else ms_it

@@ -83,6 +83,10 @@ int gmcp_system_pcg_stats(const gmcp_system* sys, double* ev_ms, int64_t* ev_ite
  * GMCP_COARSE_AGGS; both default on). */
 int gmcp_system_precond_info(gmcp_system* sys, int32_t* pair_jacobi, int32_t* coarse, int32_t* n_aggregates,
                              int32_t* n_coarse_padded);
+/* PCG operand storage: *stored_blocks = 3x3 blocks the SpMV streams from the
+ * symmetric-half copy (blocks on and above the diagonal, once each; 0 when
+ * the SpMV reads the full merged BCSR: batched scenes, GMCP_HALF_SPMV=0). */
+int gmcp_system_operand_info(gmcp_system* sys, int64_t* stored_blocks);
 int gmcp_system_positions(gmcp_system* sys, double* x, int64_t n_dof);
 int gmcp_system_set_positions(gmcp_system* sys, const double* x, int64_t n_dof);
 int64_t gmcp_system_num_samples(gmcp_system* sys, int32_t pair);

@@ -3931,6 +3931,14 @@ int gmcp_system_precond_info(gmcp_system* sys, int32_t* pair_jacobi, int32_t* co
   });
 }
 
+int gmcp_system_operand_info(gmcp_system* sys, int64_t* stored_blocks) {
+  return sguard(sys, [&] {
+    const SystemImpl& S = sys->s;
+    *stored_blocks = S.u_half_ok ? S.u_hn : 0;
+    return GMCP_OK;
+  });
+}
+
 int gmcp_system_scene_step_stats(gmcp_system* sys, int32_t* n_steps, gmcp_step_stats* out) {
   return sguard(sys, [&] {
     const SystemImpl& S = sys->s;

@@ -300,6 +300,13 @@ class System:
         _check(self.L, self.L.gmcp_system_precond_info(self.h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
         return {"pair_jacobi": bool(a.value), "coarse": bool(b.value), "aggregates": c.value, "coarse_padded": d.value}
 
+    def operand_info(self) -> dict:
+        """Blocks the PCG SpMV streams from the symmetric-half operand copy
+        (0: it reads the full merged BCSR)."""
+        n = C.c_int64()
+        _check(self.L, self.L.gmcp_system_operand_info(self.h, C.byref(n)))
+        return {"half": n.value > 0, "stored_blocks": n.value}
+
     def linear_stats(self, reset: bool = False) -> dict:
         """Recomputed true residuals of the linear solves since the last reset:
         max ||H dx - rhs||_2/||rhs||_2, max inf-norm ratio (the reference's
