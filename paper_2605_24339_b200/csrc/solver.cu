@@ -1736,7 +1736,7 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
   k_gj_pivot0<<<1, 32, 0, S.stream>>>(n_pad, X, C.piv.p, S.coarse_drop, S.redu.p + 4);
   ++S.launches;
   for (int k = 0; k < nt; ++k) {
-    k_gj_step<<<dim3(nt, nt), 256, 0, S.stream>>>(n_pad, k, X, Y, C.piv.p + (k & 1) * kGJ * kGJ,
+    k_gj_step<<<dim3(nt, nt), kGJThreads, 0, S.stream>>>(n_pad, k, X, Y, C.piv.p + (k & 1) * kGJ * kGJ,
                                                   C.piv.p + ((k + 1) & 1) * kGJ * kGJ, S.coarse_drop, S.redu.p + 4);
     ++S.launches;
     std::swap(X, Y);
@@ -1849,13 +1849,13 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     // inverses with iteration counts within 15% (the contact Hessian settled)
     const bool steady = C.prev_fresh_iters > 0 && C.ref_iters > 0 &&
                         std::abs(C.ref_iters - C.prev_fresh_iters) <= 0.15 * C.prev_fresh_iters;
-    const bool stale = !C.have_inv || C.inv_step != S.load_step || C.inv_gen != gen || C.inv_shift != M.shift ||
-                       S.coarse_refresh_always || !steady ||
-                       (C.ref_iters > 0 && C.last_iters > kCoarseStale * C.ref_iters);
-    if (stale) {
-      const bool same_context = C.have_inv && C.inv_step == S.load_step && C.inv_gen == gen && C.inv_shift == M.shift;
-      C.prev_fresh_iters = same_context ? C.ref_iters : -1;
-    }
+    const bool same_context = C.have_inv && C.inv_step == S.load_step && C.inv_gen == gen && C.inv_shift == M.shift;
+    // a refinement pass (rhs = the true residual) solves with the operator of
+    // the solve it refines: that solve's coarse inverse is current
+    const bool refining = gsrc != S.grad.p && same_context;
+    const bool stale = !refining && (!same_context || S.coarse_refresh_always || !steady ||
+                                     (C.ref_iters > 0 && C.last_iters > kCoarseStale * C.ref_iters));
+    if (stale) C.prev_fresh_iters = same_context ? C.ref_iters : -1;
     if (stale) {
       coarse_setup(S, M);
       C.have_inv = true;
