@@ -14,15 +14,18 @@ ncu --set full --clock-control none --import-source on -k regex:k_run_partials -
 ncu --set full --clock-control none --import-source on -k regex:k_gather -s 2 -c 1 -o $O/k8 \
     python tools/k7_time.py > /dev/null 2>&1
 # the PCG kernels inside the C3 Newton solve (steady iteration: skip the first solves)
-ncu --set full --clock-control none --import-source on -k regex:k_spmv_cg -s 2600 -c 1 -o $O/spmv \
+ncu --set full --clock-control none --import-source on -k regex:k_spmv_cg -s 600 -c 1 -o $O/spmv \
     python tools/newton_c3.py 3 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_update_agg -s 2600 -c 1 -o $O/update_agg \
+ncu --set full --clock-control none --import-source on -k regex:k_update_agg -s 600 -c 1 -o $O/update_agg \
     python tools/newton_c3.py 3 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_coarse_prolong -s 2600 -c 1 -o $O/coarse_prolong \
+ncu --set full --clock-control none --import-source on -k regex:k_coarse_prolong -s 600 -c 1 -o $O/coarse_prolong \
     python tools/newton_c3.py 3 > /dev/null 2>&1
 # per-launch durations of one steady PCG stretch
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"k_spmv_cg|k_update_agg|k_coarse_prolong" -s 3000 -c 60 --csv --log-file $O/pcg_launches.csv \
+    -k regex:"k_spmv_cg|k_update_agg|k_coarse_prolong" -s 1800 -c 60 --csv --log-file $O/pcg_launches.csv \
+    python tools/newton_c3.py 3 > /dev/null 2>&1
+# one blocked Gauss-Jordan step of the coarse inverse (704 coarse dofs)
+ncu --set full --clock-control none --import-source on -k regex:k_gj_step -s 40 -c 1 -o $O/gj_step \
     python tools/newton_c3.py 3 > /dev/null 2>&1
 # the per-scene CTA PCG (C5, two-level) and the per-scene coarse inverse
 ncu --set full --clock-control none -k regex:k_pcg_scene -s 4 -c 1 -o $O/pcg_scene python tools/c5_newton.py 1024 4 \
