@@ -823,8 +823,12 @@ template <int Mode>
 __global__ void __launch_bounds__(128) k_sample(SamplerArgs A, int64_t ntask, const int32_t* __restrict__ task_st,
                                                 const int32_t* __restrict__ task_feat,
                                                 const int8_t* __restrict__ task_kind, int64_t* __restrict__ cnt,
-                                                const int64_t* __restrict__ off, Out O, unsigned long long* err) {
-  GRID_LOOP(t, ntask) {
+                                                const int64_t* __restrict__ off, Out O, unsigned long long* err,
+                                                const int32_t* __restrict__ task_ord = nullptr) {
+  GRID_LOOP(it, ntask) {
+    // single pass: tasks visited grouped by kind (faces, edges, points), so a
+    // warp runs one branch; records are keyed by the task's reference index t
+    const int64_t t = task_ord ? (int64_t)task_ord[it] : it;
     const int st = task_st[t];
     const int kind = task_kind[t];
     const int feat = task_feat[t];
@@ -974,23 +978,28 @@ __global__ void __launch_bounds__(128) k_sample(SamplerArgs A, int64_t ntask, co
 __global__ void k_tasks(int32_t nst, const int64_t* __restrict__ toff, const int32_t* __restrict__ tids,
                         const int64_t* __restrict__ eoff, const int32_t* __restrict__ eids,
                         const int64_t* __restrict__ poff, const int32_t* __restrict__ pids,
-                        int32_t* __restrict__ task_st, int32_t* __restrict__ task_feat, int8_t* __restrict__ task_kind) {
+                        int32_t* __restrict__ task_st, int32_t* __restrict__ task_feat, int8_t* __restrict__ task_kind,
+                        int32_t* __restrict__ task_ord) {
+  const int64_t nf = toff[nst], ne = eoff[nst];  // kind-grouped order: faces, edges, points
   GRID_LOOP(st, nst) {
     int64_t o = toff[st] + eoff[st] + poff[st];
     for (int64_t i = toff[st]; i < toff[st + 1]; ++i, ++o) {
       task_st[o] = (int32_t)st;
       task_feat[o] = tids[i];
       task_kind[o] = kFace;
+      task_ord[i] = (int32_t)o;
     }
     for (int64_t i = eoff[st]; i < eoff[st + 1]; ++i, ++o) {
       task_st[o] = (int32_t)st;
       task_feat[o] = eids[i];
       task_kind[o] = kEdge;
+      task_ord[nf + i] = (int32_t)o;
     }
     for (int64_t i = poff[st]; i < poff[st + 1]; ++i, ++o) {
       task_st[o] = (int32_t)st;
       task_feat[o] = pids[i];
       task_kind[o] = kPoint;
+      task_ord[nf + ne + i] = (int32_t)o;
     }
   }
 }
@@ -1226,7 +1235,7 @@ struct RebuildTmp : TmpBase {
   DBuf<unsigned long long> k1, k2;
   DBuf<int64_t> by_off, pcnt, poff, pt_off;
   DBuf<int32_t> by_st, pt_ids;
-  DBuf<int32_t> task_st, task_feat;
+  DBuf<int32_t> task_st, task_feat, task_ord;
   DBuf<int8_t> task_kind;
   DBuf<int64_t> tcnt, toff;
   struct Stage {
@@ -1445,11 +1454,13 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
   task_st.resize(std::max<int64_t>(ntask, 1));
   task_feat.resize(std::max<int64_t>(ntask, 1));
   task_kind.resize(std::max<int64_t>(ntask, 1));
+  RT.task_ord.resize(std::max<int64_t>(ntask, 1));
+  static const bool kind_order = !std::getenv("GMCP_SAMPLER_TASK_ORDER") || std::atoi(std::getenv("GMCP_SAMPLER_TASK_ORDER")) != 0;
   Out O{};
   if (ntask) {
     k_tasks<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.pair_off[1].p,
                                                 c.pair_ids[1].p, pt_off.p, pt_ids.p, task_st.p, task_feat.p,
-                                                task_kind.p);
+                                                task_kind.p, RT.task_ord.p);
     ++c.launches;
   }
   if (ntask >= (int64_t)1 << 27) throw StatusError(GMCP_ERR_CONFIG, "sampler: too many (slave tri, feature) tasks");
@@ -1485,7 +1496,7 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
     sctr.zero(s);
     if (ntask) {
       k_sample<2><<<grid_for(ntask, 128), 128, 0, s>>>(A, ntask, task_st.p, task_feat.p, task_kind.p, nullptr,
-                                                        nullptr, SO, err.p);
+                                                        nullptr, SO, err.p, kind_order ? RT.task_ord.p : nullptr);
       ++c.launches;
     }
     GMCP_CUDA(cudaMemcpyAsync(&cnt_h, sctr.p, sizeof cnt_h, cudaMemcpyDeviceToHost, s));
