@@ -83,6 +83,23 @@ int gmcp_system_pcg_stats(const gmcp_system* sys, double* ev_ms, int64_t* ev_ite
  * GMCP_COARSE_AGGS; both default on). */
 int gmcp_system_precond_info(gmcp_system* sys, int32_t* pair_jacobi, int32_t* coarse, int32_t* n_aggregates,
                              int32_t* n_coarse_padded);
+/* Standalone Newton linear solve: replaces solve_descent (solver.hpp:325-375)
+ * under the reference's own CPU System. The matrix is an AoS BCSR of 3x3
+ * blocks over n_vertices (rowptr[n_vertices + 1], ascending columns per row,
+ * vals[9 nnzb] row-major blocks): H = the assembled elastic + contact Hessian
+ * over all dofs; fixed[3 n_vertices] (or NULL) marks Dirichlet dofs, which are
+ * eliminated as P H P + I - P with the rhs masked (solver.hpp:271-277, 331-341).
+ * positions[3 n_vertices] (or NULL) enable the two-level preconditioner's
+ * geometric aggregates. Solves H dx = rhs with the device PCG to pcg_tol and
+ * accepts as the reference accepts its LDL^T solve (||H dx - rhs||_inf <= 1e-6
+ * ||rhs||_inf); otherwise retries with the diagonal shifted by 1e-8 x the mean
+ * free diagonal entry (*regularized = 1), and returns GMCP_ERR_SOLVER if that
+ * fails too (the reference's SolverError). Use a system handle with no bodies
+ * and no contact pairs. */
+int gmcp_system_linear_solve(gmcp_system* sys, int64_t n_vertices, const int32_t* rowptr, const int32_t* cols,
+                             const double* vals, const uint8_t* fixed, const double* positions, const double* rhs,
+                             double pcg_tol, int32_t max_iters, double* dx, int32_t* iterations,
+                             double* residual_inf_rel, int32_t* regularized);
 /* PCG operand storage: *stored_blocks = 3x3 blocks the SpMV streams from the
  * symmetric-half copy (blocks on and above the diagonal, once each; 0 when
  * the SpMV reads the full merged BCSR: batched scenes, GMCP_HALF_SPMV=0). */

@@ -1191,6 +1191,45 @@ void build_operators(Body& b) {
 }
 
 // Constant elastic BCSR (elasticity.hpp:124-141), blocks summed in tet order.
+// Vertex pairs of the 6x6 block-Jacobi (single systems and the per-scene CTA
+// PCG) from an AoS BCSR of the operand's constant part: greedy matching of the
+// strongest normalized couplings |K_vw|_F^2 / (|K_vv|_F |K_ww|_F) (ties by index).
+void build_pairing(SystemImpl& S, const std::vector<int32_t>& rowptr, const std::vector<int32_t>& cols,
+                   const std::vector<double>& vals) {
+  const int nv = (int)rowptr.size() - 1;
+#if GMCP_PAIR_JACOBI
+  S.has_pairs = false;
+  if (S.use_pair) {
+    std::vector<double> dn(nv, 0.0);
+    for (int v = 0; v < nv; ++v)
+      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k)
+        if (cols[k] == v)
+          for (int q = 0; q < 9; ++q) dn[v] += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
+    struct Edge { double s; int32_t a, b; };
+    std::vector<Edge> edges;
+    for (int v = 0; v < nv; ++v)
+      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
+        const int w = cols[k];
+        if (w <= v || !(dn[v] > 0) || !(dn[w] > 0)) continue;
+        double f = 0;
+        for (int q = 0; q < 9; ++q) f += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
+        edges.push_back({f / std::sqrt(dn[v] * dn[w]), v, w});
+      }
+    std::stable_sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) { return x.s > y.s; });
+    std::vector<int32_t> mate(nv, -1);
+    for (const Edge& e : edges)
+      if (mate[e.a] < 0 && mate[e.b] < 0) {
+        mate[e.a] = e.b;
+        mate[e.b] = e.a;
+      }
+    S.pair_d.upload(mate, S.stream);
+    S.has_pairs = true;
+  }
+#else
+  S.has_pairs = false;
+#endif
+}
+
 void build_elastic(SystemImpl& S) {
   const int nv = S.nv();
   std::vector<std::vector<std::pair<int32_t, std::array<double, 9>>>> rows(nv);
@@ -1233,36 +1272,7 @@ void build_elastic(SystemImpl& S) {
   S.k_cols.upload(cols, S.stream);
   S.k_vals.upload(vals, S.stream);
   S.el_nnzb = (int64_t)cols.size();
-#if GMCP_PAIR_JACOBI
-  S.has_pairs = false;
-  if (S.use_pair) {  // vertex pairs for the 6x6 block-Jacobi (single systems and the per-scene CTA PCG): greedy matching of the strongest
-     // normalized elastic couplings |K_vw|_F^2 / (|K_vv|_F |K_ww|_F) (ties by index)
-    std::vector<double> dn(nv, 0.0);
-    for (int v = 0; v < nv; ++v)
-      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k)
-        if (cols[k] == v)
-          for (int q = 0; q < 9; ++q) dn[v] += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
-    struct Edge { double s; int32_t a, b; };
-    std::vector<Edge> edges;
-    for (int v = 0; v < nv; ++v)
-      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
-        const int w = cols[k];
-        if (w <= v || !(dn[v] > 0) || !(dn[w] > 0)) continue;
-        double f = 0;
-        for (int q = 0; q < 9; ++q) f += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
-        edges.push_back({f / std::sqrt(dn[v] * dn[w]), v, w});
-      }
-    std::stable_sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) { return x.s > y.s; });
-    std::vector<int32_t> mate(nv, -1);
-    for (const Edge& e : edges)
-      if (mate[e.a] < 0 && mate[e.b] < 0) {
-        mate[e.a] = e.b;
-        mate[e.b] = e.a;
-      }
-    S.pair_d.upload(mate, S.stream);
-    S.has_pairs = true;
-  }
-#endif
+  build_pairing(S, rowptr, cols, vals);
   S.el_built = true;
 }
 
@@ -3566,6 +3576,113 @@ void system_solve(SystemImpl& S, const gmcp_solver_settings& st, gmcp_step_callb
   out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
 }
 
+// Standalone linear solve (gmcp_system_linear_solve): the reference's
+// solve_descent (solver.hpp:325-375) on a caller-given Newton matrix. The
+// caller's AoS BCSR is the operand (Dirichlet dofs masked: P H P + I - P, rhs
+// masked), the smoother pairs come from its values, and the two-level space
+// from optional positions (one body). The ladder is the Newton loop's:
+// PCG; if not accepted (converged and ||H dx - rhs||_inf <= 1e-6 ||rhs||_inf,
+// solver.hpp:349-356), regularized by 1e-8 x the mean free diagonal entry
+// (solver.hpp:352-361); last, regularized with the smoother alone.
+struct LinearSolveOut {
+  int32_t iterations = 0, regularized = 0;
+  double relinf = 0;
+};
+LinearSolveOut linear_solve(SystemImpl& S, int64_t nv, const int32_t* rowptr, const int32_t* cols, const double* vals,
+                            const uint8_t* fixed, const double* positions, const double* rhs, double tol, int maxit,
+                            double* dx) {
+  if (!S.bodies.empty() || !S.pairs.empty())
+    throw StatusError(GMCP_ERR_CONFIG, "linear_solve: use a system handle without bodies or contact pairs");
+  if (nv <= 0 || !rowptr || !cols || !vals || !rhs || !dx) throw StatusError(GMCP_ERR_ARG, "linear_solve: null input");
+  if (!(tol > 0) || maxit < 1) throw StatusError(GMCP_ERR_ARG, "linear_solve: tol > 0 and max_iters >= 1");
+  const int64_t n = 3 * nv, nnzb = rowptr[nv];
+  if (rowptr[0] != 0 || nnzb < 0) throw StatusError(GMCP_ERR_ARG, "linear_solve: bad row pointers");
+  for (int64_t v = 0; v < nv; ++v) {
+    if (rowptr[v + 1] < rowptr[v]) throw StatusError(GMCP_ERR_ARG, "linear_solve: bad row pointers");
+    for (int32_t k = rowptr[v]; k < rowptr[v + 1]; ++k)
+      if (cols[k] < 0 || cols[k] >= nv || (k > rowptr[v] && cols[k] <= cols[k - 1]))
+        throw StatusError(GMCP_ERR_ARG, "linear_solve: columns must be in range and ascending per row");
+  }
+  std::vector<int32_t> rp(rowptr, rowptr + nv + 1), cl(cols, cols + nnzb);
+  std::vector<double> vl(vals, vals + 9 * nnzb);
+  S.n_dof = n;
+  S.k_rowptr.upload(rp, S.stream);
+  S.k_cols.upload(cl, S.stream);
+  S.k_vals.upload(vl, S.stream);
+  S.el_nnzb = nnzb;
+  S.el_built = true;
+  build_pairing(S, rp, cl, vl);
+  S.fixed.assign(n, 0);
+  int64_t n_free = 0;
+  std::vector<double> mask(n);
+  for (int64_t d = 0; d < n; ++d) {
+    S.fixed[d] = fixed ? (fixed[d] ? 1 : 0) : 0;
+    mask[d] = S.fixed[d] ? 0.0 : 1.0;
+    n_free += S.fixed[d] == 0;
+  }
+  if (n_free == 0) throw StatusError(GMCP_ERR_CONFIG, "linear_solve: no free degrees of freedom");
+  for (auto* b : {&S.x, &S.dx, &S.grad, &S.r, &S.z, &S.p, &S.q, &S.w, &S.rt, &S.xacc}) b->resize(n);
+  S.minv.resize(3 * n);
+  S.scal.resize(16);
+  S.parts.resize(kBlocks * 4);
+  S.counter.resize(16);
+  S.counter.zero(S.stream);
+  S.redu.resize(8);
+  S.mask_d.upload(mask, S.stream);
+  std::vector<double> g(n);
+  for (int64_t d = 0; d < n; ++d) g[d] = -rhs[d];  // PCG's rhs is -mask .* grad
+  S.grad.upload(g, S.stream);
+  if (S.pcg_exec) {
+    cudaGraphExecDestroy(S.pcg_exec);
+    S.pcg_exec = nullptr;
+  }
+  S.cs.enabled = false;
+  if (positions) {  // the two-level space over one body spanning every vertex
+    Body b;
+    b.verts.assign(positions, positions + n);
+    b.offset = 0;
+    b.nv = (int32_t)nv;
+    S.bodies.push_back(std::move(b));
+    S.rest.assign(positions, positions + n);  // aggregate centroids and offsets
+    try {
+      build_coarse(S, mask);
+    } catch (...) {
+      S.bodies.clear();
+      S.rest.clear();
+      throw;
+    }
+    S.bodies.clear();
+    S.rest.clear();
+  }
+  S.cs.have_inv = false;
+  S.load_step += 1;  // a fresh coarse inverse for this operand
+  LinearSolveOut out;
+  double rel = 0;
+  out.iterations = pcg(S, tol, maxit, &rel);
+  if (!(rel <= tol) || !(S.last_true_relinf <= kAcceptRelInf)) {
+    k_diag_sum<<<kBlocks, kThreads, 0, S.stream>>>(S.nv(), mats(S), S.mask_d.p, S.scal.p + 10, S.slot(4));
+    double dsum = 0;
+    GMCP_CUDA(cudaMemcpyAsync(&dsum, S.scal.p + 10, sizeof dsum, cudaMemcpyDeviceToHost, S.stream));
+    S.sync();
+    const double shift = kRegularization * dsum / (double)n_free;
+    out.regularized = 1;
+    out.iterations += pcg(S, tol, maxit, &rel, shift);
+    if ((!(rel <= tol) || !(S.last_true_relinf <= kAcceptRelInf)) && S.cs.enabled) {
+      S.cs.enabled = false;
+      out.iterations += pcg(S, tol, maxit, &rel, shift);
+      S.cs.enabled = true;
+    }
+    if (!(rel <= tol) || !(S.last_true_relinf <= kAcceptRelInf))
+      throw StatusError(GMCP_ERR_SOLVER, "linear solve failed even with regularization; the system is insufficiently "
+                                         "constrained (unfixed rigid body modes?)");
+  }
+  record_accepted_solve(S);
+  out.relinf = S.last_true_relinf;
+  GMCP_CUDA(cudaMemcpyAsync(dx, S.dx.p, n * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
+  S.sync();
+  return out;
+}
+
 }  // namespace gmcp_b200
 
 // ===========================================================================
@@ -3927,6 +4044,21 @@ int gmcp_system_precond_info(gmcp_system* sys, int32_t* pair_jacobi, int32_t* co
     *coarse = S.cs.enabled ? 1 : 0;
     *n_aggregates = S.cs.enabled ? S.cs.n_agg : 0;
     *n_coarse_padded = S.cs.enabled ? S.cs.n_pad : 0;
+    return GMCP_OK;
+  });
+}
+
+int gmcp_system_linear_solve(gmcp_system* sys, int64_t n_vertices, const int32_t* rowptr, const int32_t* cols,
+                             const double* vals, const uint8_t* fixed, const double* positions, const double* rhs,
+                             double pcg_tol, int32_t max_iters, double* dx, int32_t* iterations,
+                             double* residual_inf_rel, int32_t* regularized) {
+  return sguard(sys, [&] {
+    if (!sys) throw StatusError(GMCP_ERR_ARG, "null system");
+    const LinearSolveOut o = linear_solve(sys->s, n_vertices, rowptr, cols, vals, fixed, positions, rhs, pcg_tol,
+                                          max_iters, dx);
+    if (iterations) *iterations = o.iterations;
+    if (residual_inf_rel) *residual_inf_rel = o.relinf;
+    if (regularized) *regularized = o.regularized;
     return GMCP_OK;
   });
 }

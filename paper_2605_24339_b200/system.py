@@ -359,6 +359,48 @@ class System:
 # ---------------------------------------------------------------------------
 # elasticity helpers (elasticity.hpp:20-61, 147-160; bench.hpp:18-25)
 
+@dataclass
+class LinearSolveResult:
+    dx: np.ndarray
+    iterations: int
+    residual_inf_rel: float  # ||H dx - rhs||_inf / ||rhs||_inf (the reference's acceptance test)
+    regularized: bool        # accepted only after the 1e-8 diagonal shift (solver.hpp:352-361)
+
+
+def solve_descent(rowptr: np.ndarray, cols: np.ndarray, vals: np.ndarray, rhs: np.ndarray,
+                  fixed: np.ndarray | None = None, positions: np.ndarray | None = None, pcg_tol: float = 1e-10,
+                  max_iters: int = 20000, device: int = 0) -> LinearSolveResult:
+    """The reference's System::solve_descent (solver.hpp:325-375) on the GPU for
+    a caller-assembled Newton matrix: H as an AoS BCSR of 3x3 blocks (rowptr
+    [n+1], ascending cols, vals [nnzb, 3, 3] or [9 nnzb]), Dirichlet dofs
+    `fixed` (eliminated as P H P + I - P), optional rest `positions` for the
+    two-level preconditioner's aggregates. Same acceptance, regularized retry
+    and SolverError as the reference (gmcp_system_linear_solve)."""
+    L = _lib()
+    h = C.c_void_p()
+    _check(L, L.gmcp_system_create(C.c_int(device), C.byref(h)))
+    try:
+        rp = np.ascontiguousarray(rowptr, np.int32)
+        cl = np.ascontiguousarray(cols, np.int32)
+        vl = np.ascontiguousarray(vals, np.float64).reshape(-1)
+        n = rp.size - 1
+        b = np.ascontiguousarray(rhs, np.float64)
+        if b.size != 3 * n or vl.size != 9 * cl.size:
+            raise _g.ConfigError("solve_descent: rhs must have 3 n entries and vals 9 per block")
+        fx = None if fixed is None else np.ascontiguousarray(fixed, np.uint8)
+        ps = None if positions is None else np.ascontiguousarray(positions, np.float64)
+        dx = np.zeros(3 * n)
+        it, rel, reg = C.c_int32(), C.c_double(), C.c_int32()
+        rc = L.gmcp_system_linear_solve(h, C.c_int64(n), _g._p(rp), _g._p(cl), _g._p(vl),
+                                        None if fx is None else _g._p(fx), None if ps is None else _g._p(ps),
+                                        _g._p(b), C.c_double(pcg_tol), C.c_int32(max_iters), _g._p(dx),
+                                        C.byref(it), C.byref(rel), C.byref(reg))
+        _check(L, rc)
+        return LinearSolveResult(dx, it.value, rel.value, bool(reg.value))
+    finally:
+        L.gmcp_system_destroy(h)
+
+
 def material(E: float, nu: float):
     lam = E * nu / ((1 + nu) * (1 - 2 * nu))
     mu = E / (2 * (1 + nu))
