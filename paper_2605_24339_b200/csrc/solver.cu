@@ -2487,7 +2487,8 @@ struct SegPcgTmp {
 constexpr int kCtaSceneRows = 16384;
 constexpr int kCtaThreads = 128;  // 8 CTAs per SM: all 1024 C5 scenes resident in one wave
 
-__device__ __forceinline__ void cta_sum2(double& a, double& b, double (*sh)[kCtaThreads / 32]) {
+template <int NT = kCtaThreads>
+__device__ __forceinline__ void cta_sum2(double& a, double& b, double (*sh)[NT / 32]) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   a = warp_sum(a);
   b = warp_sum(b);
@@ -2498,7 +2499,7 @@ __device__ __forceinline__ void cta_sum2(double& a, double& b, double (*sh)[kCta
   }
   __syncthreads();
   double s0 = 0, s1 = 0;
-  for (int i = 0; i < kCtaThreads / 32; ++i) {  // every thread, same order: uniform result
+  for (int i = 0; i < NT / 32; ++i) {  // every thread, same order: uniform result
     s0 += sh[0][i];
     s1 += sh[1][i];
   }
@@ -2524,14 +2525,14 @@ struct SceneCoarse {
 // warp w sums aggregates w, w + 4, ... (lanes over the vertex list, fixed
 // butterfly); coarse rows: one warp per row; prolongation: the thread's own
 // vertices (the update loop's assignment).
+template <int NT = kCtaThreads>
 __device__ double scene_coarse(int sc, int v0, int v1, const double* r, double* z, const double* __restrict__ mask,
-                               const SceneCoarse& C, double* s_sm, double* y_sm,
-                               double (*sh)[kCtaThreads / 32]) {
+                               const SceneCoarse& C, double* s_sm, double* y_sm, double (*sh)[NT / 32]) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int a0 = C.scene_agg[sc], na = C.scene_agg[sc + 1] - a0, dim = 6 * na;
   const double* Ai = C.inv + C.scene_coff[sc];
   const double* scl = C.scale + 6 * (int64_t)a0;
-  for (int la = wid; la < na; la += kCtaThreads / 32) {
+  for (int la = wid; la < na; la += NT / 32) {
     const int a = a0 + la;
     double t[6] = {0, 0, 0, 0, 0, 0};
     for (int e = __ldg(C.agg_off + a) + lane; e < __ldg(C.agg_off + a + 1); e += 32) {
@@ -2554,7 +2555,7 @@ __device__ double scene_coarse(int sc, int v0, int v1, const double* r, double* 
   }
   __syncthreads();
   double sy = 0;
-  for (int i = wid; i < dim; i += kCtaThreads / 32) {
+  for (int i = wid; i < dim; i += NT / 32) {
     const double* row = Ai + (int64_t)i * dim;
     double acc = 0;
     for (int j = lane; j < dim; j += 32) acc += __ldg(row + j) * s_sm[j];
@@ -2565,7 +2566,7 @@ __device__ double scene_coarse(int sc, int v0, int v1, const double* r, double* 
     }
   }
   __syncthreads();
-  for (int v = v0 + threadIdx.x; v < v1; v += kCtaThreads) {
+  for (int v = v0 + threadIdx.x; v < v1; v += NT) {
     const int la = __ldg(C.agg + v) - a0;
     const double* ya = y_sm + 6 * la;
     const d3 u = mk3(ya[0], ya[1], ya[2]) + cross(mk3(ya[3], ya[4], ya[5]), ld3(C.dvec, v));
@@ -2575,7 +2576,7 @@ __device__ double scene_coarse(int sc, int v0, int v1, const double* r, double* 
     z[3 * v + 2] += m.z * u.z;
   }
   double unused = 0;
-  cta_sum2(sy, unused, sh);  // lane-0 partials of each warp, summed in warp order
+  cta_sum2<NT>(sy, unused, sh);  // lane-0 partials of each warp, summed in warp order
   return sy;
 }
 
@@ -2783,6 +2784,226 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
   }
 }
 
+// The same per-scene PCG with the scene's p, r and z in shared memory: the
+// SpMV gathers p from shared memory, the smoother reads its partners' r there,
+// and the operand, the smoother rows, the coarse inverse, q and x stream from
+// HBM. Used when every scene fits (kSmSceneBytes); same arithmetic as
+// k_pcg_scene except for the summation layout of the dots.
+// NT threads per scene CTA, MINB CTAs per SM; p always in shared memory, r
+// and z when kRZ (else in the global buffers rg / zg), q in global memory.
+// (p alone in shared memory with 128 threads x 6 CTAs per SM: 6,736 vs 8,014
+// scene-Newton-steps/s for the global kernel -- the 1.15-wave tail; p, r, z
+// with 512 x 2: 8,403; 1024 x 1: 7,910.)
+constexpr int kSmThreads = 512;
+constexpr size_t kSmSceneBytes = 110 * 1024;  // two CTAs per SM
+template <bool kCoarse, int NT, int MINB, bool kRZ>
+__global__ void __launch_bounds__(NT, MINB) k_pcg_scene_sm(MatSet M, const double* __restrict__ mask,
+                                                               const int64_t* __restrict__ voff,
+                                                               const int32_t* __restrict__ act,
+                                                               const double* __restrict__ shift_s,
+                                                               const double* __restrict__ minv,
+                                                               const double* __restrict__ grad,
+                                                               double* __restrict__ x, double* __restrict__ qg,
+                                                               double* __restrict__ rg, double* __restrict__ zg,
+                                                               double tol2, int maxit,
+                                                               double* __restrict__ st, SceneCoarse CS,
+                                                               const int32_t* __restrict__ pair,
+                                                               const double* __restrict__ minv2, int max_rows,
+                                                               int coarse_dim) {
+  extern __shared__ double dsm[];
+  constexpr int kSmThreads = NT;
+  __shared__ double sh[2][kSmThreads / 32];
+  const int sc = blockIdx.x;
+  if (!act[sc]) return;
+  const int v0 = (int)voff[sc], v1 = (int)voff[sc + 1];
+  // scene-local vectors, indexed by global vertex id through the shifted bases
+  double* const ps = dsm;
+  double* const rs = ps + 3 * (int64_t)max_rows;
+  double* const zs = kRZ ? rs + 3 * (int64_t)max_rows : rs;
+  double* const s_sm = kRZ ? zs + 3 * (int64_t)max_rows : rs;
+  double* const y_sm = s_sm + coarse_dim;
+  double* const p = ps - 3 * (int64_t)v0;
+  double* const q = qg;  // q in global memory (written and read once per iteration)
+  double* const r = kRZ ? rs - 3 * (int64_t)v0 : rg;
+  double* const z = kRZ ? zs - 3 * (int64_t)v0 : zg;
+  const double shift = shift_s[sc];
+  double rz = 0, rr = 0;
+  for (int v = v0 + threadIdx.x; v < v1; v += kSmThreads) {
+    const d3 m = ld3(mask, v), g = ld3(grad, v);
+    r[3 * v] = -m.x * g.x;
+    r[3 * v + 1] = -m.y * g.y;
+    r[3 * v + 2] = -m.z * g.z;
+  }
+  __syncthreads();
+  for (int v = v0 + threadIdx.x; v < v1; v += kSmThreads) {
+    const d3 rv = ld3nc(r, v);
+    d3 zv;
+    if (pair) {
+      const int pp = pair[v];
+      zv = pair_apply(minv2, v, rv, pp < 0 ? mk3(0, 0, 0) : ld3nc(r, pp));
+    } else {
+      zv = bmv(minv + 9 * (int64_t)v, rv);
+    }
+    x[3 * v] = x[3 * v + 1] = x[3 * v + 2] = 0;
+    z[3 * v] = zv.x;
+    z[3 * v + 1] = zv.y;
+    z[3 * v + 2] = zv.z;
+    if (!kCoarse) {
+      p[3 * v] = zv.x;
+      p[3 * v + 1] = zv.y;
+      p[3 * v + 2] = zv.z;
+    }
+    rz += dot(rv, zv);
+    rr += dot(rv, rv);
+  }
+  cta_sum2<kSmThreads>(rz, rr, sh);
+  bool indefinite = false, drifted = false;
+  if (kCoarse) {  // z += P Ac^+ P^T r, then p = z
+    rz += scene_coarse<kSmThreads>(sc, v0, v1, r, z, mask, CS, s_sm, y_sm, sh);
+    indefinite = !(rz > 0) && rr > 0;
+    __syncthreads();
+    for (int v = v0 + threadIdx.x; v < v1; v += kSmThreads)
+      for (int k = 0; k < 3; ++k) p[3 * v + k] = z[3 * v + k];
+  }
+  const double bb = rr;
+  int it = 0;
+  double pq = 0, alpha = 0, beta = 0;
+  double win_min = INFINITY, prev_min = INFINITY;
+  const int lane = threadIdx.x & 31, sub = lane & 7;
+  const Bcsr& A = M.el;
+  while (rr > tol2 * bb && it < maxit && !indefinite) {
+    __syncthreads();  // p complete
+    double pqa = 0, unused = 0;
+    for (int vb = v0 + (threadIdx.x >> 3); vb - (lane >> 3) < v1; vb += kSmThreads / 8) {
+      const int v = vb;
+      d3 acc0 = mk3(0, 0, 0), acc1 = mk3(0, 0, 0);
+      if (v < v1) {
+        const int a = __ldg(A.rowptr + v), b = __ldg(A.rowptr + v + 1);
+        int k = a + sub;
+        for (; k + 8 < b; k += 16) {
+          const int j0 = __ldg(A.cols + k), j1 = __ldg(A.cols + k + 8);
+          acc0 = acc0 + bmv_ro(A, k, ld3nc(p, j0));
+          acc1 = acc1 + bmv_ro(A, k + 8, ld3nc(p, j1));
+        }
+        if (k < b) acc0 = acc0 + bmv_ro(A, k, ld3nc(p, __ldg(A.cols + k)));
+      }
+      d3 acc = acc0 + acc1;
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+      }
+      if (sub == 0 && v < v1) {
+        const d3 m = ld3(mask, v), pv = ld3nc(p, v);
+        if (shift != 0) acc = acc + shift * pv;
+        const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
+        q[3 * v] = y.x;
+        q[3 * v + 1] = y.y;
+        q[3 * v + 2] = y.z;
+        pqa += dot(pv, y);
+      }
+    }
+    cta_sum2<kSmThreads>(pqa, unused, sh);  // includes the barrier that publishes q
+    pq = pqa;
+    alpha = pq != 0 ? rz / pq : 0.0;
+    double rzn = 0, rrn = 0;
+    for (int v = v0 + threadIdx.x; v < v1; v += kSmThreads) {  // x += alpha p, r -= alpha q
+      const d3 xv = ld3nc(x, v) + alpha * ld3nc(p, v);
+      const d3 rv = ld3nc(r, v) - alpha * ld3nc(q, v);
+      x[3 * v] = xv.x;
+      x[3 * v + 1] = xv.y;
+      x[3 * v + 2] = xv.z;
+      r[3 * v] = rv.x;
+      r[3 * v + 1] = rv.y;
+      r[3 * v + 2] = rv.z;
+    }
+    __syncthreads();  // r published (pair partners)
+    for (int v = v0 + threadIdx.x; v < v1; v += kSmThreads) {  // z = M1^-1 r
+      const d3 rv = ld3nc(r, v);
+      d3 zv;
+      if (pair) {
+        const int pp = pair[v];
+        zv = pair_apply(minv2, v, rv, pp < 0 ? mk3(0, 0, 0) : ld3nc(r, pp));
+      } else {
+        zv = bmv(minv + 9 * (int64_t)v, rv);
+      }
+      z[3 * v] = zv.x;
+      z[3 * v + 1] = zv.y;
+      z[3 * v + 2] = zv.z;
+      rzn += dot(rv, zv);
+      rrn += dot(rv, rv);
+    }
+    cta_sum2<kSmThreads>(rzn, rrn, sh);
+    if (kCoarse) {
+      rzn += scene_coarse<kSmThreads>(sc, v0, v1, r, z, mask, CS, s_sm, y_sm, sh);
+      if (!(rzn > 0) && rrn > 0) {
+        indefinite = true;
+        rr = rrn;
+        break;
+      }
+    }
+    beta = rz != 0 ? rzn / rz : 0.0;
+    rz = rzn;
+    rr = rrn;
+    ++it;
+    if (!isfinite(rr)) break;
+    if (kCoarse && it % kDriftWindow == 0) {  // true residual from x (global, plain loads)
+      __syncthreads();
+      double tr = 0, unused2 = 0;
+      for (int vb = v0 + (threadIdx.x >> 3); vb - (lane >> 3) < v1; vb += kSmThreads / 8) {
+        const int v = vb;
+        d3 acc = mk3(0, 0, 0);
+        if (v < v1)
+          for (int k = __ldg(A.rowptr + v) + sub; k < __ldg(A.rowptr + v + 1); k += 8)
+            acc = acc + bmv_ro(A, k, ld3nc(x, __ldg(A.cols + k)));
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+          acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        }
+        if (sub == 0 && v < v1) {
+          const d3 m = ld3(mask, v), g = ld3(grad, v), xv = ld3nc(x, v);
+          if (shift != 0) acc = acc + shift * xv;
+          const d3 e = mk3(m.x * (acc.x + g.x), m.y * (acc.y + g.y), m.z * (acc.z + g.z));
+          tr += dot(e, e);
+        }
+      }
+      cta_sum2<kSmThreads>(tr, unused2, sh);
+      if (sqrt(tr / bb) - sqrt(rr / bb) > kDriftFail * sqrt(tol2)) {
+        drifted = true;
+        break;
+      }
+    }
+    win_min = fmin(win_min, rr);
+    constexpr int stag = kCoarse ? kStagWindowCoarse : kStagWindow;
+    if (it % stag == 0) {
+      if (it >= 2 * stag && !(win_min < 0.5 * prev_min) && rr > 1e-8 * bb) break;  // stagnated
+      prev_min = fmin(prev_min, win_min);
+      win_min = INFINITY;
+    }
+    __syncthreads();  // z complete (coarse prolongation) before p = z + beta p
+    for (int v = v0 + threadIdx.x; v < v1; v += kSmThreads) {
+      const d3 pv = ld3nc(z, v) + beta * ld3nc(p, v);
+      p[3 * v] = pv.x;
+      p[3 * v + 1] = pv.y;
+      p[3 * v + 2] = pv.z;
+    }
+  }
+  if (threadIdx.x == 0) {
+    double* o = st + 8 * sc;
+    o[0] = rz;
+    o[1] = pq;
+    o[2] = alpha;
+    o[3] = beta;
+    o[4] = rr;
+    o[5] = bb;
+    o[6] = (double)it;
+    o[7] = indefinite ? 1.0 : drifted ? 2.0 : 0.0;
+  }
+}
+
 // Per scene (one CTA): max |mask .* ((H + shift I) dx) + mask .* grad| and
 // max |mask .* grad| (the reference's inf-norm acceptance test,
 // solver.hpp:349-356), as ordered bits (max is order-free).
@@ -2866,6 +3087,22 @@ int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::v
       coarse_setup_scenes(S, M, T.shift.p);
       CS = SceneCoarse{C.agg.p, C.dvec.p, C.agg_off.p, C.agg_verts.p, C.scene_agg.p, C.scene_coff.p, C.A.p,
                        C.scale.p};
+    }
+    // p, r and z of each scene in shared memory (512 threads, two scenes per SM)
+    // when every scene fits; GMCP_SCENE_SMEM=0 selects the global-memory kernel
+    static const bool smem_on = !std::getenv("GMCP_SCENE_SMEM") || std::atoi(std::getenv("GMCP_SCENE_SMEM")) != 0;
+    const int cdim = coarse ? std::max(C.n_scene_c, 1) : 1;
+    const size_t smem = (9 * (size_t)max_rows + 2 * cdim) * sizeof(double);
+    auto launch = [&](auto kern) {
+      GMCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<NS, kSmThreads, smem, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.minv.p, S.grad.p, S.dx.p,
+                                        S.q.p, S.r.p, S.z.p, tol * tol, maxit, T.st.p, CS,
+                                        pair_smoother ? S.pair_d.p : nullptr, S.minv2.p, (int)max_rows, cdim);
+    };
+    if (smem_on && smem <= kSmSceneBytes) {
+      if (coarse) launch(k_pcg_scene_sm<true, kSmThreads, 2, true>);
+      else launch(k_pcg_scene_sm<false, kSmThreads, 2, true>);
+    } else if (coarse) {
       k_pcg_scene<true><<<NS, kCtaThreads, 0, s>>>(M, S.mask_d.p, T.voff.p, T.act.p, T.shift.p, S.minv.p, S.grad.p,
                                                    S.dx.p, S.r.p, S.z.p, S.p.p, S.q.p, tol * tol, maxit, T.st.p, CS,
                                                    pair_smoother ? S.pair_d.p : nullptr, S.minv2.p);
