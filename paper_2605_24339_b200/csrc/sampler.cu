@@ -1111,33 +1111,41 @@ __global__ void __launch_bounds__(128) k_face_samples(SamplerArgs A, int64_t nsu
 }
 
 // tasks per slave tri in reference order: faces (cand tris), edges (cand
-// edges), points (owned vertices ascending)
+// edges), points (owned vertices ascending); task_ord lists them grouped by
+// kind (faces, edges, points). One thread per task: a binary search over the
+// per-slave-tri offsets of its kind finds its slave tri.
+__device__ __forceinline__ int32_t owner_of(const int64_t* __restrict__ off, int32_t nst, int64_t i) {
+  int32_t lo = 0, hi = nst;  // last st with off[st] <= i
+  while (hi - lo > 1) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (off[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 __global__ void k_tasks(int32_t nst, const int64_t* __restrict__ toff, const int32_t* __restrict__ tids,
                         const int64_t* __restrict__ eoff, const int32_t* __restrict__ eids,
                         const int64_t* __restrict__ poff, const int32_t* __restrict__ pids,
                         int32_t* __restrict__ task_st, int32_t* __restrict__ task_feat, int8_t* __restrict__ task_kind,
                         int32_t* __restrict__ task_ord) {
-  const int64_t nf = toff[nst], ne = eoff[nst];  // kind-grouped order: faces, edges, points
-  GRID_LOOP(st, nst) {
-    int64_t o = toff[st] + eoff[st] + poff[st];
-    for (int64_t i = toff[st]; i < toff[st + 1]; ++i, ++o) {
-      task_st[o] = (int32_t)st;
-      task_feat[o] = tids[i];
-      task_kind[o] = kFace;
-      task_ord[i] = (int32_t)o;
-    }
-    for (int64_t i = eoff[st]; i < eoff[st + 1]; ++i, ++o) {
-      task_st[o] = (int32_t)st;
-      task_feat[o] = eids[i];
-      task_kind[o] = kEdge;
-      task_ord[nf + i] = (int32_t)o;
-    }
-    for (int64_t i = poff[st]; i < poff[st + 1]; ++i, ++o) {
-      task_st[o] = (int32_t)st;
-      task_feat[o] = pids[i];
-      task_kind[o] = kPoint;
-      task_ord[nf + ne + i] = (int32_t)o;
-    }
+  const int64_t nf = toff[nst], ne = eoff[nst], np = poff[nst];
+  GRID_LOOP(g, nf + ne + np) {
+    int kind;
+    int64_t i;
+    const int64_t* off;
+    if (g < nf) { kind = kFace; i = g; off = toff; }
+    else if (g < nf + ne) { kind = kEdge; i = g - nf; off = eoff; }
+    else { kind = kPoint; i = g - nf - ne; off = poff; }
+    const int32_t st = owner_of(off, nst, i);
+    // reference index: the slave tri's earlier tasks, then this kind's earlier ones
+    const int64_t base = toff[st] + eoff[st] + poff[st];
+    const int64_t o = base + (kind == kFace ? i - toff[st]
+                                            : kind == kEdge ? (toff[st + 1] - toff[st]) + (i - eoff[st])
+                                                            : (toff[st + 1] - toff[st]) + (eoff[st + 1] - eoff[st]) +
+                                                                  (i - poff[st]));
+    task_st[o] = st;
+    task_feat[o] = kind == kFace ? tids[i] : kind == kEdge ? eids[i] : pids[i];
+    task_kind[o] = (int8_t)kind;
+    task_ord[g] = (int32_t)o;
   }
 }
 
@@ -1599,7 +1607,7 @@ int64_t run_sampler(Ctx& c, const double* eps_ref_dev) {
   static const bool kind_order = !std::getenv("GMCP_SAMPLER_TASK_ORDER") || std::atoi(std::getenv("GMCP_SAMPLER_TASK_ORDER")) != 0;
   Out O{};
   if (ntask) {
-    k_tasks<<<grid_for(nst, 128), 128, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.pair_off[1].p,
+    k_tasks<<<grid_for(ntask, 256), 256, 0, s>>>(nst, c.pair_off[0].p, c.pair_ids[0].p, c.pair_off[1].p,
                                                 c.pair_ids[1].p, pt_off.p, pt_ids.p, task_st.p, task_feat.p,
                                                 task_kind.p, RT.task_ord.p);
     ++c.launches;

@@ -3099,7 +3099,12 @@ int pcg_batched(SystemImpl& S, SegPcgTmp& T, double tol, int maxit, const std::v
                                         S.q.p, S.r.p, S.z.p, tol * tol, maxit, T.st.p, CS,
                                         pair_smoother ? S.pair_d.p : nullptr, S.minv2.p, (int)max_rows, cdim);
     };
-    if (smem_on && smem <= kSmSceneBytes) {
+    int n_act = 0;
+    for (int32_t a : active) n_act += a != 0;
+    // two scenes per SM: with nearly every scene of a large batch active the
+    // global kernel's single wave (8 scenes per SM) wins, below it the shared one
+    // (C5: 1024 active 123 vs 120 ms per pass; 871: 98 vs 110; 591: 70 vs 97)
+    if (smem_on && smem <= kSmSceneBytes && n_act <= 960) {
       if (coarse) launch(k_pcg_scene_sm<true, kSmThreads, 2, true>);
       else launch(k_pcg_scene_sm<false, kSmThreads, 2, true>);
     } else if (coarse) {

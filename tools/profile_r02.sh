@@ -27,7 +27,13 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 # one blocked Gauss-Jordan step of the coarse inverse (704 coarse dofs)
 ncu --set full --clock-control none --import-source on -k regex:k_gj_step -s 40 -c 1 -o $O/gj_step \
     python tools/newton_c3.py 3 > /dev/null 2>&1
-# the per-scene CTA PCG (C5, two-level) and the per-scene coarse inverse
-ncu --set full --clock-control none -k regex:k_pcg_scene -s 4 -c 1 -o $O/pcg_scene python tools/c5_newton.py 1024 4 \
+# the per-scene CTA PCG (C5, two-level): shared-memory variant (default) and the global one
+ncu --set full --clock-control none -k regex:k_pcg_scene -s 4 -c 1 -o $O/pcg_scene_sm python tools/c5_newton.py 1024 4 \
     > /dev/null 2>&1
+GMCP_SCENE_SMEM=0 ncu --set full --clock-control none -k regex:k_pcg_scene -s 4 -c 1 -o $O/pcg_scene \
+    python tools/c5_newton.py 1024 4 > /dev/null 2>&1
+# the C3 rebuild's sampler kernels (warm rebuilds)
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:"k_sample|k_face|k_query|k_features|k_point_owner|k_tasks" -c 40 --csv --log-file $O/rebuild_launches.csv \
+    python tools/rebuild_c3.py > /dev/null 2>&1
 ls -la $O
