@@ -677,25 +677,30 @@ __global__ void __launch_bounds__(kAggThreads) k_coarse_prolong(
     const int32_t* __restrict__ agg_off, const int32_t* __restrict__ agg_verts, const double* __restrict__ dvec,
     const double* __restrict__ mask, double* __restrict__ z, double* scal, RedSlot rs) {
   __shared__ double ya[6], sy[6];
+  __shared__ double part[kAggThreads / 32][6];
   const int a = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (wid < 6) {
-    const int i = 6 * a + wid;
-    const double* row = Ainv + (int64_t)i * n_pad;
-    double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-    int j = lane;
-    for (; j + 96 < n_pad; j += 128) {
-      const double a0 = __ldg(row + j), a1 = __ldg(row + j + 32), a2 = __ldg(row + j + 64), a3 = __ldg(row + j + 96);
-      const double b0 = __ldg(s + j), b1 = __ldg(s + j + 32), b2 = __ldg(s + j + 64), b3 = __ldg(s + j + 96);
-      c0 += a0 * b0;
-      c1 += a1 * b1;
-      c2 += a2 * b2;
-      c3 += a3 * b3;
+  {  // the aggregate's 6 coarse rows dotted with s by the whole CTA: every
+     // thread loads its column slice of each row at once (one L2 round trip),
+     // warp sums, then the 32 warp partials in warp order (deterministic)
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    const double* rows = Ainv + (int64_t)(6 * a) * n_pad;
+    for (int j = threadIdx.x; j < n_pad; j += kAggThreads) {
+      const double sj = __ldg(s + j);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) acc[r] += __ldg(rows + (int64_t)r * n_pad + j) * sj;
     }
-    for (; j < n_pad; j += 32) c0 += __ldg(row + j) * __ldg(s + j);
-    const double acc = warp_sum((c0 + c1) + (c2 + c3));
-    if (lane == 0) {
-      ya[wid] = scale[i] * acc;
-      sy[wid] = s[i] * acc;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) acc[r] = warp_sum(acc[r]);
+    if (lane == 0)
+#pragma unroll
+      for (int r = 0; r < 6; ++r) part[wid][r] = acc[r];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      const int r = threadIdx.x, i = 6 * a + r;
+      double t = 0;
+      for (int w = 0; w < kAggThreads / 32; ++w) t += part[w][r];
+      ya[r] = scale[i] * t;
+      sy[r] = s[i] * t;
     }
   }
   __syncthreads();
@@ -1845,6 +1850,10 @@ void true_residual(SystemImpl& S, const MatSet& M) {
 // CUDA graph) for rhs = -mask .* gsrc. Returns iterations; solution in S.dx.
 constexpr int kDriftWindow = 256;
 constexpr double kDriftFail = 1e6;  // 100x the largest true/tolerance ratio refinement accepts (kRefineMaxDrift)
+// an unshifted solve whose true residual is this far above the rhs at a drift
+// check diverges along an unconstrained mode (singular system) -> fail now (a
+// regularized solve may pass through large residuals on its way down: exempt)
+constexpr double kDivergeRel = 10.0;
 
 int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift, const double* gsrc) {
   const int nv = S.nv();
@@ -2037,7 +2046,8 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
       S.capture = false;
       true_residual(S, M);
       S.capture = cap;
-      if (S.last_true_rel2 - std::sqrt(h[4] / bb) > kDriftFail * tol) {
+      if (S.last_true_rel2 - std::sqrt(h[4] / bb) > kDriftFail * tol ||
+          (shift == 0 && S.last_true_rel2 > kDivergeRel)) {
         failed = true;
         ++S.drift_fails;
         break;
@@ -2091,8 +2101,10 @@ int pcg(SystemImpl& S, double tol, int maxit, double* rel_out, double shift = 0.
   const int n = (int)S.n_dof;
   // refine a drifted residual only; a true residual orders of magnitude above the
   // recursive one means a failed (e.g. singular) solve -> regularized retry
-  for (int k = 0; k < kMaxRefine && *rel_out <= tol && S.last_true_rel2 > tol &&
-                  S.last_true_rel2 < kRefineMaxDrift * tol && it < maxit;
+  // (a regularized solve is nonsingular: its drift is refined from further away)
+  const double max_drift = shift > 0 ? std::max(kRefineMaxDrift * tol, 1e-2) : kRefineMaxDrift * tol;
+  for (int k = 0; k < kMaxRefine && *rel_out <= tol && S.last_true_rel2 > tol && S.last_true_rel2 < max_drift &&
+                  it < maxit;
        ++k) {
     GMCP_CUDA(cudaMemcpyAsync(S.xacc.p, S.dx.p, n * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
     double rel_c;
@@ -2751,7 +2763,7 @@ __global__ void __launch_bounds__(kCtaThreads, 8) k_pcg_scene(MatSet M, const do
         }
       }
       cta_sum2(tr, unused2, sh);
-      if (sqrt(tr / bb) - sqrt(rr / bb) > kDriftFail * sqrt(tol2)) {
+      if (sqrt(tr / bb) - sqrt(rr / bb) > kDriftFail * sqrt(tol2) || (shift == 0 && sqrt(tr / bb) > kDivergeRel)) {
         drifted = true;
         break;
       }
@@ -2971,7 +2983,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pcg_scene_sm(MatSet M, const doubl
         }
       }
       cta_sum2<kSmThreads>(tr, unused2, sh);
-      if (sqrt(tr / bb) - sqrt(rr / bb) > kDriftFail * sqrt(tol2)) {
+      if (sqrt(tr / bb) - sqrt(rr / bb) > kDriftFail * sqrt(tol2) || (shift == 0 && sqrt(tr / bb) > kDivergeRel)) {
         drifted = true;
         break;
       }
