@@ -590,9 +590,11 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(int nv, const double* __r
 // fixed-order reductions (deterministic), and every z entry is completed by
 // the CTA that owns its vertex.
 
-// CTA sum of W values in warp order (thread 0 holds the result)
+// CTA sum of W values in warp order (thread 0 holds the result): thread q
+// sums value q over the warps, so the W sums run side by side
 template <int W, int NT>
 __device__ __forceinline__ void cta_sum(double (&v)[W], double (&sh)[NT / 32][W]) {
+  __shared__ double tot[W];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < W; ++q) v[q] = warp_sum(v[q]);
@@ -600,13 +602,15 @@ __device__ __forceinline__ void cta_sum(double (&v)[W], double (&sh)[NT / 32][W]
 #pragma unroll
     for (int q = 0; q < W; ++q) sh[wid][q] = v[q];
   __syncthreads();
+  if (threadIdx.x < W) {
+    double t = 0;
+    for (int w = 0; w < NT / 32; ++w) t += sh[w][threadIdx.x];
+    tot[threadIdx.x] = t;
+  }
+  __syncthreads();
   if (threadIdx.x == 0)
 #pragma unroll
-    for (int q = 0; q < W; ++q) {
-      double t = 0;
-      for (int w = 0; w < NT / 32; ++w) t += sh[w][q];
-      v[q] = t;
-    }
+    for (int q = 0; q < W; ++q) v[q] = tot[q];
 }
 
 // x += alpha p, r = r_in - alpha q, z = M1^-1 r (pair or 3x3 block-Jacobi);
