@@ -184,7 +184,7 @@ __device__ __forceinline__ d3 half_bmv(int raw, const double* __restrict__ hv, i
 }
 
 // row_mv8 over the symmetric-half operand (MatSet::hv / hix)
-template <int kRowLanes>
+template <int kRowLanes, bool kOne = false>
 __device__ __forceinline__ d3 row_mv8_half(const Bcsr& A, const int32_t* __restrict__ hix,
                                            const double* __restrict__ hv, int64_t nh, int v,
                                            const double* __restrict__ z, const double* __restrict__ p, double beta,
@@ -195,14 +195,14 @@ __device__ __forceinline__ d3 row_mv8_half(const Bcsr& A, const int32_t* __restr
   int k = a + sub;
   for (; k + kRowLanes < b; k += 2 * kRowLanes) {
     const int2 c0 = __ldg(ch + k), c1 = __ldg(ch + k + kRowLanes);
-    const d3 x0 = ld3(z, c0.x) + beta * ld3(p, c0.x);
-    const d3 x1 = ld3(z, c1.x) + beta * ld3(p, c1.x);
+    const d3 x0 = kOne ? ld3(p, c0.x) : ld3(z, c0.x) + beta * ld3(p, c0.x);
+    const d3 x1 = kOne ? ld3(p, c1.x) : ld3(z, c1.x) + beta * ld3(p, c1.x);
     acc0 = acc0 + half_bmv(c0.y, hv, nh, x0);
     acc1 = acc1 + half_bmv(c1.y, hv, nh, x1);
   }
   if (k < b) {
     const int2 c0 = __ldg(ch + k);
-    acc0 = acc0 + half_bmv(c0.y, hv, nh, ld3(z, c0.x) + beta * ld3(p, c0.x));
+    acc0 = acc0 + half_bmv(c0.y, hv, nh, kOne ? ld3(p, c0.x) : ld3(z, c0.x) + beta * ld3(p, c0.x));
   }
   return acc0 + acc1;
 }
@@ -228,7 +228,21 @@ __device__ __forceinline__ d3 row_mv8(const Bcsr& A, int v, const double* __rest
 }
 
 // K9a: p_new = z + beta p_old (own rows), q = mask .* (H p_new), pq -> alpha (last block).
-template <int kRowLanes, bool kHalf = false>
+inline bool pupdate_on() {  // GMCP_PUPDATE=0: p_new formed inside the SpMV on every system
+  static const bool on = !std::getenv("GMCP_PUPDATE") || std::atoi(std::getenv("GMCP_PUPDATE")) != 0;
+  return on;
+}
+
+// p_new = z + beta p_old, streamed (the SpMV then gathers one vector, not two)
+__global__ void __launch_bounds__(kThreads) k_pupdate(int64_t n, const double* __restrict__ z,
+                                                      const double* __restrict__ p_old, double* __restrict__ p_new,
+                                                      const double* __restrict__ scal) {
+  const double beta = scal[3];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p_new[i] = z[i] + beta * p_old[i];
+}
+
+template <int kRowLanes, bool kHalf = false, bool kPre = false>
 __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const double* __restrict__ mask,
                                                       const double* __restrict__ z, const double* __restrict__ p_old,
                                                       double* __restrict__ p_new, double* __restrict__ q,
@@ -243,7 +257,9 @@ __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const do
     const int v = v0 + (lane / kRowLanes);
     d3 acc = mk3(0, 0, 0);
     if (v < nv) {
-      if (kHalf) {
+      if (kPre) {  // p_new formed by k_pupdate: one gathered vector
+        acc = row_mv8_half<kRowLanes, true>(M.el, M.hix, M.hv, M.hn, v, nullptr, p_new, 0.0, sub);
+      } else if (kHalf) {
         acc = row_mv8_half<kRowLanes>(M.el, M.hix, M.hv, M.hn, v, z, p_old, beta, sub);
       } else {
         acc = row_mv8<kRowLanes>(M.el, v, z, p_old, beta, sub);
@@ -258,15 +274,17 @@ __global__ void __launch_bounds__(kThreads) k_spmv_cg(int nv, MatSet M, const do
     }
     if (sub == 0 && v < nv) {
       const d3 m = ld3(mask, v);
-      const d3 pv = ld3(z, v) + beta * ld3(p_old, v);
+      const d3 pv = kPre ? ld3(p_new, v) : ld3(z, v) + beta * ld3(p_old, v);
       if (M.shift != 0) acc = acc + M.shift * pv;
       const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
       q[3 * v] = y.x;
       q[3 * v + 1] = y.y;
       q[3 * v + 2] = y.z;
-      p_new[3 * v] = pv.x;
-      p_new[3 * v + 1] = pv.y;
-      p_new[3 * v + 2] = pv.z;
+      if (!kPre) {
+        p_new[3 * v] = pv.x;
+        p_new[3 * v + 1] = pv.y;
+        p_new[3 * v + 2] = pv.z;
+      }
       dots[0] += dot(pv, y);
     }
   }
@@ -1970,7 +1988,16 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
       double* p_old = (k & 1) ? S.w.p : S.p.p;
       double* p_new = (k & 1) ? S.p.p : S.w.p;
       const bool half = M.hv != nullptr && M.np == 0;
-      if (lanes == 8 && half)
+      const bool pre = pupdate_on();
+      // large systems: p_new streamed by its own kernel, the SpMV gathers one vector
+      // (C3 PCG iteration 47.1 -> 45.3 us); small ones keep the fused form (the
+      // extra launch costs more than it saves: Hertz 5.4 -> 5.9 ms per Newton step)
+      if (half && pre && lanes == 4) {
+        k_pupdate<<<std::min(grid_for(3 * (int64_t)nv, kThreads), kBlocks), kThreads, 0, S.stream>>>(
+            3 * (int64_t)nv, S.z.p, p_old, p_new, S.scal.p);
+        k_spmv_cg<4, true, true><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p,
+                                                                  S.scal.p, S.slot(1));
+      } else if (lanes == 8 && half)
         k_spmv_cg<8, true><<<gsp, kThreads, 0, S.stream>>>(nv, M, S.mask_d.p, S.z.p, p_old, p_new, S.q.p, S.scal.p,
                                                             S.slot(1));
       else if (lanes == 8)
@@ -2025,7 +2052,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     GMCP_CUDA(cudaEventRecord(S.ev0, S.stream));
     GMCP_CUDA(cudaGraphLaunch(exec, S.stream));
     GMCP_CUDA(cudaEventRecord(S.ev1, S.stream));
-    S.launches += (coarse ? 3 : 2) * chunk;
+    S.launches += ((coarse ? 3 : 2) + (M.hv && M.np == 0 && lanes == 4 && pupdate_on() ? 1 : 0)) * chunk;
     it += chunk;
     GMCP_CUDA(cudaMemcpyAsync(h, S.scal.p, sizeof h, cudaMemcpyDeviceToHost, S.stream));
     S.sync();
