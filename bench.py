@@ -148,7 +148,9 @@ def pcg_roofline(ps: dict, pre: dict | None = None) -> dict:
               the diagonal) + 8 B (column, stored index) per block of the merged
               pattern (76 B per block when the full BCSR is read) + per row 4 B
               row pointer and 24 B each of z, p_old, mask read and p_new, q
-              written (124 B);
+              written (124 B); large systems split p = z + beta p into
+              k_pupdate (z, p_old read, p_new written: 72 B/row) and the SpMV
+              then reads p_new and mask and writes q (76 B/row);
       update  24 B each of p, q, x, r read and x, r, z written (168 B), the
               vertex-pair block-Jacobi rows (3x6 = 144 B) + 4 B pair index
               (316 B/row; the partner's r and q rows are L2 hits of rows another
@@ -160,8 +162,9 @@ def pcg_roofline(ps: dict, pre: dict | None = None) -> dict:
     if not ps["iters"]:
         return None
     peak, src = peaks()
-    row = 124 + (316 if (pre is None or pre["pair_jacobi"]) else 168 + 72)
     half = ps.get("stored_blocks", 0) > 0
+    split = half and ps["rows"] >= 32768  # large systems stream p = z + beta p in k_pupdate
+    row = (76 + 72 if split else 124) + (316 if (pre is None or pre["pair_jacobi"]) else 168 + 72)
     coarse = bool(pre and pre["coarse"])
     if coarse:
         row += 52 + 100
@@ -169,7 +172,8 @@ def pcg_roofline(ps: dict, pre: dict | None = None) -> dict:
     per_iter = mat + row * ps["rows"] + (8 * pre["coarse_padded"] ** 2 if coarse else 0)
     ms = ps["ms"] / ps["iters"]
     achieved = per_iter / (ms / 1e3) / 1e9
-    kern = "k_spmv_cg + k_update_agg + k_coarse_prolong" if coarse else "k_spmv_cg + k_update_cg_pair"
+    kern = ("k_pupdate + " if split else "") + (
+        "k_spmv_cg + k_update_agg + k_coarse_prolong" if coarse else "k_spmv_cg + k_update_cg_pair")
     return {"bound": "hbm", "kernels": kern + " (one PCG iteration)", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "algorithmic_bytes": per_iter,
             "us_per_iter": 1e3 * ms, "iters_timed": ps["iters"], "operand_blocks": ps["nnzb"], "rows": ps["rows"],
