@@ -1770,7 +1770,7 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
   }
   GMCP_CUDA(cudaMemsetAsync(S.redu.p + 4, 0, sizeof(unsigned long long), S.stream));
   C.piv.resize(2 * kGJ * kGJ);
-  k_gj_pivot0<<<1, 32, 0, S.stream>>>(n_pad, X, C.piv.p, S.coarse_drop, S.redu.p + 4);
+  k_gj_pivot0<<<1, kGJThreads, 0, S.stream>>>(n_pad, X, C.piv.p, S.coarse_drop, S.redu.p + 4);
   ++S.launches;
   for (int k = 0; k < nt; ++k) {
     k_gj_step<<<dim3(nt, nt), kGJThreads, 0, S.stream>>>(n_pad, k, X, Y, C.piv.p + (k & 1) * kGJ * kGJ,
