@@ -1770,6 +1770,39 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
   }
   GMCP_CUDA(cudaMemsetAsync(S.redu.p + 4, 0, sizeof(unsigned long long), S.stream));
   C.piv.resize(2 * kGJ * kGJ);
+  // one cooperative launch when every CTA's tiles fit in shared memory
+  static const bool persistent = !std::getenv("GMCP_GJ_PERSISTENT") || std::atoi(std::getenv("GMCP_GJ_PERSISTENT")) != 0;
+  int sms = 0;
+  GMCP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, S.device));
+  const int G = std::min(sms, nt * nt);
+  const size_t gsmem = (size_t)((nt * nt + G - 1) / G + 1 + 3 * kGJGroups) * kGJ * (kGJ + 1) * sizeof(double);
+  if (persistent && gsmem <= 200 * 1024) {
+    GMCP_CUDA(cudaFuncSetAttribute(k_gj_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
+    int occ = 0;
+    GMCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gj_persistent, kGJPThreads, gsmem));
+    if (occ >= 1) {
+      C.gj_rowp.resize(2 * (size_t)nt * kGJ * kGJ);
+      C.gj_colp.resize(2 * (size_t)nt * kGJ * kGJ);
+      int np_ = n_pad;
+      double thr = S.coarse_drop;
+      unsigned long long* dr = S.redu.p + 4;
+      void* args[] = {&np_, &X, &C.gj_rowp.p, &C.gj_colp.p, &C.piv.p, &thr, &dr};
+      if (trace) GMCP_CUDA(cudaEventRecord(te[1], S.stream));
+      GMCP_CUDA(cudaLaunchCooperativeKernel((const void*)k_gj_persistent, G, kGJPThreads, args, gsmem, S.stream));
+      ++S.launches;
+      C.inv = X;
+      if (trace) {
+        GMCP_CUDA(cudaEventRecord(te[2], S.stream));
+        GMCP_CUDA(cudaEventSynchronize(te[2]));
+        float a = 0, b = 0;
+        GMCP_CUDA(cudaEventElapsedTime(&a, te[0], te[1]));
+        GMCP_CUDA(cudaEventElapsedTime(&b, te[1], te[2]));
+        std::fprintf(stderr, "[gmcp] Gauss-Jordan (one cooperative launch, %d CTAs): %.3f ms\n", G, b);
+        for (auto& e : te) cudaEventDestroy(e);
+      }
+      return;
+    }
+  }
   k_gj_pivot0<<<1, kGJThreads, 0, S.stream>>>(n_pad, X, C.piv.p, S.coarse_drop, S.redu.p + 4);
   ++S.launches;
   for (int k = 0; k < nt; ++k) {
