@@ -1137,6 +1137,8 @@ struct SystemImpl {
   double last_true_rel2 = 0, last_true_relinf = 0, true_rel2_max = 0, true_relinf_max = 0;
   int64_t n_linear_solves = 0, refinements = 0;
   int64_t drift_fails = 0;       // PCG solves failed early on a true/recursive residual gap (pcg_core)
+  double last_solve_shift = -1;  // shift / pattern generation of the last pcg_core call (refinement passes)
+  int64_t last_solve_ops = -1;
   int64_t coarse_fallbacks = 0;  // batched: scene solves re-run with block-Jacobi after a failed two-level solve
   DBuf<double> rt, xacc;  // true residual vector, accumulated solution (residual replacement)
   // optional host capture of the last linear system (gmcp_system_capture_linear_system)
@@ -1914,6 +1916,11 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
   const int nv = S.nv();
   MatSet M = mats(S);
   M.shift = shift;
+  // a refinement pass (pcg(): rhs = the true residual) solves with the operator
+  // and shift of the solve it refines, right after it
+  const bool refine_pass = gsrc != S.grad.p && S.last_solve_shift == shift && S.last_solve_ops == S.u_gen;
+  S.last_solve_shift = shift;
+  S.last_solve_ops = S.u_gen;
   const bool pairs = S.has_pairs && S.pair_d.n == nv;
   const bool coarse = S.cs.enabled && M.np == 0;
   CoarseSpace& C = S.cs;
@@ -1951,7 +1958,8 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
   if (pairs) {
     S.minv2.resize(18 * (int64_t)nv);
     S.r2.resize(3 * (int64_t)nv);
-    k_pair_jacobi<<<grid_for(nv, 128), 128, 0, S.stream>>>(nv, M, S.mask_d.p, S.pair_d.p, S.minv2.p);
+    if (!refine_pass)  // a refinement pass keeps the operator, so the smoother too
+      k_pair_jacobi<<<grid_for(nv, 128), 128, 0, S.stream>>>(nv, M, S.mask_d.p, S.pair_d.p, S.minv2.p);
     if (coarse)
       k_pcg_init_pair<true><<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv2.p, S.pair_d.p, S.dx.p,
                                                                 S.r.p, S.z.p, S.p.p, S.scal.p, S.slot(0));
@@ -1959,7 +1967,8 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     k_pcg_init_pair<false><<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv2.p, S.pair_d.p, S.dx.p,
                                                         S.r.p, S.z.p, S.p.p, S.scal.p, S.slot(0));
   } else {
-    k_block_jacobi<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, M, S.mask_d.p, S.minv.p);
+    if (!refine_pass)
+      k_block_jacobi<<<grid_for(nv, 256), 256, 0, S.stream>>>(nv, M, S.mask_d.p, S.minv.p);
     if (coarse)
       k_pcg_init<true><<<kBlocks, kThreads, 0, S.stream>>>(nv, gsrc, S.mask_d.p, S.minv.p, S.dx.p, S.r.p, S.z.p,
                                                            S.p.p, S.scal.p, S.slot(0));
