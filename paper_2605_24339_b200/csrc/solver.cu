@@ -6,6 +6,7 @@
 // every Krylov vector stay on the device for the whole run; the host reads
 // only scalars (residual, alpha, energy decrease, convergence) per iteration.
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <chrono>
 #include <cstdio>
@@ -14,6 +15,8 @@
 #include <cmath>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <thread>
 
 #include "../../include/gmcp_solver.h"
 #include "ctx.hpp"
@@ -1220,37 +1223,82 @@ void build_operators(Body& b) {
 }
 
 // Constant elastic BCSR (elasticity.hpp:124-141), blocks summed in tet order.
+// Host-side set-up work over independent items (bodies) on up to 32 threads;
+// every item is computed by exactly one thread, so results do not depend on
+// the thread count.
+template <class F>
+void parallel_for(int64_t n, F&& f) {
+  const int nt = (int)std::min<int64_t>(n, std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+  if (nt <= 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<int64_t> next{0};
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex m;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&]() {
+      try {
+        for (int64_t i; (i = next.fetch_add(1)) < n;) f(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(m);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+
 // Vertex pairs of the 6x6 block-Jacobi (single systems and the per-scene CTA
 // PCG) from an AoS BCSR of the operand's constant part: greedy matching of the
 // strongest normalized couplings |K_vw|_F^2 / (|K_vv|_F |K_ww|_F) (ties by index).
-void build_pairing(SystemImpl& S, const std::vector<int32_t>& rowptr, const std::vector<int32_t>& cols,
-                   const std::vector<double>& vals) {
-  const int nv = (int)rowptr.size() - 1;
+void build_pairing(SystemImpl& S, int nv, const int32_t* rowptr, const int32_t* cols, const double* vals) {
 #if GMCP_PAIR_JACOBI
   S.has_pairs = false;
   if (S.use_pair) {
+    // vertex ranges matched independently: the bodies when no block couples two
+    // of them (the elastic operator), else the whole system. Greedy matching
+    // in descending score (ties in (row, block) order) on disjoint components
+    // equals the global greedy matching, so each range sorts its own edges.
+    std::vector<std::pair<int32_t, int32_t>> ranges;
+    for (const Body& b : S.bodies) ranges.push_back({b.offset, b.offset + b.nv});
+    std::atomic<bool> split{!ranges.empty()};
+    parallel_for((int64_t)ranges.size(), [&](int64_t r) {
+      for (int v = ranges[r].first; v < ranges[r].second; ++v)
+        for (int k = rowptr[v]; k < rowptr[v + 1]; ++k)
+          if (cols[k] < ranges[r].first || cols[k] >= ranges[r].second) {
+            split = false;
+            return;
+          }
+    });
+    if (!split) ranges.assign(1, {0, nv});
     std::vector<double> dn(nv, 0.0);
-    for (int v = 0; v < nv; ++v)
-      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k)
-        if (cols[k] == v)
-          for (int q = 0; q < 9; ++q) dn[v] += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
-    struct Edge { double s; int32_t a, b; };
-    std::vector<Edge> edges;
-    for (int v = 0; v < nv; ++v)
-      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
-        const int w = cols[k];
-        if (w <= v || !(dn[v] > 0) || !(dn[w] > 0)) continue;
-        double f = 0;
-        for (int q = 0; q < 9; ++q) f += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
-        edges.push_back({f / std::sqrt(dn[v] * dn[w]), v, w});
-      }
-    std::stable_sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) { return x.s > y.s; });
+    parallel_for((int64_t)ranges.size(), [&](int64_t r) {
+      for (int v = ranges[r].first; v < ranges[r].second; ++v)
+        for (int k = rowptr[v]; k < rowptr[v + 1]; ++k)
+          if (cols[k] == v)
+            for (int q = 0; q < 9; ++q) dn[v] += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
+    });
     std::vector<int32_t> mate(nv, -1);
-    for (const Edge& e : edges)
-      if (mate[e.a] < 0 && mate[e.b] < 0) {
-        mate[e.a] = e.b;
-        mate[e.b] = e.a;
-      }
+    parallel_for((int64_t)ranges.size(), [&](int64_t r) {
+      struct Edge { double s; int32_t a, b; };
+      std::vector<Edge> edges;
+      for (int v = ranges[r].first; v < ranges[r].second; ++v)
+        for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
+          const int w = cols[k];
+          if (w <= v || !(dn[v] > 0) || !(dn[w] > 0)) continue;
+          double f = 0;
+          for (int q = 0; q < 9; ++q) f += vals[9 * (size_t)k + q] * vals[9 * (size_t)k + q];
+          edges.push_back({f / std::sqrt(dn[v] * dn[w]), v, w});
+        }
+      std::stable_sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) { return x.s > y.s; });
+      for (const Edge& e : edges)
+        if (mate[e.a] < 0 && mate[e.b] < 0) {
+          mate[e.a] = e.b;
+          mate[e.b] = e.a;
+        }
+    });
     S.pair_d.upload(mate, S.stream);
     S.has_pairs = true;
   }
@@ -1261,8 +1309,16 @@ void build_pairing(SystemImpl& S, const std::vector<int32_t>& rowptr, const std:
 
 void build_elastic(SystemImpl& S) {
   const int nv = S.nv();
-  std::vector<std::vector<std::pair<int32_t, std::array<double, 9>>>> rows(nv);
-  for (const Body& b : S.bodies) {
+  // per body (bodies are independent; one thread each): its rows, columns
+  // ascending, blocks summed over its tets in tet order
+  struct BodyCsr {
+    std::vector<int32_t> len, cols;
+    std::vector<double> vals;
+  };
+  std::vector<BodyCsr> part(S.bodies.size());
+  parallel_for((int64_t)S.bodies.size(), [&](int64_t bi_) {
+    const Body& b = S.bodies[bi_];
+    std::vector<std::vector<std::pair<int32_t, std::array<double, 9>>>> rows(b.nv);
     const int64_t nt = (int64_t)b.tets.size() / 4;
     for (int64_t t = 0; t < nt; ++t) {
       const double* g = &b.grads[12 * t];
@@ -1275,8 +1331,8 @@ void build_elastic(SystemImpl& S) {
           for (int r = 0; r < 3; ++r)
             for (int c = 0; c < 3; ++c)
               blk[3 * r + c] = b.vol[t] * (b.lambda * gi[r] * gj[c] + b.mu * gj[r] * gi[c] + (r == c ? b.mu * gg : 0.0));
-          const int32_t bi = b.offset + b.tets[4 * t + i], bj = b.offset + b.tets[4 * t + j];
-          auto& row = rows[bi];
+          const int32_t li = b.tets[4 * t + i], bj = b.offset + b.tets[4 * t + j];
+          auto& row = rows[li];
           auto it = std::find_if(row.begin(), row.end(), [&](const auto& e) { return e.first == bj; });
           if (it == row.end()) {
             row.push_back({bj, blk});
@@ -1285,23 +1341,45 @@ void build_elastic(SystemImpl& S) {
           }
         }
     }
-  }
-  std::vector<int32_t> rowptr(nv + 1, 0), cols;
-  std::vector<double> vals;
-  for (int v = 0; v < nv; ++v) {
-    auto& row = rows[v];
-    std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    for (const auto& e : row) {
-      cols.push_back(e.first);
-      vals.insert(vals.end(), e.second.begin(), e.second.end());
+    BodyCsr& P = part[bi_];
+    P.len.resize(b.nv);
+    size_t tot = 0;
+    for (const auto& row : rows) tot += row.size();
+    P.cols.reserve(tot);
+    P.vals.reserve(9 * tot);
+    for (int v = 0; v < b.nv; ++v) {
+      auto& row = rows[v];
+      std::sort(row.begin(), row.end(), [](const auto& a, const auto& c) { return a.first < c.first; });
+      P.len[v] = (int32_t)row.size();
+      for (const auto& e : row) {
+        P.cols.push_back(e.first);
+        P.vals.insert(P.vals.end(), e.second.begin(), e.second.end());
+      }
     }
-    rowptr[v + 1] = (int32_t)cols.size();
+  });
+  std::vector<int32_t> rowptr(nv + 1, 0);
+  std::vector<int64_t> boff(S.bodies.size() + 1, 0);
+  for (size_t bi_ = 0; bi_ < S.bodies.size(); ++bi_) {
+    const Body& b = S.bodies[bi_];
+    for (int v = 0; v < b.nv; ++v) rowptr[b.offset + v + 1] = part[bi_].len[v];
   }
+  for (int v = 0; v < nv; ++v) rowptr[v + 1] += rowptr[v];
+  const int64_t nnzb = rowptr[nv];
+  // uninitialized host arrays (every entry is copied below): no 1.4 GB memset at C5
+  std::unique_ptr<int32_t[]> cols(new int32_t[std::max<int64_t>(nnzb, 1)]);
+  std::unique_ptr<double[]> vals(new double[std::max<int64_t>(9 * nnzb, 1)]);
+  parallel_for((int64_t)S.bodies.size(), [&](int64_t bi_) {
+    const Body& b = S.bodies[bi_];
+    const int64_t o = rowptr[b.offset];
+    std::copy(part[bi_].cols.begin(), part[bi_].cols.end(), cols.get() + o);
+    std::copy(part[bi_].vals.begin(), part[bi_].vals.end(), vals.get() + 9 * o);
+  });
   S.k_rowptr.upload(rowptr, S.stream);
-  S.k_cols.upload(cols, S.stream);
-  S.k_vals.upload(vals, S.stream);
-  S.el_nnzb = (int64_t)cols.size();
-  build_pairing(S, rowptr, cols, vals);
+  S.k_cols.upload(cols.get(), nnzb, S.stream);
+  S.k_vals.upload(vals.get(), 9 * nnzb, S.stream);
+  S.el_nnzb = nnzb;
+  build_pairing(S, nv, rowptr.data(), cols.get(), vals.get());
+  S.sync();  // the uploads read the host arrays
   S.el_built = true;
 }
 
@@ -2211,7 +2289,17 @@ void setup_solve(SystemImpl& S, int64_t& n_free, DBuf<double>& eps_ref) {
   n_free = 0;
   for (uint8_t f : S.fixed) n_free += f == 0;
   if (n_free == 0) throw StatusError(GMCP_ERR_CONFIG, "solve: no free degrees of freedom");
+  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    S.sync();
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gmcp setup] %s %.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   if (!S.el_built) build_elastic(S);
+  lap("elastic operator + pairing");
   // fixed dofs at their targets (solver.hpp:139-140)
   for (int64_t d = 0; d < S.n_dof; ++d)
     if (S.fixed[d]) S.x_host[d] = S.dirichlet[d];
@@ -2236,7 +2324,9 @@ void setup_solve(SystemImpl& S, int64_t& n_free, DBuf<double>& eps_ref) {
     cudaGraphExecDestroy(S.pcg_exec);
     S.pcg_exec = nullptr;
   }
+  lap("vectors + mask");
   build_coarse(S, mask);
+  lap("coarse space");
   eps_ref.resize(n);
   GMCP_CUDA(cudaMemcpyAsync(eps_ref.p, S.x.p, n * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
   for (auto& pr : S.pairs) {
@@ -3482,10 +3572,14 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
     ss.step = step;
     ss.min_gap = 1.7976931348623157e308;
     ss.energy_monotone = 1;
+    const auto t_step = tnow();
     rebuild_all();
+    const double ms_rb = ms_since(t_step);
     assemble(S, lambda);
     scene_el();
     scene_contact(S.x.p, ce);
+    if (trace) std::fprintf(stderr, "[gmcp batched] step %d start: rebuild %.2f ms, assemble + energies %.2f ms\n", step,
+                            ms_rb, ms_since(t_step) - ms_rb);
     gmcp_step_stats* sst = S.scene_stats.data() + (size_t)(step - 1) * NS;  // this step, per scene
     for (int sc = 0; sc < NS; ++sc) {
       if (!feas[sc]) throw StatusError(GMCP_ERR_SOLVER, "solve: configuration with penetrating contact sample");
@@ -3661,8 +3755,9 @@ void system_solve_batched(SystemImpl& S, const gmcp_solver_settings& st, gmcp_st
       if (trace)
         std::fprintf(stderr,
                      "[gmcp batched] step %d it %d active %d: assemble+resid %.2f ms, pcg %.2f ms (%d it), "
-                     "alpha+line search %.2f ms (%d trials), rebuild %.2f ms (%d scenes)\n",
-                     step, it, n_active, ms_asm, ms_pcg, pit, ms_ls, n_trials, ms_since(t_rb), n_flag_total);
+                     "alpha+line search %.2f ms (%d trials), rebuild %.2f ms (%d scenes); pass %.2f ms\n",
+                     step, it, n_active, ms_asm, ms_pcg, pit, ms_ls, n_trials, ms_since(t_rb), n_flag_total,
+                     ms_since(t_it));
       if (S.iter_limit > 0) {  // timing mode (gmcp_system_time_newton): loop passes
         S.sync();
         S.iter_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_it).count());
@@ -3938,7 +4033,7 @@ LinearSolveOut linear_solve(SystemImpl& S, int64_t nv, const int32_t* rowptr, co
   S.k_vals.upload(vl, S.stream);
   S.el_nnzb = nnzb;
   S.el_built = true;
-  build_pairing(S, rp, cl, vl);
+  build_pairing(S, (int)nv, rp.data(), cl.data(), vl.data());
   S.fixed.assign(n, 0);
   int64_t n_free = 0;
   std::vector<double> mask(n);
