@@ -1868,7 +1868,12 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
       unsigned long long* dr = S.redu.p + 4;
       void* args[] = {&np_, &X, &C.gj_rowp.p, &C.gj_colp.p, &C.piv.p, &thr, &dr};
       if (trace) GMCP_CUDA(cudaEventRecord(te[1], S.stream));
-      GMCP_CUDA(cudaLaunchCooperativeKernel((const void*)k_gj_persistent, G, kGJPThreads, args, gsmem, S.stream));
+      const cudaError_t le =
+          cudaLaunchCooperativeKernel((const void*)k_gj_persistent, G, kGJPThreads, args, gsmem, S.stream);
+      if (le != cudaSuccess) {  // e.g. the SMs are shared and the grid cannot be co-resident: per-step launches
+        (void)cudaGetLastError();
+        goto per_step;
+      }
       ++S.launches;
       C.inv = X;
       if (trace) {
@@ -1883,6 +1888,7 @@ void coarse_setup_impl(SystemImpl& S, const MatSet& M) {
       return;
     }
   }
+per_step:
   k_gj_pivot0<<<1, kGJThreads, 0, S.stream>>>(n_pad, X, C.piv.p, S.coarse_drop, S.redu.p + 4);
   ++S.launches;
   for (int k = 0; k < nt; ++k) {
