@@ -22,10 +22,12 @@ ncu --set full --clock-control none --import-source on -k regex:k_coarse_prolong
     python tools/newton_c3.py 3 > /dev/null 2>&1
 # per-launch durations of one steady PCG stretch
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"k_spmv_cg|k_update_agg|k_coarse_prolong" -s 1800 -c 60 --csv --log-file $O/pcg_launches.csv \
+    -k regex:"k_pupdate|k_spmv_cg|k_update_agg|k_coarse_prolong" -s 2400 -c 80 --csv --log-file $O/pcg_launches.csv \
     python tools/newton_c3.py 3 > /dev/null 2>&1
-# one blocked Gauss-Jordan step of the coarse inverse (704 coarse dofs)
-ncu --set full --clock-control none --import-source on -k regex:k_gj_step -s 40 -c 1 -o $O/gj_step \
+# the cooperative blocked Gauss-Jordan coarse inverse (704 coarse dofs, one launch) and the p-update
+ncu --set full --clock-control none --import-source on -k regex:k_gj_persistent -s 1 -c 1 -o $O/gj_persistent \
+    python tools/newton_c3.py 3 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_pupdate -s 600 -c 1 -o $O/pupdate \
     python tools/newton_c3.py 3 > /dev/null 2>&1
 # the per-scene CTA PCG (C5, two-level): shared-memory variant (default) and the global one
 ncu --set full --clock-control none -k regex:k_pcg_scene -s 4 -c 1 -o $O/pcg_scene_sm python tools/c5_newton.py 1024 4 \
