@@ -2204,7 +2204,7 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
       true_residual(S, M);
       S.capture = cap;
       if (S.last_true_rel2 - std::sqrt(h[4] / bb) > kDriftFail * tol ||
-          (shift == 0 && S.last_true_rel2 > kDivergeRel)) {
+          (coarse && shift == 0 && S.last_true_rel2 > kDivergeRel)) {
         failed = true;
         ++S.drift_fails;
         break;
