@@ -22,6 +22,7 @@
 #include "ctx.hpp"
 #include "kin.cuh"
 #include "cubutil.cuh"
+#include <cooperative_groups.h>
 #include "coarse.cuh"
 
 namespace gmcp_b200 {
@@ -151,6 +152,12 @@ constexpr double kRegularization = 1e-8;  // SolverSettings::regularization (sol
 // magnitude per window and never trip it.
 constexpr int kStagWindow = 1024;
 constexpr int kStagWindowCoarse = 256;
+constexpr int kDriftWindow = 256;
+constexpr double kDriftFail = 1e6;  // 100x the largest true/tolerance ratio refinement accepts (kRefineMaxDrift)
+// an unshifted solve whose true residual is this far above the rhs at a drift
+// check diverges along an unconstrained mode (singular system) -> fail now (a
+// regularized solve may pass through large residuals on its way down: exempt)
+constexpr double kDivergeRel = 10.0;
 constexpr double kAcceptRelInf = 1e-6;  // solver.hpp:349-356 acceptance of a linear solve
 // scaled coarse pivots below this drop their rigid mode: low enough to keep a
 // floating body's regularized rigid mode (pivot ~ shift / aggregate stiffness)
@@ -754,6 +761,289 @@ __global__ void __launch_bounds__(kAggThreads) k_coarse_prolong(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small systems (C1, C4, the patch test): the whole two-level PCG iteration
+// loop in ONE cooperative launch. The three-kernel iteration is latency-bound
+// there (~27 us for 1,253 vertices); here it is three grid barriers:
+//   A  p = z + beta p_old (own rows) and q = mask .* (H + shift) p, p.q partial
+//   B  per aggregate (CTA-owned): x += alpha p, r = r_in - alpha q, z = M1^-1 r
+//      (vertex pairs), restriction s_a, r.z and r.r partials
+//   C  per aggregate: its 6 coarse rows of y = S Ac^+ s', z += Phi y, s.y partial
+// then every thread sums the per-CTA partials in CTA order (the same values in
+// every CTA: deterministic) and takes the same convergence / stagnation /
+// failure decisions. Vectors written inside the kernel are read with ld.cg
+// (L2): the L1s are not coherent across SMs. The drift check of pcg_core runs
+// every kDriftWindow iterations on the true residual.
+constexpr int kCoopThreads = 256, kCoopMaxCtas = 64;
+constexpr int kCoopMaxRows = 16384;  // systems up to this many vertices run k_pcg_coop
+struct CoopArgs {
+  MatSet M;
+  int nv;
+  const double* mask;
+  const double* grad;  // rhs = -mask .* grad (the drift check)
+  const double* minv2;
+  const int32_t* pair;
+  const int32_t* agg_off;
+  const int32_t* agg_verts;
+  const double* dvec;
+  const double* scale;
+  const double* inv;
+  int n_agg, n_pad;
+  double* x;
+  double* r0;
+  double* r1;
+  double* z;
+  double* p0;
+  double* p1;
+  double* q;
+  double* s;
+  double* part;  // [4][kCoopMaxCtas]
+  double* scal;  // in: [0] rz [4] rr [5] bb; out: [0] rz [4] rr [9] status [10] iterations
+  double tol2;
+  int maxit;
+  int drift_check;
+  double drift_tol;  // kDriftFail * tol
+};
+__device__ __forceinline__ d3 ldcg3(const double* p, int v) {
+  return mk3(__ldcg(p + 3 * (int64_t)v), __ldcg(p + 3 * (int64_t)v + 1), __ldcg(p + 3 * (int64_t)v + 2));
+}
+// CTA sum of W values (thread 0 of the CTA holds them), fixed order
+template <int W>
+__device__ __forceinline__ void coop_cta_sum(double (&v)[W], double (*sh)[W]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < W; ++q) v[q] = warp_sum(v[q]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < W; ++q) sh[wid][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      double t = 0;
+      for (int w = 0; w < kCoopThreads / 32; ++w) t += sh[w][q];
+      v[q] = t;
+    }
+}
+__global__ void __launch_bounds__(kCoopThreads) k_pcg_coop(CoopArgs A) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[kCoopThreads / 32][8];
+  __shared__ double ya[6];
+  const int G = gridDim.x, b = blockIdx.x, t = threadIdx.x, lane = t & 31, sub = lane & 7;
+  const int gt = b * kCoopThreads + t, nthreads = G * kCoopThreads;
+  const MatSet& M = A.M;
+  double rz = __ldcg(A.scal), rr = __ldcg(A.scal + 4);
+  const double bb = __ldcg(A.scal + 5), target = A.tol2 * bb;
+  double beta = 0;
+  int it = 0, status = 0;
+  double win_min = INFINITY, prev_min = INFINITY;
+  while (rr > target && it < A.maxit) {
+    double* p_old = (it & 1) ? A.p1 : A.p0;
+    double* p_new = (it & 1) ? A.p0 : A.p1;
+    const double* r_in = (it & 1) ? A.r1 : A.r0;
+    double* r_out = (it & 1) ? A.r0 : A.r1;
+    // A: SpMV, 8 lanes per row, rows grid-strided
+    double pq = 0;
+    for (int v0 = gt >> 3; v0 - (lane >> 3) < A.nv; v0 += nthreads >> 3) {  // warp-uniform bound
+      const int v = v0;
+      d3 acc0 = mk3(0, 0, 0), acc1 = mk3(0, 0, 0);
+      if (v < A.nv) {
+        const Bcsr& E = M.el;
+        if (M.hv) {
+          const int a0 = __ldg(E.rowptr + v), a1 = __ldg(E.rowptr + v + 1);
+          const int2* ch = reinterpret_cast<const int2*>(M.hix);
+          for (int k = a0 + sub; k < a1; k += 8) {
+            const int2 c = __ldg(ch + k);
+            acc0 = acc0 + half_bmv(c.y, M.hv, M.hn, ldcg3(A.z, c.x) + beta * ldcg3(p_old, c.x));
+          }
+        } else {
+          const int a0 = __ldg(E.rowptr + v), a1 = __ldg(E.rowptr + v + 1);
+          for (int k = a0 + sub; k < a1; k += 8) {
+            const int j = __ldg(E.cols + k);
+            acc0 = acc0 + bmv_ro(E, k, ldcg3(A.z, j) + beta * ldcg3(p_old, j));
+          }
+        }
+      }
+      d3 acc = acc0 + acc1;
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+      }
+      if (sub == 0 && v < A.nv) {
+        const d3 m = ld3(A.mask, v);
+        const d3 pv = ldcg3(A.z, v) + beta * ldcg3(p_old, v);
+        if (M.shift != 0) acc = acc + M.shift * pv;
+        const d3 y = mk3(m.x * acc.x, m.y * acc.y, m.z * acc.z);
+        __stcg(A.q + 3 * (int64_t)v, y.x);
+        __stcg(A.q + 3 * (int64_t)v + 1, y.y);
+        __stcg(A.q + 3 * (int64_t)v + 2, y.z);
+        __stcg(p_new + 3 * (int64_t)v, pv.x);
+        __stcg(p_new + 3 * (int64_t)v + 1, pv.y);
+        __stcg(p_new + 3 * (int64_t)v + 2, pv.z);
+        pq += dot(pv, y);
+      }
+    }
+    {
+      double v1[1] = {pq};
+      coop_cta_sum<1>(v1, reinterpret_cast<double(*)[1]>(sh));
+      if (t == 0) __stcg(A.part + b, v1[0]);
+    }
+    grid.sync();
+    pq = 0;
+    for (int i = 0; i < G; ++i) pq += __ldcg(A.part + i);
+    const double alpha = pq != 0 ? rz / pq : 0.0;
+    // B: per aggregate: update, smoother, restriction
+    double rzs = 0, rrs = 0;
+    for (int a = b; a < A.n_agg; a += G) {
+      double acc[6] = {0, 0, 0, 0, 0, 0};
+      const int e1 = __ldg(A.agg_off + a + 1);
+      for (int e = __ldg(A.agg_off + a) + t; e < e1; e += kCoopThreads) {
+        const int v = __ldg(A.agg_verts + e);
+        const d3 xv = ldcg3(A.x, v) + alpha * ldcg3(p_new, v);
+        const d3 rv = ldcg3(r_in, v) - alpha * ldcg3(A.q, v);
+        const int pp = __ldg(A.pair + v);
+        const d3 rp = pp < 0 ? mk3(0, 0, 0) : ldcg3(r_in, pp) - alpha * ldcg3(A.q, pp);
+        const d3 zv = pair_apply(A.minv2, v, rv, rp);
+        __stcg(A.x + 3 * (int64_t)v, xv.x);
+        __stcg(A.x + 3 * (int64_t)v + 1, xv.y);
+        __stcg(A.x + 3 * (int64_t)v + 2, xv.z);
+        __stcg(r_out + 3 * (int64_t)v, rv.x);
+        __stcg(r_out + 3 * (int64_t)v + 1, rv.y);
+        __stcg(r_out + 3 * (int64_t)v + 2, rv.z);
+        __stcg(A.z + 3 * (int64_t)v, zv.x);
+        __stcg(A.z + 3 * (int64_t)v + 1, zv.y);
+        __stcg(A.z + 3 * (int64_t)v + 2, zv.z);
+        const d3 m = ld3(A.mask, v);
+        const d3 mr = mk3(m.x * rv.x, m.y * rv.y, m.z * rv.z);
+        const d3 w = cross(ld3(A.dvec, v), mr);
+        acc[0] += mr.x;
+        acc[1] += mr.y;
+        acc[2] += mr.z;
+        acc[3] += w.x;
+        acc[4] += w.y;
+        acc[5] += w.z;
+        rzs += dot(rv, zv);
+        rrs += dot(rv, rv);
+      }
+      coop_cta_sum<6>(acc, reinterpret_cast<double(*)[6]>(sh));
+      if (t == 0)
+        for (int k = 0; k < 6; ++k) __stcg(A.s + 6 * a + k, acc[k] * __ldg(A.scale + 6 * a + k));
+    }
+    {
+      double v2[2] = {rzs, rrs};
+      coop_cta_sum<2>(v2, reinterpret_cast<double(*)[2]>(sh));
+      if (t == 0) {
+        __stcg(A.part + kCoopMaxCtas + b, v2[0]);
+        __stcg(A.part + 2 * kCoopMaxCtas + b, v2[1]);
+      }
+    }
+    grid.sync();
+    // C: coarse rows of the CTA's aggregates, prolongation, s.y
+    double sy = 0;
+    for (int a = b; a < A.n_agg; a += G) {
+      double acc[6] = {0, 0, 0, 0, 0, 0};
+      const double* rows = A.inv + (int64_t)(6 * a) * A.n_pad;
+      for (int j = t; j < A.n_pad; j += kCoopThreads) {
+        const double sj = __ldcg(A.s + j);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) acc[k] += __ldg(rows + (int64_t)k * A.n_pad + j) * sj;
+      }
+      coop_cta_sum<6>(acc, reinterpret_cast<double(*)[6]>(sh));
+      if (t == 0) {
+        double syl = 0;
+        for (int k = 0; k < 6; ++k) {
+          const int i = 6 * a + k;
+          ya[k] = __ldg(A.scale + i) * acc[k];
+          syl += __ldcg(A.s + i) * acc[k];
+        }
+        sy += syl;
+      }
+      __syncthreads();
+      const d3 tt = mk3(ya[0], ya[1], ya[2]), om = mk3(ya[3], ya[4], ya[5]);
+      const int e1 = __ldg(A.agg_off + a + 1);
+      for (int e = __ldg(A.agg_off + a) + t; e < e1; e += kCoopThreads) {
+        const int v = __ldg(A.agg_verts + e);
+        const d3 u = tt + cross(om, ld3(A.dvec, v));
+        const d3 m = ld3(A.mask, v);
+        const d3 zv = ldcg3(A.z, v);
+        __stcg(A.z + 3 * (int64_t)v, zv.x + m.x * u.x);
+        __stcg(A.z + 3 * (int64_t)v + 1, zv.y + m.y * u.y);
+        __stcg(A.z + 3 * (int64_t)v + 2, zv.z + m.z * u.z);
+      }
+      __syncthreads();
+    }
+    if (t == 0) __stcg(A.part + 3 * kCoopMaxCtas + b, sy);
+    grid.sync();
+    double rzn = 0, rrn = 0, syt = 0;
+    for (int i = 0; i < G; ++i) {
+      rzn += __ldcg(A.part + kCoopMaxCtas + i);
+      rrn += __ldcg(A.part + 2 * kCoopMaxCtas + i);
+      syt += __ldcg(A.part + 3 * kCoopMaxCtas + i);
+    }
+    rzn += syt;
+    beta = rz != 0 ? rzn / rz : 0.0;
+    rz = rzn;
+    rr = rrn;
+    ++it;
+    if (!isfinite(rr) || !(rz > 0)) {
+      status = 1;
+      break;
+    }
+    if (A.drift_check && it % kDriftWindow == 0) {  // true residual ||mask .* (grad + (H + shift) x)||
+      double tr = 0;
+      for (int v0 = gt >> 3; v0 - (lane >> 3) < A.nv; v0 += nthreads >> 3) {
+        const int v = v0;
+        d3 acc = mk3(0, 0, 0);
+        if (v < A.nv) {
+          const Bcsr& E = M.el;
+          const int a0 = __ldg(E.rowptr + v), a1 = __ldg(E.rowptr + v + 1);
+          for (int k = a0 + sub; k < a1; k += 8) acc = acc + bmv_ro(E, k, ldcg3(A.x, __ldg(E.cols + k)));
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+          acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        }
+        if (sub == 0 && v < A.nv) {
+          const d3 m = ld3(A.mask, v), gg = ld3(A.grad, v), xv = ldcg3(A.x, v);
+          if (M.shift != 0) acc = acc + M.shift * xv;
+          const d3 e = mk3(m.x * (acc.x + gg.x), m.y * (acc.y + gg.y), m.z * (acc.z + gg.z));
+          tr += dot(e, e);
+        }
+      }
+      double v1[1] = {tr};
+      coop_cta_sum<1>(v1, reinterpret_cast<double(*)[1]>(sh));
+      if (t == 0) __stcg(A.part + b, v1[0]);
+      grid.sync();
+      tr = 0;
+      for (int i = 0; i < G; ++i) tr += __ldcg(A.part + i);
+      const double true_rel = sqrt(tr / bb), rec_rel = sqrt(rr / bb);
+      if (true_rel - rec_rel > A.drift_tol || (M.shift == 0 && true_rel > kDivergeRel)) {
+        status = 2;
+        break;
+      }
+      grid.sync();  // part reused by the next phase A
+    }
+    win_min = fmin(win_min, rr);
+    if (it % kStagWindowCoarse == 0) {
+      if (it >= 2 * kStagWindowCoarse && !(win_min < 0.5 * prev_min) && rr > 1e-8 * bb) break;  // stagnated
+      prev_min = fmin(prev_min, win_min);
+      win_min = INFINITY;
+    }
+  }
+  if (b == 0 && t == 0) {
+    A.scal[0] = rz;
+    A.scal[4] = rr;
+    A.scal[9] = (double)status;
+    A.scal[10] = (double)it;
+  }
+}
+
 // Block-Jacobi: Minv_v = inverse of the masked 3x3 diagonal block.
 // diagonal block of row v copied to d[9] (either layout); false if absent
 __device__ __forceinline__ bool get_diag(const Bcsr& A, int v, double* d) {
@@ -1140,6 +1430,7 @@ struct SystemImpl {
   double last_true_rel2 = 0, last_true_relinf = 0, true_rel2_max = 0, true_relinf_max = 0;
   int64_t n_linear_solves = 0, refinements = 0;
   int64_t drift_fails = 0;       // PCG solves failed early on a true/recursive residual gap (pcg_core)
+  DBuf<double> coop_part;        // per-CTA partial sums of k_pcg_coop
   double last_solve_shift = -1;  // shift / pattern generation of the last pcg_core call (refinement passes)
   int64_t last_solve_ops = -1;
   int64_t coarse_fallbacks = 0;  // batched: scene solves re-run with block-Jacobi after a failed two-level solve
@@ -1989,12 +2280,7 @@ void true_residual(SystemImpl& S, const MatSet& M) {
 
 // Block-Jacobi PCG on the masked system (chunks of iterations replayed as one
 // CUDA graph) for rhs = -mask .* gsrc. Returns iterations; solution in S.dx.
-constexpr int kDriftWindow = 256;
-constexpr double kDriftFail = 1e6;  // 100x the largest true/tolerance ratio refinement accepts (kRefineMaxDrift)
-// an unshifted solve whose true residual is this far above the rhs at a drift
-// check diverges along an unconstrained mode (singular system) -> fail now (a
-// regularized solve may pass through large residuals on its way down: exempt)
-constexpr double kDivergeRel = 10.0;
+
 
 int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift, const double* gsrc) {
   const int nv = S.nv();
@@ -2072,6 +2358,44 @@ int pcg_core(SystemImpl& S, double tol, int maxit, double* rel_out, double shift
     return 0;
   }
   const double target = tol * tol * bb;
+  // small two-level systems: the whole iteration loop in one cooperative launch
+  static const bool coop_on = !std::getenv("GMCP_PCG_COOP") || std::atoi(std::getenv("GMCP_PCG_COOP")) != 0;
+  if (coop_on && coarse && pairs && nv <= kCoopMaxRows && C.n_agg > 0) {
+    int sms = 0, occ = 0;
+    GMCP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, S.device));
+    GMCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_coop, kCoopThreads, 0));
+    const int G = std::min({C.n_agg, kCoopMaxCtas, std::max(1, occ) * sms});
+    S.coop_part.resize(4 * kCoopMaxCtas);
+    S.r2.resize(3 * (int64_t)nv);
+    CoopArgs ca{M, nv, S.mask_d.p, gsrc, S.minv2.p, S.pair_d.p, C.agg_off.p, C.agg_verts.p, C.dvec.p, C.scale.p,
+                C.inv, C.n_agg, C.n_pad, S.dx.p, S.r.p, S.r2.p, S.z.p, S.p.p, S.w.p, S.q.p, C.s.p, S.coop_part.p,
+                S.scal.p, tol * tol, maxit, gsrc == S.grad.p ? 1 : 0, kDriftFail * tol};
+    void* args[] = {&ca};
+    if (!S.ev0) {
+      GMCP_CUDA(cudaEventCreate(&S.ev0));
+      GMCP_CUDA(cudaEventCreate(&S.ev1));
+    }
+    GMCP_CUDA(cudaEventRecord(S.ev0, S.stream));
+    const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k_pcg_coop, G, kCoopThreads, args, 0, S.stream);
+    if (le == cudaSuccess) {
+      GMCP_CUDA(cudaEventRecord(S.ev1, S.stream));
+      ++S.launches;
+      double hc[11];
+      GMCP_CUDA(cudaMemcpyAsync(hc, S.scal.p, sizeof hc, cudaMemcpyDeviceToHost, S.stream));
+      S.sync();
+      float ems = 0;
+      GMCP_CUDA(cudaEventElapsedTime(&ems, S.ev0, S.ev1));
+      const int it = (int)hc[10];
+      S.pcg_ev_ms += ems;
+      S.pcg_ev_iters += it;
+      const int status = (int)hc[9];
+      if (status == 2) ++S.drift_fails;
+      *rel_out = status != 0 ? INFINITY : std::sqrt(hc[4] / bb);
+      GMCP_CUDA(cudaGetLastError());
+      return it;
+    }
+    (void)cudaGetLastError();  // not co-resident (shared SMs): the chunked path below
+  }
   const int chunk = 16;
   const int lanes = nv < kSmallRows ? 8 : 4;
   const int gsp = std::min(grid_for((int64_t)nv * lanes, kThreads), kBlocks);
