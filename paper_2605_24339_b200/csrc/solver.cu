@@ -1826,10 +1826,27 @@ void rebuild_pair(SystemImpl& S, PairRt& pr, const double* eps_ref_dev) {
   Ctx& c = *pr.c;
   S.u_valid = false;
   int64_t counts[3];
+  static const bool trace = std::getenv("GMCP_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  double tms[3];
+  auto lap = [&](int k) {
+    if (!trace) return;
+    S.sync();
+    const auto t1 = std::chrono::steady_clock::now();
+    tms[k] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t0 = t1;
+  };
+  const int64_t l0 = c.launches;
   run_broadphase(c, pr.params.detection_radius, counts);
+  lap(0);
   run_sampler(c, eps_ref_dev);
+  lap(1);
   c.plan.valid = false;
   build_assembly_plan(c);
+  lap(2);
+  if (trace)
+    std::fprintf(stderr, "[gmcp rebuild pair] broadphase %.2f sampler %.2f plan %.2f ms, %lld launches\n", tms[0],
+                 tms[1], tms[2], (long long)(c.launches - l0));
   pr.ref_pos.resize(S.n_dof);
   GMCP_CUDA(cudaMemcpyAsync(pr.ref_pos.p, S.x.p, S.n_dof * sizeof(double), cudaMemcpyDeviceToDevice, S.stream));
 }
