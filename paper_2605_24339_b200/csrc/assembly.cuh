@@ -95,7 +95,9 @@ constexpr int kLDS = kStage + 4;      // column stride (doubles): conflict-free 
 // Per-warp shared memory: staged U' / V rows (column-major); after the last
 // pass the same space holds C.
 constexpr int kLDT = 9;               // T tile row stride (doubles)
-struct RunSmem {
+constexpr int kPst = 2 * kUC * kLDS - kUC * (kUC + 1) - 16 * kLDT;  // what the staging tile leaves
+static_assert(kPst >= partial_size(kRunMasters), "run partial staging does not fit");
+struct alignas(16) RunSmem {
   union {
     struct {
       double u[kUC][kLDS];
@@ -104,6 +106,7 @@ struct RunSmem {
     struct {
       double C[kUC][kUC + 1];
       double T[16][kLDT];  // finalize: F C[0:8][0:8] rows, staged as DMMA A fragments
+      double Pst[kPst];    // finalize: the run partial, stored out coalesced
     };
   };
   double A[27];   // A_i with T_i(v) = A_i v: [i][row][col]
@@ -174,8 +177,8 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
           if (i < j || (i == j && a <= c)) {
             const int bid = i == 0 ? j : (i == 1 ? 2 + j : 5);
             const uint64_t clr = ~(0xffull << (8 * slot));
-            ss_off = (ss_off & clr) | ((uint64_t)(9 * bid + 3 * a + c) << (8 * slot));
-            if (i == j && a != c) ss_mir = (ss_mir & clr) | ((uint64_t)(9 * bid + 3 * c + a) << (8 * slot));
+            ss_off = (ss_off & clr) | ((uint64_t)(kSSBase + 12 * bid + 3 * a + c) << (8 * slot));
+            if (i == j && a != c) ss_mir = (ss_mir & clr) | ((uint64_t)(kSSBase + 12 * bid + 3 * c + a) << (8 * slot));
           }
         }
       }
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
   // persistent warps; the next run's metadata loads during this run
   struct Meta {
     int64_t s0, s1, pb;
-    int M, sid0, sid1, sid2, my_lm;
+    int M, sid0, sid1, sid2;
   };
   auto load_meta = [&](int64_t r, Meta& m) {
     m.s0 = run_off[r];
@@ -201,7 +204,6 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     m.sid1 = run_slave[3 * r + 1];
     m.sid2 = run_slave[3 * r + 2];
     m.pb = pbase[r];
-    m.my_lm = lane < m.M ? lm_ids[L0 + lane] : 0;
   };
   const int64_t stride = (int64_t)gridDim.x * kRunWarps;
   int64_t r = blockIdx.x * (int64_t)kRunWarps + (threadIdx.x >> 5);
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     load_meta(r, cur);
 #endif
     const int64_t s0 = cur.s0, s1 = cur.s1, pb = cur.pb;
-    const int M = cur.M, sid0 = cur.sid0, sid1 = cur.sid1, sid2 = cur.sid2, my_lm = cur.my_lm;
+    const int M = cur.M, sid0 = cur.sid0, sid1 = cur.sid1, sid2 = cur.sid2;
     {
       const d3 a0 = ld3(x, sid0), a1 = ld3(x, sid1), a2 = ld3(x, sid2);
       const d3 e1 = a1 - a0, e2 = a2 - a0;
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     C[8 + g][9 + 2 * t4] = d31;
     __syncwarp();
     double* P = partial + pb;
+    double* Q = Hess ? W.Pst : P;  // Hess: the partial is staged, then stored coalesced
     const int colF = 6 + M, colE = 7 + M;
     const double* A = W.A;
     const double* nn = W.geo + 15;
@@ -376,8 +379,8 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
         for (int e = 0; e < 2; ++e) {
           const int ia = 8 * mt + g, q = 8 * nt + 2 * t4 + e;
           if (ia < 9) {
-            if (q == colF) P[4 + ia] = t[mt][nt][e];  // [4 + 3 i + a]
-            else if (Hess && q >= 6 && q < colF) P[m_base(M) + 10 * (q - 6) + 1 + ia] = t[mt][nt][e];
+            if (q == colF) Q[4 + ia + ia / 3] = t[mt][nt][e];  // [4 + 4 i + a]
+            else if (Hess && q >= 6 && q < colF) Q[m_base(q - 6) + ia + ia / 3] = t[mt][nt][e];
           }
         }
     if (Hess) {
@@ -405,27 +408,22 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
           for (int e = 0; e < 2; ++e) {
             const int slot = 4 * mt + 2 * nt + e;
             const int o = (int)((ss_tab[0][lane] >> (8 * slot)) & 0xff), om = (int)((ss_tab[1][lane] >> (8 * slot)) & 0xff);
-            if (o != 0xff) P[kSSBase + o] = sv[mt][nt][e];
-            if (om != 0xff) P[kSSBase + om] = sv[mt][nt][e];
+            if (o != 0xff) Q[o] = sv[mt][nt][e];
+            if (om != 0xff) Q[om] = sv[mt][nt][e];
           }
       for (int tq = lane; tq < M * (M + 1) / 2; tq += 32) {  // master pairs, dense upper triangle
         const int pr = pair_tab[M][tq];
-        P[pair_base(M) + tq] = C[6 + (pr & 15)][6 + (pr >> 4)];
+        Q[pair_base(M) + tq] = C[6 + (pr & 15)][6 + (pr >> 4)];
       }
     }
     const double Erun = C[6 + M][colE];
-    if (lane < 4) P[lane] = lane == 0 ? Erun : nn[lane - 1];
-    if (lane < M) {
-      P[kHdr + lane] = (double)my_lm;  // header: local master ids
-      P[m_base(M) + 10 * lane] = C[6 + lane][colF];  // s_m
-    } else if (lane == 28) {
-      P[kSlv] = (double)sid0;
-    } else if (lane == 29) {
-      P[kSlv + 1] = (double)sid1;
-    } else if (lane == 30) {
-      P[kSlv + 2] = (double)sid2;
-    } else if (lane == 31) {
-      P[kMcnt] = (double)M;
+    if (lane < 4) Q[lane] = lane == 3 ? Erun : nn[lane];
+    if (lane < M) Q[m_base(lane) + 3] = C[6 + lane][colF];  // s_m
+    if (Hess) {  // 16-byte chunks, consecutive lanes on consecutive chunks
+      __syncwarp();
+      const int nch = partial_size(M) / 2;
+      for (int q = lane; q < nch; q += 32)
+        reinterpret_cast<double2*>(P)[q] = reinterpret_cast<const double2*>(W.Pst)[q];
     }
     e_warp += Erun;
     __syncwarp();
@@ -443,42 +441,40 @@ __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
 // role < 3: slave vertex i of the run, else local master role - 3; b indexes
 // the run's columns the same way.
 
-// Block (role, b) of a run partial P.
+// Block (role, b) of a run partial P; every group read is one 256-bit load.
 __device__ __forceinline__ void contrib_block(int role, int b, const double* __restrict__ P, int M, double* blk) {
   if (role < 3 && b < 3) {  // SS: upper blocks stored, lower = transpose
     const int lo = min(role, b), hi = max(role, b);
     const int bid = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
-    const double* Sb = P + kSSBase + 9 * bid;
+    const double* Sb = P + kSSBase + 12 * bid;
+    double sb[9];
+    ldg4(Sb, sb[0], sb[1], sb[2], sb[3]);
+    ldg4(Sb + 4, sb[4], sb[5], sb[6], sb[7]);
+    sb[8] = __ldg(Sb + 8);
     if (role <= b) {
 #pragma unroll
-      for (int q = 0; q < 9; ++q) blk[q] = Sb[q];
+      for (int q = 0; q < 9; ++q) blk[q] = sb[q];
     } else {
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) blk[3 * a + c] = Sb[3 * c + a];
+        for (int c = 0; c < 3; ++c) blk[3 * a + c] = sb[3 * c + a];
     }
     return;
   }
-  const double nn[3] = {P[1], P[2], P[3]};
-  if (role < 3) {  // SM(i, m) = a_{m,i} n^T
-    const double* A = P + m_base(M) + 10 * (b - 3) + 1 + 3 * role;
+  double nn[3], e_;
+  ldg4(P, nn[0], nn[1], nn[2], e_);
+  if (role < 3 || b < 3) {  // SM(i, m) = a_{m,i} n^T, MS(m, i) = n a_{m,i}^T
+    const bool sm = role < 3;
+    double A[3], w_;
+    ldg4(P + m_base(sm ? b - 3 : role - 3) + 4 * (sm ? role : b), A[0], A[1], A[2], w_);
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) blk[3 * a + c] = A[a] * nn[c];
+      for (int c = 0; c < 3; ++c) blk[3 * a + c] = sm ? A[a] * nn[c] : nn[a] * A[c];
     return;
   }
-  const int m = role - 3;
-  if (b < 3) {  // MS(m, i) = n a_{m,i}^T
-    const double* A = P + m_base(M) + 10 * m + 1 + 3 * b;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) blk[3 * a + c] = nn[a] * A[c];
-    return;
-  }
-  const int l = b - 3;  // MM(m, l) = c_ml n n^T
+  const int m = role - 3, l = b - 3;  // MM(m, l) = c_ml n n^T
   const double cv = P[pair_base(M) + (m <= l ? tri_index(m, l, M) : tri_index(l, m, M))];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
@@ -547,11 +543,17 @@ __global__ void __launch_bounds__(kGatherThreads, K8_MINB) k_gather(int64_t nnzb
       for (int e = ent_off[v]; e < e1; ++e) {
         const int64_t en = ent[e];
         const double* P = partial + (en >> 12);
-        const int role = (int)(en & 0xff), M = (int)((en >> 8) & 0xf);
-        if (role < 3)
-          g = g + mk3(P[4 + 3 * role], P[5 + 3 * role], P[6 + 3 * role]);
-        else
-          g = g + P[m_base(M) + 10 * (role - 3)] * mk3(P[1], P[2], P[3]);
+        const int role = (int)(en & 0xff);
+        double v0, v1, v2, v3;
+        if (role < 3) {
+          ldg4(P + 4 + 4 * role, v0, v1, v2, v3);
+          g = g + mk3(v0, v1, v2);
+        } else {
+          double n0, n1, n2, e_;
+          ldg4(P, n0, n1, n2, e_);
+          ldg4(P + m_base(role - 3), v0, v1, v2, v3);
+          g = g + v3 * mk3(n0, n1, n2);
+        }
       }
       grad[3 * v] = g.x;
       grad[3 * v + 1] = g.y;

@@ -181,6 +181,10 @@ __device__ __forceinline__ d3 ld3(const double* __restrict__ x, int v) {
   const double* p = x + 3 * (int64_t)v;
   return d3{__ldg(p), __ldg(p + 1), __ldg(p + 2)};
 }
+// one 256-bit read-only load of a 32-byte aligned group of four doubles
+__device__ __forceinline__ void ldg4(const double* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
 __device__ __forceinline__ d3 ld3nc(const double* x, int v) {
   const double* p = x + 3 * (int64_t)v;
   return d3{p[0], p[1], p[2]};

@@ -178,9 +178,6 @@ __device__ __forceinline__ d3 bmv_ro(const Bcsr& A, int64_t k, d3 p) {
 // blocks in flight per lane (fixed order: deterministic)
 // block k of the symmetric-half operand times p: H_vj for j >= v, else the
 // transpose of the stored block (j, v)
-__device__ __forceinline__ void ldg4(const double* p, double& a, double& b, double& c, double& d) {
-  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
-}
 __device__ __forceinline__ d3 half_bmv(int raw, const double* __restrict__ hv, int64_t nh, d3 p) {
   const bool lower = raw < 0;
   const int64_t idx = lower ? ~raw : raw;
