@@ -141,7 +141,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 template <bool Hess>
 __global__ void __launch_bounds__(32 * kRunWarps, K7_MINB) k_run_partials(
     DevSamples S, const double* __restrict__ x, int64_t n_runs, const int64_t* __restrict__ run_off,
-    const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm_off, const int32_t* __restrict__ lm_ids,
+    const int32_t* __restrict__ run_slave, const int32_t* __restrict__ lm_off,
     const uint32_t* __restrict__ li4, const int64_t* __restrict__ pbase, double* __restrict__ partial,
     unsigned long long* __restrict__ red, double* __restrict__ warp_energy) {
   __shared__ RunSmem wsm[kRunWarps];

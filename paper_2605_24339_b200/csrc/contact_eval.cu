@@ -42,11 +42,11 @@ int launch_k7(Ctx& c, int mode) {
   double* we = c.red_d.p + kWarpE;
   if (mode == 1)
     k_run_partials<true><<<gb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
-                                                              P.lm_off.p, P.lm_ids.p, P.li4.p, P.pbase.p,
+                                                              P.lm_off.p, P.li4.p, P.pbase.p,
                                                               P.partial.p, c.red_u.p, we);
   else
     k_run_partials<false><<<gb, 32 * kRunWarps, 0, c.stream>>>(S, c.X(), P.n_runs, P.run_off.p, P.run_slave.p,
-                                                               P.lm_off.p, P.lm_ids.p, P.li4.p, P.pbase.p,
+                                                               P.lm_off.p, P.li4.p, P.pbase.p,
                                                                P.partial.p, c.red_u.p, we);
   ++c.launches;
   return gb * kRunWarps;
