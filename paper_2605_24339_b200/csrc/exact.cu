@@ -18,7 +18,7 @@ namespace {
 // red_u[0] = first non-positive gap index, red_u[1] = first degenerate index,
 // red_u[2] = ord_bits(min gap). Samples i >= limit are skipped.
 
-__global__ void __launch_bounds__(kRedThreads) k_energy(DevSamples S, const double* __restrict__ x, int64_t limit,
+__global__ void __launch_bounds__(kRedThreads, 4) k_energy(DevSamples S, const double* __restrict__ x, int64_t limit,
                                                          double* __restrict__ parts, unsigned long long* red) {
   __shared__ double sh[kRedThreads / 32];
   double e = 0;
@@ -127,7 +127,7 @@ __global__ void k_kinematics(DevSamples S, const double* __restrict__ x, double*
 
 
 // red[0] = ord_bits(alpha), red[1] = first degenerate index
-__global__ void k_step_filter(DevSamples S, const double* __restrict__ x, const double* __restrict__ dx,
+__global__ void __launch_bounds__(256, 3) k_step_filter(DevSamples S, const double* __restrict__ x, const double* __restrict__ dx,
                               unsigned long long* red) {
   unsigned long long best = ord_bits(1.0), deg = ~0ull;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S.n; i += (int64_t)gridDim.x * blockDim.x) {
