@@ -489,8 +489,11 @@ constexpr int kGatherThreads = 256;
 #ifndef K8_MINB
 #define K8_MINB 5  // 48 registers, 40 warps/SM: more loads in flight (pass -3%; 6 and 8 spill)
 #endif
+#ifndef K8_BLOCKS_MINB
+#define K8_BLOCKS_MINB 5  // blocks-only gather (host-buffer path): 48 registers + 24 B of spills; 4 (62, no spills) is 2% slower end to end
+#endif
 template <bool Hess, bool Rows = true>
-__global__ void __launch_bounds__(kGatherThreads, K8_MINB) k_gather(int64_t nnzb, int32_t n_rows,
+__global__ void __launch_bounds__(kGatherThreads, Rows ? K8_MINB : K8_BLOCKS_MINB) k_gather(int64_t nnzb, int32_t n_rows,
                                                            const int32_t* __restrict__ blk_off,
                                                            const int64_t* __restrict__ contrib,
                                                            double* __restrict__ vals,
